@@ -1,0 +1,232 @@
+/*
+ * fusionb200 -- C-ABI of the B200-native Coherent-Fusion pose-scoring path.
+ *
+ * Replaces, for the hot path only, the reference package `fusionscreen`
+ * (/root/reference/pkg/src/fusionscreen).  Each entry point names the
+ * reference interface it stands in for.  The reference is pure Python, so
+ * its "FFI" is the Python operator/plugin API; the binding a maintainer adds
+ * is the ctypes layer in INTEGRATION.md (our own package binds it the same
+ * way in paper_2104_04547_b200/_native.py).
+ *
+ * Conventions
+ *   - C types only; no exceptions cross the ABI; every function returns an
+ *     int status (FS_OK == 0, negative on error, see fs_strerror()).
+ *   - Every array argument is a CALLER-OWNED DEVICE pointer unless the
+ *     parameter name starts with `host_`.  The library never allocates or
+ *     frees caller memory; scratch comes from a caller-provided workspace
+ *     sized by fs_workspace_bytes().
+ *   - Every launch takes a cudaStream_t (passed as void*) and is
+ *     stream-ordered and asynchronous.  No call synchronises the device.
+ *   - Reentrant: no mutable globals; a packed weight blob is immutable, so
+ *     several host threads may score concurrently on separate streams
+ *     (SPEC.md:298 -- frozen models are safe for concurrent prediction).
+ *   - Per-pose item failures are reported in an int32 err[P] bit mask and
+ *     never abort the batch (models.py:470-498 contract).
+ */
+#ifndef FUSIONB200_H
+#define FUSIONB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ----------------------------------------------------- */
+#define FS_OK         0
+#define FS_EINVAL    -1   /* bad argument (ValueError in the reference)   */
+#define FS_ECAPACITY -2   /* workspace / per-pose size limit exceeded      */
+#define FS_ECUDA     -3   /* CUDA runtime error                            */
+#define FS_ENOTSUP   -4   /* configuration not supported by this precision */
+
+/* ---- per-pose error bits (int32 err[P]) -------------------------------- */
+#define FS_ERR_ROLE       1  /* role not in {PROTEIN=0, LIGAND=1}           */
+#define FS_ERR_NAN        2  /* NaN coordinate (voxelize raises, :180-183)  */
+#define FS_ERR_NONFINITE  4  /* +-inf/NaN coordinate -> non-finite features */
+#define FS_ERR_EDGE_CAP   8  /* CSR workspace overflow: retry, larger cap   */
+#define FS_ERR_TOO_LARGE 16  /* pose exceeds FS_MAX_POSE_ATOMS              */
+#define FS_ERR_GRID_NONFINITE 32  /* given voxel grid has inf/NaN (models.py:521-522) */
+#define FS_ERR_FEAT_NONFINITE 64  /* given node features have inf/NaN (:527-528)   */
+
+#define FS_MAX_POSE_ATOMS 4096
+
+/* ---- precision of the scoring path ------------------------------------ */
+#define FS_PREC_FP32 0  /* FFMA fp32 everywhere: reference within 1e-3 rel   */
+#define FS_PREC_BF16 1  /* tcgen05 bf16 Conv3d (fp32 accumulate), fp32 rest  */
+
+/* ---- grid layouts ------------------------------------------------------ */
+#define FS_GRID_NCDHW_F64  0  /* reference VoxelGrid.occupancy [C,G,G,G] f64 */
+#define FS_GRID_NDHWC_F32  1  /* conv input, fp32, channels innermost        */
+#define FS_GRID_NDHWC_BF16 2  /* conv input, bf16, channels innermost        */
+
+/* A batch of poses.  Pose p's nodes are: the pocket atoms of target
+ * pose_target[p] (if pose_target != NULL and pose_target[p] >= 0), followed
+ * by atoms atom_off[p] .. atom_off[p+1]-1.  This is exactly the reference's
+ * `np.vstack([prot, lig])` node order (complexes.py:114-118) when the pocket
+ * holds the protein atoms; a plain SyntheticComplex is a pose with no pocket.
+ * Coordinates are float64 [n,3] (complexes.py:74); elements and roles int32. */
+typedef struct {
+  const double*  pocket_xyz;
+  const int32_t* pocket_elem;
+  const int32_t* pocket_role;
+  const int64_t* pocket_off;   /* [n_pockets+1] */
+  int32_t        n_pockets;
+  const double*  atom_xyz;
+  const int32_t* atom_elem;
+  const int32_t* atom_role;
+  const int64_t* atom_off;     /* [n_poses+1] */
+  const int32_t* pose_target;  /* [n_poses] or NULL */
+  int32_t        n_poses;
+  int32_t        max_pose_atoms; /* upper bound on nodes of any pose (host-known) */
+} fs_pose_batch;
+
+/* Model configuration: the union of VoxelHeadConfig (models.py:40-63),
+ * GraphHeadConfig (:66-93) and FusionConfig (:96-118) fields that affect
+ * inference, plus the featurizer box size (models.py:638-642). */
+typedef struct {
+  int32_t grid_extent, in_channels, conv_filters_1, conv_filters_2;
+  int32_t dense_nodes, kernel_1, kernel_2;
+  int32_t residual_1, residual_2, batch_norm;
+  int32_t c_elem, k_cov, k_noncov, gather_width_cov, gather_width_noncov;
+  double  cov_thresh, noncov_thresh, box_size;
+  int32_t fusion_mode;          /* 0 late, 1 mid, 2 coherent               */
+  int32_t n_fusion_layers, model_specific_layers, residual_fusion;
+  int32_t activation;           /* 0 relu, 1 leaky-relu, 2 selu            */
+  int32_t fusion_dense_nodes;
+} fs_model_desc;
+
+#define FS_MODE_LATE 0
+#define FS_MODE_MID 1
+#define FS_MODE_COHERENT 2
+
+/* Packed device weight blob (immutable after fs_pack_weights).  Holds fp32
+ * copies in kernel layouts plus bf16 UMMA-layout conv weights. */
+typedef struct fs_model fs_model;
+
+/* ---- library ------------------------------------------------------------ */
+const char* fs_strerror(int code);
+int fs_version(void);
+/* Last CUDA error string seen by this thread (diagnostics). */
+const char* fs_last_cuda_error(void);
+
+/* ---- weights (FusionModel.__init__/load -> device) ---------------------- */
+/* Replaces FusionModel parameter binding (models.py:263-278, :441-467).
+ * host_names/host_params: the reference parameter dict flattened as
+ * "voxel/<name>", "graph/<name>", "fusion/<name>" (models.py:532-539), fp64,
+ * shapes as in init_*_params (models.py:150-218).  Optional BN running stats
+ * "voxel/bn1_mean", "voxel/bn1_var", "voxel/bn2_mean", "voxel/bn2_var".
+ * Creates a host handle; device memory is the caller's `dev_blob` of
+ * fs_weights_bytes() bytes, filled asynchronously on `stream`. */
+size_t fs_weights_bytes(const fs_model_desc* desc);
+int fs_model_create(const fs_model_desc* desc, const char* const* host_names,
+                    const double* const* host_params, int n_params,
+                    void* dev_blob, size_t blob_bytes, void* stream,
+                    fs_model** out);
+int fs_model_destroy(fs_model* m);
+/* 1 if `precision` is implemented for this model's configuration. */
+int fs_model_supports(const fs_model* m, int precision);
+
+/* ---- featurizer (complexes.py:171-254) --------------------------------- */
+/* node_off[P+1] (int64) of a pose batch; required by the graph calls. */
+int fs_node_offsets(const fs_pose_batch* b, int64_t* node_off, void* ws,
+                    size_t ws_bytes, void* stream);
+size_t fs_node_offsets_ws_bytes(int32_t n_poses);
+
+/* voxelize (complexes.py:171-184) for every pose; `out` layout per
+ * FS_GRID_*; err[p] |= FS_ERR_ROLE / FS_ERR_NAN.  Output is overwritten. */
+int fs_voxelize(const fs_pose_batch* b, int32_t extent, int32_t c_elem,
+                double box_size, int32_t layout, void* out, int32_t* err,
+                void* stream);
+
+/* Node features [onehot(clip elem) | role | pos/box+0.5] (complexes.py:233-236),
+ * float64 [N, c_elem+4]. */
+int fs_node_features(const fs_pose_batch* b, const int64_t* node_off,
+                     int32_t c_elem, double box_size, double* out, void* stream);
+
+/* Radius graph (complexes.py:237-246), two passes.
+ * count: deg_cov/deg_ncov [N] = per-node degrees of the symmetric adjacency.
+ * fill:  CSR rows row_cov/row_ncov [N+1] (int64, global entry offsets) are
+ *        produced by fs_graph_rows; col_* hold POSE-LOCAL neighbour ids,
+ *        each row sorted ascending; dist_* (nullable) the float64 distances.
+ * Predicate (exact, float64, no FMA): d2 = (dx*dx+dy*dy)+dz*dz;
+ *   edge iff d2 <= rmax*rmax and sqrt(d2) <= t_role (rmax = max(t_cov,t_ncov)). */
+int fs_graph_count(const fs_pose_batch* b, const int64_t* node_off,
+                   double cov_thresh, double noncov_thresh,
+                   int32_t* deg_cov, int32_t* deg_ncov, int32_t* err,
+                   void* stream);
+int fs_graph_rows(const int32_t* deg, int64_t n_nodes, int64_t* row_ptr,
+                  void* ws, size_t ws_bytes, void* stream);
+size_t fs_graph_rows_ws_bytes(int64_t n_nodes);
+int fs_graph_fill(const fs_pose_batch* b, const int64_t* node_off,
+                  double cov_thresh, double noncov_thresh,
+                  const int64_t* row_cov, const int64_t* row_ncov,
+                  int32_t* col_cov, int32_t* col_ncov,
+                  double* dist_cov, double* dist_ncov,
+                  int64_t cap_cov, int64_t cap_ncov, int32_t* err, void* stream);
+/* Extract the i<j edge list (lexsorted) of one CSR: edges [E,2] (pose-local
+ * node ids, int64) and dists.  `edge_off` [P+1] int64 from fs_graph_edge_counts. */
+int fs_graph_edge_counts(const int64_t* node_off, int32_t n_poses,
+                         const int64_t* row_ptr, const int32_t* col,
+                         int64_t* edge_off, void* ws, size_t ws_bytes,
+                         void* stream);
+int fs_graph_edges(const int64_t* node_off, int32_t n_poses,
+                   const int64_t* row_ptr, const int32_t* col, const double* dist,
+                   const int64_t* edge_off, int64_t* edges, double* dists,
+                   void* stream);
+
+/* ---- scoring (FusionModel.predict_batch, models.py:470-498) ------------ */
+/* Workspace for fs_score_poses / fs_score_features. */
+size_t fs_workspace_bytes(const fs_model* m, int32_t max_poses,
+                          int64_t max_nodes, int64_t max_edges, int precision);
+
+/* Fused featurize + 3D-CNN + SG-CNN + fusion for raw poses (the screening
+ * path: models.featurize (:638-651) then predict_batch).  Outputs (nullable
+ * except scores) are float32 device arrays: scores[P], lat_v[P,latent_v],
+ * lat_g[P,latent_g], pred_v[P], pred_g[P].  err[P] bit mask; poses with
+ * err != 0 get NaN score.  max_edges bounds the directed CSR entries of the
+ * whole batch per edge type; overflow sets FS_ERR_EDGE_CAP (host retries). */
+int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b,
+                   int64_t max_edges, void* ws, size_t ws_bytes,
+                   float* scores, float* lat_v, float* lat_g, float* pred_v,
+                   float* pred_g, int32_t* err, void* stream);
+
+/* Pre-featurized batch: the drop-in predict_batch / voxel_head_forward /
+ * graph_head_forward path.  grids: float64 [P,C,G,G,G] (VoxelGrid layout,
+ * nullable when only the graph head is wanted); feats: float64
+ * [N, c_elem+4]; node_off [P+1]; edges given as i<j pairs with GLOBAL node
+ * ids (int64 [E,2]) per edge type.  heads: bit0 voxel head, bit1 graph head,
+ * bit2 fusion. */
+int fs_score_features(const fs_model* m, int precision, int32_t n_poses,
+                      const double* grids, const double* feats,
+                      const int64_t* node_off, int64_t n_nodes,
+                      const int64_t* cov_edges, int64_t n_cov,
+                      const int64_t* ncov_edges, int64_t n_ncov, int32_t heads,
+                      void* ws, size_t ws_bytes, float* scores, float* lat_v,
+                      float* lat_g, float* pred_v, float* pred_g, int32_t* err,
+                      void* stream);
+
+/* ---- ranking (top-k merge; tie rule of evaluate.py:67-83) -------------- */
+/* Sorts the concatenation of (a) and (b) by (score desc, index asc) and keeps
+ * the first k into (out_scores, out_idx).  NaN scores rank last.  Indices
+ * must be < 2^32.  Either input may be empty. */
+size_t fs_topk_ws_bytes(int64_t n);
+int fs_topk_merge(const float* a_scores, const int64_t* a_idx, int64_t na,
+                  const float* b_scores, const int64_t* b_idx, int64_t nb,
+                  int32_t k, float* out_scores, int64_t* out_idx, void* ws,
+                  size_t ws_bytes, void* stream);
+
+/* Per-compound best pose (evaluate.aggregate_best_pose, :67-83) on device:
+ * compound[n] int64 ids in [0, n_compounds) (runs need not be contiguous),
+ * pose_id[n] (< 2^32); direction +1 max / -1 min.  best_idx[n_compounds] =
+ * winning row (-1 if the compound has no rows); best_key[n_compounds] is
+ * caller scratch. */
+int fs_best_pose(const int64_t* compound, const int64_t* pose_id,
+                 const float* scores, int64_t n, int64_t n_compounds,
+                 int32_t direction, int64_t* best_idx, uint64_t* best_key,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FUSIONB200_H */

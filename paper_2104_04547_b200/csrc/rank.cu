@@ -1,0 +1,109 @@
+// Ranking kernels: top-k merge and per-compound best pose.
+//
+// Tie rule of evaluate.aggregate_best_pose (evaluate.py:67-83): higher score
+// first, ties to the lowest pose id.  The reference has no top-k; ranking the
+// whole library by (score desc, global pose index asc) is the natural
+// extension the multi-GPU merge needs.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace fs {
+
+// Monotone map: ascending key <=> (score descending); NaN last; -0 == +0.
+__device__ __forceinline__ uint32_t score_desc_bits(float s) {
+  if (isnan(s)) return 0xffffffffu;
+  if (s == 0.0f) s = 0.0f;
+  uint32_t u = __float_as_uint(s);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);   // ascending float order
+  return ~u;                                         // descending
+}
+
+__device__ __forceinline__ float score_from_bits(uint32_t k) {
+  if (k == 0xffffffffu) return __int_as_float(0x7fc00000);
+  uint32_t u = ~k;
+  u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+  return __uint_as_float(u);
+}
+
+__global__ void topk_keys_kernel(const float* as, const int64_t* ai, int64_t na, const float* bs,
+                                 const int64_t* bi, int64_t nb, uint64_t* keys) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= na + nb) return;
+  float s; int64_t i;
+  if (t < na) { s = as[t]; i = ai[t]; } else { s = bs[t - na]; i = bi[t - na]; }
+  keys[t] = ((uint64_t)score_desc_bits(s) << 32) | (uint64_t)(uint32_t)i;
+}
+
+__global__ void topk_decode_kernel(const uint64_t* keys, int64_t k, float* os, int64_t* oi) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  uint64_t key = keys[t];
+  os[t] = score_from_bits((uint32_t)(key >> 32));
+  oi[t] = (int64_t)(uint32_t)key;
+}
+
+size_t topk_ws_bytes(int64_t n) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n);
+  return tmp + 2 * (size_t)n * 8 + 512;
+}
+
+int launch_topk_merge(const float* as, const int64_t* ai, int64_t na, const float* bs,
+                      const int64_t* bi, int64_t nb, int k, float* os, int64_t* oi, void* ws,
+                      size_t ws_bytes, cudaStream_t st) {
+  const int64_t n = na + nb;
+  if (k < 0) return FS_EINVAL;
+  if (n == 0 || k == 0) return FS_OK;
+  if ((size_t)topk_ws_bytes(n) > ws_bytes) return FS_ECAPACITY;
+  char* w = (char*)ws;
+  uint64_t* keys_in = (uint64_t*)w;
+  uint64_t* keys_out = keys_in + n;
+  void* tmp = (void*)(((uintptr_t)(keys_out + n) + 255) & ~(uintptr_t)255);
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys_in, keys_out, (int)n, 0, 64, st);
+  topk_keys_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(as, ai, na, bs, bi, nb, keys_in);
+  FS_LAUNCH_CHECK();
+  FS_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys_in, keys_out, (int)n, 0, 64, st));
+  const int64_t kk = k < n ? k : n;
+  topk_decode_kernel<<<(unsigned)cdiv(kk, 256), 256, 0, st>>>(keys_out, kk, os, oi);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
+// best pose per compound: key = (score-order bits, pose id) min-reduced.
+__global__ void best_key_kernel(const int64_t* compound, const int64_t* pose_id, const float* s,
+                                int64_t n, int dir, unsigned long long* best) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  float v = dir > 0 ? s[t] : -s[t];
+  unsigned long long key = ((unsigned long long)score_desc_bits(v) << 32) | (uint32_t)pose_id[t];
+  atomicMin(&best[compound[t]], key);
+}
+
+__global__ void best_idx_kernel(const int64_t* compound, const int64_t* pose_id, const float* s,
+                                int64_t n, int dir, const unsigned long long* best, int64_t* idx) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  float v = dir > 0 ? s[t] : -s[t];
+  unsigned long long key = ((unsigned long long)score_desc_bits(v) << 32) | (uint32_t)pose_id[t];
+  if (key == best[compound[t]]) atomicMin((unsigned long long*)&idx[compound[t]], (unsigned long long)t);
+}
+
+int launch_best_pose(const int64_t* compound, const int64_t* pose_id, const float* s, int64_t n,
+                     int64_t n_compounds, int dir, int64_t* best_idx, uint64_t* best_key,
+                     cudaStream_t st) {
+  if (dir != 1 && dir != -1) return FS_EINVAL;
+  if (n_compounds <= 0) return FS_OK;
+  // all-ones: the unsigned atomicMin sentinel, and -1 (no rows) as int64
+  FS_CUDA_CHECK(cudaMemsetAsync(best_idx, 0xff, sizeof(int64_t) * n_compounds, st));
+  unsigned long long* keys = (unsigned long long*)best_key;
+  FS_CUDA_CHECK(cudaMemsetAsync(keys, 0xff, sizeof(unsigned long long) * n_compounds, st));
+  best_key_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(compound, pose_id, s, n, dir, keys);
+  FS_LAUNCH_CHECK();
+  best_idx_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(compound, pose_id, s, n, dir, keys, best_idx);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
+}  // namespace fs

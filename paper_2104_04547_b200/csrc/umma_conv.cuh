@@ -1,0 +1,28 @@
+// tcgen05 (UMMA) implicit-GEMM Conv3d chain for the default voxel head
+// (bf16 operands, fp32 accumulation in TMEM).  See umma_conv.cu.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "../../include/fusionb200.h"
+
+namespace fs {
+namespace umma {
+
+// True if the voxel-head configuration matches the specialised kernels
+// (G=16, Cin=8, filters 32/64, kernels 5/3, residual_2 only, no BN).
+bool supports(const fs_model_desc& d);
+size_t weights_bytes(const fs_model_desc& d);
+// Pack reference fp64 conv weights [O][C][k][k][k] into the UMMA blob.
+void pack_weights(const fs_model_desc& d, const double* c1, const double* c2, const double* c3,
+                  const double* c4, char* out);
+size_t workspace_bytes(const fs_model_desc& d, int64_t n_poses);
+// grid: [P][G][G][G][Cin] bf16 -> pooled conv4 output [P][(G/4)^3][f2] fp32
+// (NDHWC flatten order, ready for dense1).
+int voxel_convs(const fs_model_desc& d, const char* wblob, const float* b1, const float* b2,
+                const float* b3, const float* b4, int n_poses, const __nv_bfloat16* grid, char* ws,
+                float* flat_out, cudaStream_t st);
+
+}  // namespace umma
+}  // namespace fs

@@ -1,0 +1,494 @@
+"""Drop-in model API of ``fusionscreen.models`` for the pose-scoring path.
+
+Same configs, presets, parameter initialisation (draw order), checkpoint
+format and ``predict_batch`` contract (order-preserving, item-level errors
+with the reference's reason strings, batch-partition invariant) as
+/root/reference/pkg/src/fusionscreen/models.py -- but every forward pass runs
+in libfusionb200 on the GPU.  Training (``train``/``train_head``/tapes) is out
+of scope: the hot path is inference.
+
+Precision: ``FusionModel.precision`` is "fp32" (FFMA, reference within 1e-3
+relative) by default; "bf16" selects the tcgen05 tensor-core Conv3d path
+(stated, measured tolerance).
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+
+from .checkpoint import load_checkpoint, save_checkpoint
+from .complexes import ComplexGraph, GridConfig, VoxelGrid, build_graph_batch, voxelize_batch
+
+_ACTIVATIONS = ("relu", "leaky-relu", "selu")
+_OPT_KINDS = ("adam", "adamw", "rmsprop", "adadelta")
+
+
+class GraphError(ValueError):
+    """Invalid graph construction or use (autodiff.py:33-34)."""
+
+
+class ShapeError(GraphError):
+    pass
+
+
+@dataclass(frozen=True)
+class OptimizerConfig:
+    """Carried for config/checkpoint compatibility only (optim.py:26-40)."""
+
+    kind: str = "adam"
+    learning_rate: float = 1e-3
+    coefficients: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        if self.kind not in _OPT_KINDS:
+            raise ValueError(f"unknown optimizer kind {self.kind!r}; expected one of {_OPT_KINDS}")
+        if not self.learning_rate > 0:
+            raise ValueError(f"learning_rate must be positive, got {self.learning_rate}")
+
+
+@dataclass(frozen=True)
+class VoxelHeadConfig:          # models.py:40-63
+    grid_extent: int = 16
+    in_channels: int = 8
+    conv_filters_1: int = 32
+    conv_filters_2: int = 64
+    dense_nodes: int = 128
+    residual_1: bool = False
+    residual_2: bool = True
+    batch_norm: bool = False
+    dropout_early: float = 0.25
+    dropout_mid: float = 0.125
+    kernel_1: int = 5
+    kernel_2: int = 3
+
+    @property
+    def flat_width(self) -> int:
+        return self.conv_filters_2 * (self.grid_extent // 4) ** 3
+
+    @property
+    def latent_width(self) -> int:
+        return self.dense_nodes // 2
+
+
+@dataclass(frozen=True)
+class GraphHeadConfig:          # models.py:66-93
+    c_elem: int = 4
+    k_cov: int = 6
+    k_noncov: int = 3
+    gather_width_cov: int = 24
+    gather_width_noncov: int = 128
+    cov_thresh: float = 2.24
+    noncov_thresh: float = 5.22
+
+    def __post_init__(self):
+        for k in (self.k_cov, self.k_noncov):
+            if not 2 <= k <= 8:
+                raise ValueError(f"message-passing steps must be in [2, 8], got {k}")
+
+    @property
+    def feature_width(self) -> int:
+        return self.c_elem + 4
+
+    @property
+    def dense_widths(self):
+        w1 = int(self.gather_width_noncov / 1.5)
+        return w1, w1 // 2
+
+    @property
+    def latent_width(self) -> int:
+        return self.gather_width_noncov
+
+
+@dataclass(frozen=True)
+class FusionConfig:             # models.py:96-118
+    mode: str = "coherent"
+    n_fusion_layers: int = 4
+    model_specific_layers: bool = False
+    residual_fusion: bool = False
+    activation: str = "selu"
+    dropout_early: float = 0.0
+    dropout_mid: float = 0.0
+    dropout_late: float = 0.0
+    fusion_dense_nodes: int = 64
+    pre_trained: bool = False
+    optimizer: OptimizerConfig = field(default_factory=OptimizerConfig)
+    batch_size: int = 48
+    epochs: int = 18
+
+    def __post_init__(self):
+        if self.mode not in ("late", "mid", "coherent"):
+            raise ValueError(f"unknown fusion mode {self.mode!r}")
+        if self.activation not in _ACTIVATIONS:
+            raise ValueError(f"unknown activation {self.activation!r}")
+        if self.mode != "late" and not 3 <= self.n_fusion_layers <= 5:
+            raise ValueError("n_fusion_layers must be 3, 4, or 5")
+
+
+def table_mid_fusion_config(**overrides) -> FusionConfig:
+    """Published Mid-level Fusion end state (models.py:121-128)."""
+    base = dict(mode="mid", n_fusion_layers=5, model_specific_layers=True, residual_fusion=True,
+                activation="selu", dropout_early=0.251, dropout_mid=0.125, dropout_late=0.0,
+                batch_size=1, epochs=64, optimizer=OptimizerConfig("adam", 4.03e-4))
+    base.update(overrides)
+    return FusionConfig(**base)
+
+
+def table_coherent_fusion_config(**overrides) -> FusionConfig:
+    """Published Coherent Fusion end state (models.py:131-138)."""
+    base = dict(mode="coherent", n_fusion_layers=4, model_specific_layers=False, residual_fusion=False,
+                activation="selu", dropout_early=0.386, dropout_mid=0.247, dropout_late=0.055,
+                batch_size=48, epochs=18, pre_trained=True, optimizer=OptimizerConfig("adam", 1.08e-4))
+    base.update(overrides)
+    return FusionConfig(**base)
+
+
+# ---------------------------------------------------------------------------
+# parameter initialisation: U(+-1/sqrt(fan_in)) from one generator, in the
+# reference's draw order (models.py:145-218) so seeds give identical weights
+# ---------------------------------------------------------------------------
+
+def _uniform(rng, fan_in, shape):
+    b = 1.0 / np.sqrt(max(fan_in, 1))
+    return rng.uniform(-b, b, size=shape)
+
+
+def init_voxel_params(cfg: VoxelHeadConfig, rng) -> dict:
+    k1, k2 = cfg.kernel_1, cfg.kernel_2
+    c, f1, f2 = cfg.in_channels, cfg.conv_filters_1, cfg.conv_filters_2
+    specs = [("conv1_w", c * k1 ** 3, (f1, c, k1, k1, k1)), ("conv1_b", c * k1 ** 3, f1),
+             ("conv2_w", f1 * k2 ** 3, (f1, f1, k2, k2, k2)), ("conv2_b", f1 * k2 ** 3, f1),
+             ("conv3_w", f1 * k2 ** 3, (f2, f1, k2, k2, k2)), ("conv3_b", f1 * k2 ** 3, f2),
+             ("conv4_w", f2 * k2 ** 3, (f2, f2, k2, k2, k2)), ("conv4_b", f2 * k2 ** 3, f2),
+             ("dense1_w", cfg.flat_width, (cfg.flat_width, cfg.dense_nodes)),
+             ("dense1_b", cfg.flat_width, cfg.dense_nodes),
+             ("dense2_w", cfg.dense_nodes, (cfg.dense_nodes, cfg.latent_width)),
+             ("dense2_b", cfg.dense_nodes, cfg.latent_width),
+             ("out_w", cfg.latent_width, (cfg.latent_width, 1)), ("out_b", cfg.latent_width, 1)]
+    p = {name: _uniform(rng, fan, shape) for name, fan, shape in specs}
+    if cfg.batch_norm:
+        p["bn1_gamma"], p["bn1_beta"] = np.ones(f1), np.zeros(f1)
+        p["bn2_gamma"], p["bn2_beta"] = np.ones(f2), np.zeros(f2)
+    return p
+
+
+def init_graph_params(cfg: GraphHeadConfig, rng) -> dict:
+    d, gn, fw = cfg.gather_width_cov, cfg.gather_width_noncov, cfg.feature_width
+    p = {"embed_w": _uniform(rng, fw, (fw, d)), "embed_b": _uniform(rng, fw, d),
+         "gather_gate_w": _uniform(rng, d, (d, gn)), "gather_gate_b": _uniform(rng, d, gn),
+         "gather_feat_w": _uniform(rng, d, (d, gn)), "gather_feat_b": _uniform(rng, d, gn)}
+    for phase in ("cov", "noncov"):
+        p[f"{phase}_msg_w"] = _uniform(rng, d, (d, d))
+        for gate in "zrh":
+            p[f"{phase}_w{gate}"] = _uniform(rng, d, (d, d))
+            p[f"{phase}_u{gate}"] = _uniform(rng, d, (d, d))
+            p[f"{phase}_b{gate}"] = _uniform(rng, d, d)
+    w1, w2 = cfg.dense_widths
+    p["dense1_w"], p["dense1_b"] = _uniform(rng, gn, (gn, w1)), _uniform(rng, gn, w1)
+    p["dense2_w"], p["dense2_b"] = _uniform(rng, w1, (w1, w2)), _uniform(rng, w1, w2)
+    p["out_w"], p["out_b"] = _uniform(rng, w2, (w2, 1)), _uniform(rng, w2, 1)
+    return p
+
+
+def init_fusion_params(cfg: FusionConfig, latent_g: int, latent_v: int, rng) -> dict:
+    if cfg.mode == "late":
+        return {}
+    p = {}
+    width = latent_g + latent_v
+    if cfg.model_specific_layers:
+        p["ms_graph_w"], p["ms_graph_b"] = _uniform(rng, latent_g, (latent_g, latent_g)), _uniform(rng, latent_g, latent_g)
+        p["ms_voxel_w"], p["ms_voxel_b"] = _uniform(rng, latent_v, (latent_v, latent_v)), _uniform(rng, latent_v, latent_v)
+        width *= 2
+    widths = [width] + [cfg.fusion_dense_nodes] * (cfg.n_fusion_layers - 1) + [1]
+    for i in range(cfg.n_fusion_layers):
+        p[f"fuse{i}_w"] = _uniform(rng, widths[i], (widths[i], widths[i + 1]))
+        p[f"fuse{i}_b"] = _uniform(rng, widths[i], widths[i + 1])
+    return p
+
+
+def late_fusion_predict(p_voxel, p_graph):
+    """Unweighted mean of the two head predictions (models.py:399-405)."""
+    p_voxel, p_graph = np.asarray(p_voxel, dtype=np.float64), np.asarray(p_graph, dtype=np.float64)
+    if not (np.all(np.isfinite(p_voxel)) and np.all(np.isfinite(p_graph))):
+        raise ValueError("late fusion requires finite head predictions")
+    return (p_voxel + p_graph) / 2.0
+
+
+# ---------------------------------------------------------------------------
+# host -> device packing of pre-featurized items
+# ---------------------------------------------------------------------------
+
+def _pack_graphs(graphs):
+    """Concatenate node features and lift per-graph i<j edges to global ids
+    (the block-diagonal adjacency of batch_graphs, models.py:233-256)."""
+    counts = np.array([g.n_nodes for g in graphs], dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    feats = np.concatenate([np.asarray(g.node_features, dtype=np.float64) for g in graphs]) \
+        if graphs else np.zeros((0, 1))
+
+    def lift(attr):
+        parts = []
+        for g, o in zip(graphs, off[:-1]):
+            e = np.asarray(getattr(g, attr), dtype=np.int64).reshape(-1, 2)
+            if len(e):
+                if e.min() < 0 or e.max() >= g.n_nodes:
+                    raise ValueError(f"{attr} index out of range for a graph of {g.n_nodes} nodes")
+                parts.append(e + o)
+        return np.concatenate(parts) if parts else np.zeros((0, 2), dtype=np.int64)
+
+    return feats, off, lift("covalent_edges"), lift("noncovalent_edges")
+
+
+def _to_dev(a, dtype=None):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.to("cuda", non_blocking=False) if dtype is None else t.to("cuda", dtype=dtype)
+
+
+def _digest(params_sets) -> bytes:
+    h = hashlib.blake2b(digest_size=16)
+    for prefix, ps in params_sets:
+        for k in sorted(ps):
+            a = np.ascontiguousarray(ps[k], dtype=np.float64)
+            h.update(f"{prefix}/{k}{a.shape}".encode())
+            h.update(a.tobytes())
+    return h.digest()
+
+
+class FusionModel:
+    """Two head parameter sets plus fusion layers (models.py:412-568)."""
+
+    def __init__(self, voxel_cfg: VoxelHeadConfig, graph_cfg: GraphHeadConfig, fusion_cfg: FusionConfig,
+                 seed: int = 0, heads_pretrained: bool = False, precision: str = "fp32"):
+        rng = np.random.default_rng(seed)
+        self.voxel_cfg, self.graph_cfg, self.fusion_cfg = voxel_cfg, graph_cfg, fusion_cfg
+        self.voxel_params = init_voxel_params(voxel_cfg, rng)
+        self.graph_params = init_graph_params(graph_cfg, rng)
+        self.fusion_params = init_fusion_params(fusion_cfg, graph_cfg.latent_width, voxel_cfg.latent_width, rng)
+        self.bn_state: dict = {}
+        self.heads_pretrained = heads_pretrained
+        self.seed = seed
+        self.precision = precision
+        self.box_size = 16.0
+        self._dev = None
+        self._dev_key = None
+
+    @classmethod
+    def from_heads(cls, voxel_params, voxel_cfg, graph_params, graph_cfg, fusion_cfg, seed=0):
+        m = cls(voxel_cfg, graph_cfg, fusion_cfg, seed=seed, heads_pretrained=True)
+        m.voxel_params = {k: v.copy() for k, v in voxel_params.items()}
+        m.graph_params = {k: v.copy() for k, v in graph_params.items()}
+        return m
+
+    def build_tape(self, *a, **k):
+        raise NotImplementedError("autodiff tapes (training) are outside the B200 scoring path")
+
+    # -- device model (packed once; re-packed if parameters change) -----------
+    def device_model(self):
+        from .engine import DeviceModel
+        key = (_digest((("voxel", self.voxel_params), ("graph", self.graph_params),
+                        ("fusion", self.fusion_params))), self.box_size,
+               repr(sorted((k, tuple(np.asarray(v["mean"]).ravel()), tuple(np.asarray(v["var"]).ravel()))
+                           for k, v in self.bn_state.items())))
+        if self._dev is None or self._dev_key != key:
+            self._dev = DeviceModel(self.voxel_cfg, self.graph_cfg, self.fusion_cfg, self.all_params(),
+                                    self.box_size, bn_state=self.bn_state or None)
+            self._dev_key = key
+        return self._dev
+
+    # -- prediction ---------------------------------------------------------
+    def predict_batch(self, items, batch_seed: int = 0):
+        """Scores (VoxelGrid, ComplexGraph) pairs (models.py:470-498).
+
+        Returns (predictions, errors); malformed items never abort the batch.
+        ``batch_seed`` only seeds dropout in the reference's eval tape, where
+        dropout is the identity, so it does not change results."""
+        preds = [None] * len(items)
+        errors = []
+        valid = []
+        for i, item in enumerate(items):
+            reason = self._validate_item(item)
+            if reason is None:
+                valid.append(i)
+            else:
+                errors.append((i, reason))
+        if not valid:
+            return preds, errors
+        grids = np.stack([np.asarray(items[i][0].occupancy, dtype=np.float64) for i in valid])
+        feats, off, ce, ne = _pack_graphs([items[i][1] for i in valid])
+        dm = self.device_model()
+        out = dm.score_features(len(valid), grids=_to_dev(grids), feats=_to_dev(feats), node_off=_to_dev(off),
+                                cov_edges=_to_dev(ce), ncov_edges=_to_dev(ne), heads=7,
+                                precision=self.precision)
+        scores = out["scores"].cpu().numpy().astype(np.float64)
+        err = out["err"].cpu().numpy()
+        from . import _native as N
+        late_errs = []
+        for slot, i in enumerate(valid):
+            e = int(err[slot])
+            if e & N.FS_ERR_GRID_NONFINITE:
+                late_errs.append((i, "voxel grid contains non-finite values"))
+            elif e & N.FS_ERR_FEAT_NONFINITE:
+                late_errs.append((i, "graph features contain non-finite values"))
+            elif e:
+                late_errs.append((i, f"device error flags {e}"))
+            else:
+                preds[i] = float(scores[slot])
+        if late_errs:
+            errors = sorted(errors + late_errs)
+        return preds, errors
+
+    def _validate_item(self, item):
+        """Host-side structural checks with the reference's reason strings
+        (models.py:511-529); finiteness is checked on device in the same pass
+        that uploads the data."""
+        try:
+            grid, graph = item
+        except (TypeError, ValueError):
+            return "item is not a (VoxelGrid, ComplexGraph) pair"
+        if not isinstance(grid, VoxelGrid) or not isinstance(graph, ComplexGraph):
+            return "item is not a (VoxelGrid, ComplexGraph) pair"
+        want = (self.voxel_cfg.in_channels,) + (self.voxel_cfg.grid_extent,) * 3
+        if grid.occupancy.shape != want:
+            return f"voxel grid shape {grid.occupancy.shape} != {want}"
+        if graph.node_features.ndim != 2 or graph.node_features.shape[1] != self.graph_cfg.feature_width:
+            return (f"graph feature width "
+                    f"{graph.node_features.shape} != {self.graph_cfg.feature_width}")
+        return None
+
+    def score_complexes(self, complexes):
+        """Fused featurize + score of raw complexes on device (the screening
+        path: models.featurize (:638-651) then predict_batch).  Returns
+        (scores float64 [P], err int32 [P])."""
+        from .engine import batch_from_complexes
+        b = batch_from_complexes(complexes)
+        out = self.device_model().score_poses(b, self.precision)
+        return out["scores"].cpu().numpy().astype(np.float64), out["err"].cpu().numpy()
+
+    # -- parameter bookkeeping (models.py:532-568) -----------------------------
+    def all_params(self) -> dict:
+        out = {}
+        for prefix, ps in (("voxel", self.voxel_params), ("graph", self.graph_params), ("fusion", self.fusion_params)):
+            for k, v in ps.items():
+                out[f"{prefix}/{k}"] = v
+        return out
+
+    def set_params(self, flat: dict) -> None:
+        for full, arr in flat.items():
+            prefix, name = full.split("/", 1)
+            target = {"voxel": self.voxel_params, "graph": self.graph_params, "fusion": self.fusion_params}[prefix]
+            target[name] = np.array(arr, dtype=np.float64)
+
+    def save(self, path) -> None:
+        meta = {"model": "fusion", "voxel_cfg": asdict(self.voxel_cfg), "graph_cfg": asdict(self.graph_cfg),
+                "fusion_cfg": _fusion_cfg_dict(self.fusion_cfg), "seed": self.seed,
+                "heads_pretrained": self.heads_pretrained}
+        save_checkpoint(path, self.all_params(), meta)
+
+    @classmethod
+    def load(cls, path, precision: str = "fp32") -> "FusionModel":
+        """Loads reference checkpoints (checkpoint.py:48-71 format) unchanged."""
+        params, meta = load_checkpoint(path)
+        m = cls(VoxelHeadConfig(**meta["voxel_cfg"]), GraphHeadConfig(**meta["graph_cfg"]),
+                _fusion_cfg_from_dict(meta["fusion_cfg"]), seed=meta.get("seed", 0),
+                heads_pretrained=meta.get("heads_pretrained", False), precision=precision)
+        m.set_params(params)
+        return m
+
+
+def _fusion_cfg_dict(cfg: FusionConfig) -> dict:
+    d = asdict(cfg)
+    d["optimizer"] = {"kind": cfg.optimizer.kind, "learning_rate": cfg.optimizer.learning_rate,
+                      "coefficients": cfg.optimizer.coefficients}
+    return d
+
+
+def _fusion_cfg_from_dict(d: dict) -> FusionConfig:
+    d = dict(d)
+    o = d.pop("optimizer")
+    return FusionConfig(optimizer=OptimizerConfig(o["kind"], o["learning_rate"], dict(o["coefficients"])), **d)
+
+
+# ---------------------------------------------------------------------------
+# individual head forwards (models.py:590-624)
+# ---------------------------------------------------------------------------
+
+def _head_model(vcfg=None, gcfg=None, vparams=None, gparams=None, precision="fp32", bn_state=None):
+    """DeviceModel for a single head: the other head's weights are unused
+    placeholders drawn from a fixed seed (never read by the requested head)."""
+    from .engine import DeviceModel
+    vcfg = vcfg or VoxelHeadConfig()
+    gcfg = gcfg or GraphHeadConfig()
+    fcfg = FusionConfig(mode="late")
+    rng = np.random.default_rng(0)
+    vp = vparams if vparams is not None else init_voxel_params(vcfg, rng)
+    gp = gparams if gparams is not None else init_graph_params(gcfg, rng)
+    flat = {f"voxel/{k}": v for k, v in vp.items()}
+    flat.update({f"graph/{k}": v for k, v in gp.items()})
+    return DeviceModel(vcfg, gcfg, fcfg, flat, bn_state=bn_state)
+
+
+def _stack_grids(grids, cfg):
+    if isinstance(grids, VoxelGrid):
+        grids = [grids]
+    vox = np.stack([np.asarray(v.occupancy, dtype=np.float64) for v in grids])
+    want = (cfg.in_channels,) + (cfg.grid_extent,) * 3
+    if vox.shape[1:] != want:
+        raise GraphError(f"voxel batch shape {vox.shape[1:]} != {want}")
+    return vox
+
+
+def voxel_head_forward(params: dict, cfg: VoxelHeadConfig, grids, training: bool = False, seed: int = 0,
+                       bn_state: dict | None = None, precision: str = "fp32"):
+    """Returns (predictions [B], latents [B, latent_width]) (models.py:590-601)."""
+    if training:
+        raise NotImplementedError("training-mode forward (dropout) is outside the scoring path")
+    vox = _stack_grids(grids, cfg)
+    dm = _head_model(vcfg=cfg, vparams=params, precision=precision, bn_state=bn_state)
+    out = dm.score_features(len(vox), grids=_to_dev(vox), heads=1, precision=precision)
+    if int(out["err"].abs().sum().item()):
+        raise GraphError("non-finite values in array")
+    return (out["pred_v"].cpu().numpy().astype(np.float64),
+            out["lat_v"].cpu().numpy().astype(np.float64))
+
+
+def graph_head_forward(params: dict, cfg: GraphHeadConfig, graphs, training: bool = False, seed: int = 0,
+                       precision: str = "fp32"):
+    """Returns (predictions [B], latents [B, gather_width_noncov]) (models.py:604-614)."""
+    if training:
+        raise NotImplementedError("training-mode forward is outside the scoring path")
+    if isinstance(graphs, ComplexGraph):
+        graphs = [graphs]
+    feats, off, ce, ne = _pack_graphs(graphs)
+    dm = _head_model(gcfg=cfg, gparams=params, precision=precision)
+    out = dm.score_features(len(graphs), feats=_to_dev(feats), node_off=_to_dev(off), cov_edges=_to_dev(ce),
+                            ncov_edges=_to_dev(ne), heads=2, precision=precision)
+    if int(out["err"].abs().sum().item()):
+        raise GraphError("non-finite values in array")
+    return (out["pred_g"].cpu().numpy().astype(np.float64),
+            out["lat_g"].cpu().numpy().astype(np.float64))
+
+
+# ---------------------------------------------------------------------------
+# featurization (models.py:631-651)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class FeaturizedItem:
+    grid: VoxelGrid
+    graph: ComplexGraph
+    label: float
+
+
+def featurize(complexes, voxel_cfg: VoxelHeadConfig, graph_cfg: GraphHeadConfig, box_size: float = 16.0):
+    """Batched on-device featurization: one voxelize and one graph launch pair
+    for the whole list (the reference loops per complex)."""
+    if not complexes:
+        return []
+    grid_cfg = GridConfig(extent=voxel_cfg.grid_extent, c_elem=voxel_cfg.in_channels // 2, box_size=box_size)
+    grids = voxelize_batch(complexes, grid_cfg)
+    graphs = build_graph_batch(complexes, graph_cfg.cov_thresh, graph_cfg.noncov_thresh, graph_cfg.c_elem,
+                               box_size)
+    return [FeaturizedItem(VoxelGrid(grids[i]), graphs[i], c.label_pk) for i, c in enumerate(complexes)]

@@ -1,0 +1,151 @@
+"""Pocket screening engine: device-resident pose libraries, batched fused
+scoring (featurize + 3D-CNN + SG-CNN + fusion in one fs_score_poses call per
+batch), running top-k on device, and the multi-GPU merge.
+
+Sharding: each rank owns a contiguous, compound-aligned slice
+of the global pose index range and scores it with no data-path collective;
+the only exchange is one all-gather of every rank's per-target top-k
+(score f32, global pose index i64) over NCCL, merged on every rank with the
+same (score desc, index asc) order (tie rule of evaluate.py:67-83).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import engine as E
+from .synth import Pocket, PoseLibrary
+
+
+class DeviceLibrary:
+    """A PoseLibrary uploaded to one device (positions float64, ids int32)."""
+
+    def __init__(self, lib: PoseLibrary, pockets, device, index_base=0):
+        self.lib = lib
+        self.device = device
+        self.index_base = int(index_base)
+        self.xyz = torch.from_numpy(np.ascontiguousarray(lib.xyz)).to(device)
+        self.elem = torch.from_numpy(np.ascontiguousarray(lib.elem, dtype=np.int32)).to(device)
+        self.role = torch.from_numpy(np.ascontiguousarray(lib.role, dtype=np.int32)).to(device)
+        self.atom_off = torch.from_numpy(np.ascontiguousarray(lib.atom_off, dtype=np.int64)).to(device)
+        self.target = torch.from_numpy(np.ascontiguousarray(lib.target, dtype=np.int32)).to(device)
+        self.pidx = torch.arange(self.index_base, self.index_base + lib.n_poses, dtype=torch.int64, device=device)
+        p_xyz = np.concatenate([p.xyz for p in pockets])
+        p_off = np.concatenate([[0], np.cumsum([len(p.xyz) for p in pockets])]).astype(np.int64)
+        self.pocket_xyz = torch.from_numpy(p_xyz).to(device)
+        self.pocket_elem = torch.from_numpy(np.concatenate([p.elem for p in pockets]).astype(np.int32)).to(device)
+        self.pocket_role = torch.from_numpy(np.concatenate([p.role for p in pockets]).astype(np.int32)).to(device)
+        self.pocket_off = torch.from_numpy(p_off).to(device)
+        lig = np.diff(lib.atom_off)
+        psz = np.diff(p_off)
+        self.max_pose_atoms = int((lig + psz[lib.target]).max()) if lib.n_poses else 1
+
+    @property
+    def n_poses(self):
+        return self.lib.n_poses
+
+    def batch(self, s, e) -> E.PoseBatch:
+        return E.PoseBatch(self.xyz, self.elem, self.role, self.atom_off[s:e + 1], self.max_pose_atoms,
+                           self.pocket_xyz, self.pocket_elem, self.pocket_role, self.pocket_off,
+                           self.target[s:e])
+
+
+class HostStager:
+    """Pinned host copy of a library, pre-cut into batches, for end-to-end
+    runs: every step copies its batch's atoms host->device (one
+    cudaMemcpyAsync per array) and reads the scores back."""
+
+    def __init__(self, lib: PoseLibrary, batch_size: int, dlib: DeviceLibrary):
+        self.lib = lib
+        self.B = batch_size
+        self.dlib = dlib
+        P = lib.n_poses
+        self.bounds = [(s, min(P, s + batch_size)) for s in range(0, P, batch_size)]
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        self.h_xyz, self.h_elem, self.h_role = pin(lib.xyz), pin(lib.elem.astype(np.int32)), pin(lib.role.astype(np.int32))
+        self.h_target = pin(lib.target.astype(np.int32))
+        offs = np.zeros((len(self.bounds), batch_size + 1), dtype=np.int64)
+        for i, (s, e) in enumerate(self.bounds):
+            offs[i, : e - s + 1] = lib.atom_off[s:e + 1] - lib.atom_off[s]
+        self.h_off = pin(offs)
+        max_atoms = max(int(lib.atom_off[e] - lib.atom_off[s]) for s, e in self.bounds)
+        dev = dlib.device
+        self.d_xyz = torch.empty((max_atoms, 3), dtype=torch.float64, device=dev)
+        self.d_elem = torch.empty(max_atoms, dtype=torch.int32, device=dev)
+        self.d_role = torch.empty(max_atoms, dtype=torch.int32, device=dev)
+        self.d_off = torch.empty(batch_size + 1, dtype=torch.int64, device=dev)
+        self.d_target = torch.empty(batch_size, dtype=torch.int32, device=dev)
+        self.h_scores = torch.empty(batch_size, dtype=torch.float32).pin_memory()
+
+    def stage(self, i):
+        """H2D copies of batch i; returns (PoseBatch, h2d bytes)."""
+        s, e = self.bounds[i]
+        a, b = int(self.lib.atom_off[s]), int(self.lib.atom_off[e])
+        n = b - a
+        self.d_xyz[:n].copy_(self.h_xyz[a:b], non_blocking=True)
+        self.d_elem[:n].copy_(self.h_elem[a:b], non_blocking=True)
+        self.d_role[:n].copy_(self.h_role[a:b], non_blocking=True)
+        self.d_off[: e - s + 1].copy_(self.h_off[i, : e - s + 1], non_blocking=True)
+        self.d_target[: e - s].copy_(self.h_target[s:e], non_blocking=True)
+        nbytes = n * (24 + 4 + 4) + (e - s + 1) * 8 + (e - s) * 4
+        d = self.dlib
+        b_ = E.PoseBatch(self.d_xyz, self.d_elem, self.d_role, self.d_off[: e - s + 1], d.max_pose_atoms,
+                         d.pocket_xyz, d.pocket_elem, d.pocket_role, d.pocket_off, self.d_target[: e - s])
+        return b_, nbytes
+
+    def read_scores(self, scores):
+        n = scores.numel()
+        self.h_scores[:n].copy_(scores, non_blocking=True)
+        return n * 4
+
+
+class Screen:
+    """Scores a DeviceLibrary batch by batch with a running device top-k."""
+
+    def __init__(self, model: E.DeviceModel, precision="bf16", batch_size=8192, k=100,
+                 max_edges_per_pose=32768):
+        self.model = model
+        self.precision = precision
+        self.B = batch_size
+        self.k = k
+        self.max_edges_per_pose = max_edges_per_pose
+
+    def score(self, batch: E.PoseBatch, outputs=("scores",)):
+        # no host sync: overflow shows up in err (checked after the screen)
+        return self.model.score_poses(batch, self.precision, self.max_edges_per_pose, outputs, retry=False)
+
+    def run(self, dlib: DeviceLibrary, keep_scores=False):
+        """Score the whole library; returns dict(topk_scores, topk_idx, err,
+        scores?).  Pose indices are global (dlib.index_base + local)."""
+        top_s = top_i = None
+        errs, all_s = [], []
+        for s in range(0, dlib.n_poses, self.B):
+            e = min(dlib.n_poses, s + self.B)
+            out = self.score(dlib.batch(s, e))
+            top_s, top_i = E.topk_merge(top_s, top_i, out["scores"], dlib.pidx[s:e], self.k)
+            errs.append(out["err"])
+            if keep_scores:
+                all_s.append(out["scores"])
+        res = {"topk_scores": top_s, "topk_idx": top_i, "err": torch.cat(errs) if errs else None}
+        if keep_scores:
+            res["scores"] = torch.cat(all_s)
+        return res
+
+
+def merge_topk_across_ranks(top_s, top_i, k, group=None):
+    """All-gather every rank's top-k (NCCL over NVLink) and merge on device.
+    Ranks holding fewer than k entries pad with NaN (ranked last)."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return top_s, top_i
+    ws = dist.get_world_size(group)
+    pad_s = torch.full((k,), float("nan"), dtype=torch.float32, device=top_s.device)
+    pad_i = torch.full((k,), np.iinfo(np.int32).max, dtype=torch.int64, device=top_s.device)
+    pad_s[: top_s.numel()] = top_s
+    pad_i[: top_i.numel()] = top_i
+    gs = torch.empty(ws * k, dtype=torch.float32, device=top_s.device)
+    gi = torch.empty(ws * k, dtype=torch.int64, device=top_s.device)
+    dist.all_gather_into_tensor(gs, pad_s, group=group)
+    dist.all_gather_into_tensor(gi, pad_i, group=group)
+    return E.topk_merge(gs, gi, None, None, k)
