@@ -1,0 +1,361 @@
+"""Throughput bench of the B200 Coherent-Fusion pose-scoring path.
+
+Workload (BASELINE.json configs[3], "config 4"): a screen of synthetic docked
+poses against one 1,000-atom pocket; ligands U{16..64} atoms, 10 poses per
+compound; random-init weights FusionModel(seed=0).  A *step* is one fused
+pass of the hot path -- featurize (voxel splat + exact radius graph) +
+3D-CNN + SG-CNN + fusion + running device top-k -- over one batch of B poses
+per GPU.  Weak scaling: every rank scores its own compound-aligned shard of
+K*B poses; the only collective is the final NCCL all-gather of the per-rank
+top-k (merged on device), inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--precision bf16|fp32]
+    python bench.py --impl reference ...   # CPU reference arm (oracle port)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "docked poses scored/sec (8×B200, device-timed) vs CPU ref; roofline fraction"
+POCKET_ATOMS = 1000
+LIGAND_ATOMS = (16, 64)
+POSES_PER_COMPOUND = 10
+TOPK = 100
+WORKLOAD = ("config4: Coherent Fusion screen vs one 1000-atom pocket, ligands U{16..64} atoms, "
+            "10 poses/compound, featurize+3D-CNN+SG-CNN+fusion+top-k per step")
+
+# algorithmic work per pose: FLOP(N,Ec,En)
+VOXEL_FLOP = 659_570_816
+CONV_FLOP = {"conv1": 2 * 131_072_000, "conv2": 2 * 113_246_208, "conv3": 2 * 28_311_552,
+             "conv4": 2 * 56_623_104}
+
+
+def graph_flop(n, ec, en):
+    return 85_248 * n + 28_984 + 48 * (6 * ec + 3 * en)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines (oracle port, the reference algorithm restated in numpy)
+# ---------------------------------------------------------------------------
+def _cpu_worker(args):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    seeds, n_poses = args
+    from oracle import fusion_oracle as orc
+    from paper_2104_04547_b200 import synth
+    from tests._cfg import COHERENT, GRAPH, VOXEL
+    params = orc.init_params(VOXEL, GRAPH, COHERENT, 0)
+    pocket = synth.make_pocket(POCKET_ATOMS, seed=0)
+    lib = synth.make_poses(max(1, n_poses // POSES_PER_COMPOUND + 1), POSES_PER_COMPOUND, seed=seeds,
+                           ligand_atoms=LIGAND_ATOMS)
+    t0 = time.perf_counter()
+    for p in range(n_poses):
+        orc.score_pose(params, (VOXEL, GRAPH, COHERENT), *synth.complex_arrays(pocket, lib, p))
+    return time.perf_counter() - t0
+
+
+def cpu_pool_rate(workers, poses_per_worker, seed=100):
+    """All-cores rate: P processes x 1 BLAS thread, poses / slowest worker."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    with ctx.Pool(workers) as pool:
+        times = pool.map(_cpu_worker, [(seed + i, poses_per_worker) for i in range(workers)])
+    return workers * poses_per_worker / max(times)
+
+
+def cpu_single_rate(n_poses=24):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    t = _cpu_worker((99, n_poses))
+    return n_poses / t
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    workers = os.cpu_count() or 1
+    per = 2
+    t0 = time.perf_counter()
+    for _ in range(args.warmup):
+        cpu_pool_rate(workers, 1)
+    rates, times = [], []
+    for _ in range(args.steps):
+        s = time.perf_counter()
+        rates.append(cpu_pool_rate(workers, per))
+        times.append(time.perf_counter() - s)
+    value = statistics.median(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "poses/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "poses_per_step": workers * per},
+            "cpu_baseline": {"value": value, "unit": "poses/s", "cores": workers, "kind": "port",
+                             "sample": f"{workers} processes x {per} poses per step (oracle/fusion_oracle.py, "
+                                       "float64, OPENBLAS_NUM_THREADS=1)"},
+            "e2e": {"value": value, "unit": "poses/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--precision", default=os.environ.get("FS_BENCH_PRECISION", "auto"))
+    ap.add_argument("--batch", type=int, default=int(os.environ.get("FS_BENCH_BATCH", "0")))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2104_04547_b200 import _native as N
+    from paper_2104_04547_b200 import engine as E
+    from paper_2104_04547_b200 import models, synth
+    from paper_2104_04547_b200.screen import DeviceLibrary, HostStager, merge_topk_across_ranks
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    vcfg, gcfg, fcfg = models.VoxelHeadConfig(), models.GraphHeadConfig(), models.table_coherent_fusion_config()
+    model = models.FusionModel(vcfg, gcfg, fcfg, seed=0)
+    dm = E.DeviceModel(vcfg, gcfg, fcfg, model.all_params(), device=dev)
+    precision = args.precision
+    if precision == "auto":
+        precision = "bf16" if dm.supports("bf16") else "fp32"
+    B = args.batch or (16384 if precision == "bf16" else 4096)
+    K, W = args.steps, args.warmup
+
+    # this rank's shard: K*B poses (weak scaling), distinct compounds per rank
+    n_comp = (K * B + POSES_PER_COMPOUND - 1) // POSES_PER_COMPOUND
+    pocket = synth.make_pocket(POCKET_ATOMS, seed=0)
+    lib = synth.make_poses(n_comp, POSES_PER_COMPOUND, seed=1000 + rank, ligand_atoms=LIGAND_ATOMS,
+                           compound_base=rank * n_comp).slice(0, K * B)
+    dlib = DeviceLibrary(lib, [pocket], dev, index_base=rank * K * B)
+    L = N.lib()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def step(s, e, top):
+        out = dm.score_poses(dlib.batch(s, e), precision, 32768, retry=False)
+        ts, ti = E.topk_merge(top[0], top[1], out["scores"], dlib.pidx[s:e], TOPK)
+        return out, (ts, ti)
+
+    # ---- warm-up (also validates: no pose may fail) ----
+    top = (None, None)
+    for i in range(W):
+        s = (i % K) * B
+        out, top = step(s, s + B, top)
+    torch.cuda.synchronize()
+    assert int(out["err"].abs().sum().item()) == 0, "pose errors in warm-up batch"
+
+    # ---- timed region: device-resident inputs ----
+    stage_ms = np.zeros(len(N.STAGES) - 1)
+    stage_events = [[torch.cuda.Event(enable_timing=True) for _ in N.STAGES] for _ in range(K)]
+    for evs in stage_events:          # torch creates CUDA events lazily: force creation
+        for e in evs:
+            e.record()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.fs_launch_count()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    errs = []
+    with Clocks(local) as clk:
+        t_start.record()
+        top = (None, None)
+        for i in range(K):
+            flush.zero_()                                  # L2 flush between steps
+            evs = stage_events[i]
+            arr = (E.C.c_void_p * len(evs))(*[E.C.c_void_p(e.cuda_event) for e in evs])
+            L.fs_set_stage_events(arr, len(evs))
+            out, top = step(i * B, (i + 1) * B, top)
+            L.fs_set_stage_events(None, 0)
+            errs.append(out["err"])
+        gs, gi = merge_topk_across_ranks(top[0], top[1], TOPK)
+        t_end.record()
+        torch.cuda.synchronize()
+    launches = L.fs_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    for i in range(K):
+        evs = stage_events[i]
+        for j in range(len(N.STAGES) - 1):
+            stage_ms[j] += evs[j].elapsed_time(evs[j + 1])
+    bad = int(torch.stack(errs).ne(0).sum().item())
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * K * B / (ms_max / 1e3)
+
+    # ---- end to end: host pinned library -> device, scores back, per step ----
+    stager = HostStager(lib, B, dlib)
+    h2d = d2h = 0
+    for i in range(min(W, len(stager.bounds))):
+        b, _ = stager.stage(i)
+        o = dm.score_poses(b, precision, 32768, retry=False)
+        stager.read_scores(o["scores"])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    top = (None, None)
+    for i in range(K):
+        b, nb = stager.stage(i)
+        o = dm.score_poses(b, precision, 32768, retry=False)
+        top = E.topk_merge(top[0], top[1], o["scores"], dlib.pidx[i * B:(i + 1) * B], TOPK)
+        d2h_b = stager.read_scores(o["scores"])
+        h2d += nb
+        d2h += d2h_b
+    gs2, gi2 = merge_topk_across_ranks(top[0], top[1], TOPK)
+    e1.record()
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * K * B / (float(te.item()) / 1e3)
+    same_topk = bool(torch.equal(gi, gi2))
+
+    if rank == 0:
+        hbm, bf16_burst, bf16_sus, peak_kind = peaks()
+        names = N.STAGES[:-1]
+        dom = int(np.argmax(stage_ms))
+        dom_name = names[dom]
+        avg_ms = stage_ms[dom] / K
+        # mean nodes/edges of the workload for the graph-side FLOP formula
+        n_mean = POCKET_ATOMS + float(np.mean(np.diff(lib.atom_off)))
+        if dom_name in CONV_FLOP:
+            flop = CONV_FLOP[dom_name] * B
+            roof = {"kernel": f"{dom_name} ({'tcgen05 bf16' if precision == 'bf16' else 'FFMA fp32'})",
+                    "bound": "tensor", "achieved": flop / (avg_ms / 1e3) / 1e12,
+                    "peak": bf16_sus, "unit": "TFLOP/s", "traffic": None}
+        elif dom_name == "gnn":
+            flop = graph_flop(n_mean, 5152, 9094) * B
+            roof = {"kernel": "gnn (fused GRU message passing, FFMA fp32)", "bound": "tensor",
+                    "achieved": flop / (avg_ms / 1e3) / 1e12, "peak": bf16_sus, "unit": "TFLOP/s",
+                    "traffic": None}
+        else:
+            flop = (VOXEL_FLOP + graph_flop(n_mean, 5152, 9094)) * B
+            roof = {"kernel": dom_name, "bound": "tensor", "achieved": flop / (avg_ms / 1e3) / 1e12,
+                    "peak": bf16_sus, "unit": "TFLOP/s", "traffic": None}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["peak_kind"] = f"{peak_kind} bf16 sustained"
+        roof["stage_ms_per_step"] = {n: round(v / K, 4) for n, v in zip(names, stage_ms)}
+        roof["dominant_share"] = float(stage_ms[dom] / stage_ms.sum())
+        line = {"metric": METRIC, "value": value, "unit": "poses/s", "n_gpus": world, "steps": K, "warmup": W,
+                "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": precision, "data": "synthetic",
+                "config": {"workload": WORKLOAD, "poses_per_step_per_gpu": B, "precision": precision,
+                           "topk": TOPK, "pocket_atoms": POCKET_ATOMS, "ligand_atoms": list(LIGAND_ATOMS),
+                           "l2": "256 MiB buffer zeroed between steps (inside the timed region)",
+                           "weights": "random-init FusionModel(seed=0)", "failed_poses": bad},
+                "roofline": roof,
+                "e2e": {"value": e2e_value, "unit": "poses/s", "h2d_bytes_per_step": h2d // K,
+                        "d2h_bytes_per_step": d2h // K, "topk_equal_device_resident": same_topk},
+                "gpu_launches": int(launches), "clocks": clk.summary()}
+        if not args.no_cpu_baseline and world == 1:
+            n_cpu = 24
+            rate = cpu_single_rate(n_cpu)
+            line["cpu_baseline"] = {"value": rate, "unit": "poses/s", "cores": 1, "kind": "port",
+                                    "sample": f"{n_cpu} poses of the same workload through oracle/fusion_oracle.py "
+                                              "(float64 numpy, 1 BLAS thread)"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

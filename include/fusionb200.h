@@ -109,6 +109,13 @@ const char* fs_strerror(int code);
 int fs_version(void);
 /* Last CUDA error string seen by this thread (diagnostics). */
 const char* fs_last_cuda_error(void);
+/* Number of kernel launches the library has issued (process-wide). */
+long long fs_launch_count(void);
+/* Optional per-stage timing for fs_score_poses on the calling thread:
+ * `events` is an array of 9 cudaEvent_t (featurize, conv1, conv2, conv3,
+ * conv4, dense, gnn, fusion, end) recorded on the scoring stream at each
+ * stage boundary; NULL disables.  Entries may be NULL. */
+int fs_set_stage_events(void** events, int n);
 
 /* ---- weights (FusionModel.__init__/load -> device) ---------------------- */
 /* Replaces FusionModel parameter binding (models.py:263-278, :441-467).

@@ -21,11 +21,13 @@ FS_PREC_FP32, FS_PREC_BF16 = 0, 1
 FS_GRID_NCDHW_F64, FS_GRID_NDHWC_F32, FS_GRID_NDHWC_BF16 = 0, 1, 2
 FS_MODE_LATE, FS_MODE_MID, FS_MODE_COHERENT = 0, 1, 2
 
+STAGES = ("featurize", "conv1", "conv2", "conv3", "conv4", "dense", "gnn", "fusion", "end")
 PRECISIONS = {"fp32": FS_PREC_FP32, "bf16": FS_PREC_BF16}
 
 # every symbol include/fusionb200.h declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "fs_strerror", "fs_version", "fs_last_cuda_error", "fs_weights_bytes", "fs_model_create",
+    "fs_strerror", "fs_version", "fs_last_cuda_error", "fs_launch_count", "fs_set_stage_events",
+    "fs_weights_bytes", "fs_model_create",
     "fs_model_destroy", "fs_model_supports", "fs_node_offsets", "fs_node_offsets_ws_bytes",
     "fs_voxelize", "fs_node_features", "fs_graph_count", "fs_graph_rows", "fs_graph_rows_ws_bytes",
     "fs_graph_fill", "fs_graph_edge_counts", "fs_graph_edges", "fs_workspace_bytes",
@@ -79,6 +81,8 @@ def _sig(lib):
         "fs_strerror": (C.c_char_p, [C.c_int]),
         "fs_version": (C.c_int, []),
         "fs_last_cuda_error": (C.c_char_p, []),
+        "fs_launch_count": (C.c_longlong, []),
+        "fs_set_stage_events": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
         "fs_weights_bytes": (_SZ, [md]),
         "fs_model_create": (C.c_int, [md, C.POINTER(C.c_char_p), C.POINTER(C.c_void_p), C.c_int,
                                       _P, _SZ, _P, C.POINTER(C.c_void_p)]),

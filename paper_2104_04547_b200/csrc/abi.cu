@@ -5,6 +5,7 @@
 // (models.py:470-498) -> build_tape (:441-467) -> _voxel_tape (:285-322),
 // _graph_tape (:351-371), _fusion_tape (:374-396); featurize (:638-651) ->
 // voxelize / build_graph (complexes.py:171-254).
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -18,6 +19,14 @@ namespace fs {
 
 static thread_local std::string g_last_cuda_error;
 void set_cuda_error(cudaError_t e) { g_last_cuda_error = cudaGetErrorString(e); }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static thread_local cudaEvent_t* g_stage_events = nullptr;   // [ST_COUNT] or null
+void mark_stage(int stage, cudaStream_t st) {
+  if (g_stage_events && g_stage_events[stage]) cudaEventRecord(g_stage_events[stage], st);
+}
 
 // ---- launchers defined in the other translation units ----------------------
 int launch_node_offsets(const fs_pose_batch& b, int64_t* node_off, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -362,18 +371,22 @@ static int voxel_head_fp32(const fs_model& m, int P, char* ws, const WsPlan& w, 
   c.in = grid; c.w = m.P(m.c1w); c.b = m.P(m.c1b); c.out = a1; c.n_vox = (int64_t)P * G * G * G;
   c.g = G; c.cin = m.cin; c.cout = m.f1; c.k = m.k1;
   if (d.batch_norm) { c.bn_scale = m.P(m.bn1s); c.bn_shift = m.P(m.bn1h); }
+  mark_stage(ST_CONV1, st);
   if ((rc = launch_conv3d_ffma(c, st))) return rc;
+  mark_stage(ST_CONV2, st);
   c = ConvArgs{};
   c.in = a1; c.w = m.P(m.c2w); c.b = m.P(m.c2b); c.out = a2; c.n_vox = (int64_t)P * G * G * G;
   c.g = G; c.cin = m.f1; c.cout = m.f1; c.k = m.k2;
   if (d.residual_1) c.residual = a1;
   if ((rc = launch_conv3d_ffma(c, st))) return rc;
   if ((rc = launch_maxpool2(a2, p1, P, H, m.f1, st))) return rc;
+  mark_stage(ST_CONV3, st);
   c = ConvArgs{};
   c.in = p1; c.w = m.P(m.c3w); c.b = m.P(m.c3b); c.out = a3; c.n_vox = (int64_t)P * H * H * H;
   c.g = H; c.cin = m.f1; c.cout = m.f2; c.k = m.k2;
   if (d.batch_norm) { c.bn_scale = m.P(m.bn2s); c.bn_shift = m.P(m.bn2h); }
   if ((rc = launch_conv3d_ffma(c, st))) return rc;
+  mark_stage(ST_CONV4, st);
   c = ConvArgs{};
   c.in = a3; c.w = m.P(m.c4w); c.b = m.P(m.c4b); c.out = a4; c.n_vox = (int64_t)P * H * H * H;
   c.g = H; c.cin = m.f2; c.cout = m.f2; c.k = m.k2;
@@ -385,6 +398,7 @@ static int voxel_head_fp32(const fs_model& m, int P, char* ws, const WsPlan& w, 
 // dense1 -> dense2 (latent_v into lat[:, gn:]) -> optional pred_v
 static int voxel_tail(const fs_model& m, int P, char* ws, const WsPlan& w, bool want_pred, cudaStream_t st) {
   float* lat = (float*)(ws + w.lat);
+  mark_stage(ST_DENSE, st);
   DenseArgs a{};
   a.x = (float*)(ws + w.p2); a.ldx = m.flat; a.w = m.P(m.d1w); a.b = m.P(m.d1b);
   a.y = (float*)(ws + w.d1); a.ldy = m.dn; a.m = P; a.k = m.flat; a.n = m.dn; a.act = FS_ACT_RELU;
@@ -413,7 +427,9 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
   g.gg = m.P(m.gg); g.bg = m.P(m.bg); g.gf = m.P(m.gf); g.bf = m.P(m.bf);
   g.k_steps[0] = m.d.k_cov; g.k_steps[1] = m.d.k_noncov; g.gn = m.gn;
   g.state = (float*)(ws + w.state); g.lat = (float*)(ws + w.lat); g.ld_lat = m.LW; g.err = err;
+  mark_stage(ST_GNN, st);
   int rc = launch_gnn(g, m.dpad, P, max_nodes, st);
+  mark_stage(ST_FUSION, st);
   if (rc || !want_pred) return rc;
   float* lat = (float*)(ws + w.lat);
   DenseArgs a{};
@@ -498,6 +514,14 @@ const char* fs_strerror(int code) {
 }
 
 int fs_version(void) { return 100; }
+
+long long fs_launch_count(void) { return g_launches.load(); }
+
+int fs_set_stage_events(void** events, int n) {
+  if (events && n < ST_COUNT) return FS_EINVAL;
+  g_stage_events = (cudaEvent_t*)events;
+  return FS_OK;
+}
 
 const char* fs_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
 
@@ -614,6 +638,7 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   if ((size_t)(W - (char*)ws) + w.total > ws_bytes) return FS_ECAPACITY;
   int64_t* node_off = (int64_t*)(W + w.node_off);
   int rc;
+  mark_stage(ST_FEATURIZE, st);
   FS_CUDA_CHECK(cudaMemsetAsync(err, 0, 4 * (size_t)P, st));
   if ((rc = launch_node_offsets(*b, node_off, W + w.scan, scan_ws_bytes(N > P ? N : P) + 1024, st))) return rc;
   const fs_model_desc& d = m->d;
@@ -646,7 +671,9 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   if ((rc = graph_head(*m, P, max_atoms, W, w, err, late || pred_g, st))) return rc;
   if (!late && (rc = fusion_head(*m, P, W, w, scores, st))) return rc;
   if ((rc = launch_finalize(P, d.fusion_mode, (float*)(W + w.pv), (float*)(W + w.pg), scores, err, st))) return rc;
-  return copy_outputs(*m, P, W, w, lat_v, lat_g, pred_v, pred_g, st);
+  rc = copy_outputs(*m, P, W, w, lat_v, lat_g, pred_v, pred_g, st);
+  mark_stage(ST_END, st);
+  return rc;
 }
 
 int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const double* grids,

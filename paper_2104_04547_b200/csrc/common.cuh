@@ -18,7 +18,19 @@ void set_cuda_error(cudaError_t e);
     if (_e != cudaSuccess) { ::fs::set_cuda_error(_e); return FS_ECUDA; } \
   } while (0)
 
-#define FS_LAUNCH_CHECK() FS_CUDA_CHECK(cudaGetLastError())
+// Kernel launches issued by the library (reported by fs_launch_count()).
+void count_launch();
+#define FS_LAUNCH_CHECK()            \
+  do {                               \
+    ::fs::count_launch();            \
+    FS_CUDA_CHECK(cudaGetLastError()); \
+  } while (0)
+
+// Optional per-stage CUDA events recorded on the launching stream
+// (fs_set_stage_events); stage ids below.
+enum Stage { ST_FEATURIZE = 0, ST_CONV1, ST_CONV2, ST_CONV3, ST_CONV4, ST_DENSE, ST_GNN, ST_FUSION, ST_END,
+             ST_COUNT };
+void mark_stage(int stage, cudaStream_t st);
 
 inline int cuda_status(cudaError_t e) {
   if (e != cudaSuccess) { set_cuda_error(e); return FS_ECUDA; }
