@@ -213,6 +213,13 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses,
                       float* lat_g, float* pred_v, float* pred_g, int32_t* err,
                       void* stream);
 
+/* Test hook: one tcgen05 Conv3d layer (1..4) of the bf16 voxel head on
+ * explicit buffers (bf16 NDHWC input).  Outputs: 1 -> bf16 [P,16^3,32];
+ * 2 -> bf16 max-pooled [P,8^3,32]; 3 -> bf16 [P,8^3,64]; 4 -> f32 pooled
+ * [P,4^3,64] with `residual` = bf16 [P,8^3,64] (h3) added after ReLU. */
+int fs_debug_conv(const fs_model* m, int layer, int32_t n_poses, const void* in,
+                  const void* residual, void* out, void* stream);
+
 /* ---- ranking (top-k merge; tie rule of evaluate.py:67-83) -------------- */
 /* Sorts the concatenation of (a) and (b) by (score desc, index asc) and keeps
  * the first k into (out_scores, out_idx).  NaN scores rank last.  Indices

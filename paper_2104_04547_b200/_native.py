@@ -31,7 +31,8 @@ EXPORTS = (
     "fs_model_destroy", "fs_model_supports", "fs_node_offsets", "fs_node_offsets_ws_bytes",
     "fs_voxelize", "fs_node_features", "fs_graph_count", "fs_graph_rows", "fs_graph_rows_ws_bytes",
     "fs_graph_fill", "fs_graph_edge_counts", "fs_graph_edges", "fs_workspace_bytes",
-    "fs_score_poses", "fs_score_features", "fs_topk_ws_bytes", "fs_topk_merge", "fs_best_pose",
+    "fs_score_poses", "fs_score_features", "fs_debug_conv", "fs_topk_ws_bytes", "fs_topk_merge",
+    "fs_best_pose",
 )
 
 
@@ -102,6 +103,7 @@ def _sig(lib):
         "fs_score_poses": (C.c_int, [_P, C.c_int, sp, _I64, _P, _SZ, _P, _P, _P, _P, _P, _P, _P]),
         "fs_score_features": (C.c_int, [_P, C.c_int, _I32, _P, _P, _P, _I64, _P, _I64, _P, _I64,
                                         _I32, _P, _SZ, _P, _P, _P, _P, _P, _P, _P]),
+        "fs_debug_conv": (C.c_int, [_P, C.c_int, _I32, _P, _P, _P, _P]),
         "fs_topk_ws_bytes": (_SZ, [_I64]),
         "fs_topk_merge": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _I32, _P, _P, _P, _SZ, _P]),
         "fs_best_pose": (C.c_int, [_P, _P, _P, _I64, _I64, _I32, _P, _P, _P]),

@@ -740,6 +740,16 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const d
                       pred_v, pred_g, st);
 }
 
+int fs_debug_conv(const fs_model* m, int layer, int32_t n_poses, const void* in, const void* residual, void* out,
+                  void* stream) {
+  if (!m || !in || !out || n_poses < 0) return FS_EINVAL;
+  if (!m->umma_ok) return FS_ENOTSUP;
+  const float* bias[5] = {nullptr, m->P(m->c1b), m->P(m->c2b), m->P(m->c3b), m->P(m->c4b)};
+  if (layer < 1 || layer > 4) return FS_EINVAL;
+  return umma::debug_layer(m->d, (const char*)m->blob + m->umma_off, bias[layer], nullptr, layer, n_poses, in,
+                           residual, out, (cudaStream_t)stream);
+}
+
 size_t fs_topk_ws_bytes(int64_t n) { return topk_ws_bytes(n); }
 
 int fs_topk_merge(const float* a_scores, const int64_t* a_idx, int64_t na, const float* b_scores,

@@ -1,17 +1,571 @@
-// tcgen05 implicit-GEMM Conv3d (placeholder until the UMMA kernels land).
+// tcgen05 (UMMA) implicit-GEMM Conv3d chain of the default voxel head:
+//   conv1 8->32 k5, conv2 32->32 k3 (+relu+2^3 max-pool), conv3 32->64 k3,
+//   conv4 64->64 k3 (+relu +residual h3 +2^3 max-pool)   (models.py:300-313)
+// bf16 operands, fp32 accumulation in TMEM, bias/ReLU/residual/pool fused in
+// the epilogue.  Reference op: conv3d (autodiff.py:208-232), cross-
+// correlation, stride 1, zero "same" padding.
+//
+// im2col-free design.  Every output plane d is one or two M=128 tiles whose
+// rows are output voxels (8 consecutive w) x 16 row groups ((h, pose)).  The
+// input planes d-r..d+r are staged by TMA into a shared-memory ring laid out
+// chunk-major: [8-channel chunk][h+2r][pose][w+2r] x 16 bytes (zero padding
+// comes from TMA out-of-bounds fill).  In that layout the A operand of
+// kernel offset (kd,kh,kw) is just a *shifted* K-major no-swizzle UMMA
+// descriptor: core-matrix rows (8 w) are 16 B apart, row groups (h,pose) are
+// SBO = (w+2r)*16 B apart, the two K chunks of one MMA are LBO apart.  So the
+// 27 (or 125) shifted GEMMs read the staged plane 27x from SMEM with zero
+// data movement -- HBM/L2 traffic is one read of each activation.
+//   16^3 layers: one pose per tile, 2 tiles (w halves) per plane.
+//   8^3 layers : two poses per tile, h rows of the pair interleaved (the TMA
+//                box spans (w, pose, h) so its dense fill is the interleave).
+// Warp roles (192 threads): warp0 = TMA producer, warp1 = TMEM owner + single
+// thread UMMA issuer, warps2-5 = epilogue (TMEM lane quadrant = warp % 4).
+// Persistent CTAs loop over units (pose or pose pair); weights stay resident.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <vector>
+
 #include "common.cuh"
 #include "umma_conv.cuh"
 
 namespace fs {
 namespace umma {
 
-bool supports(const fs_model_desc&) { return false; }
-size_t weights_bytes(const fs_model_desc&) { return 0; }
-void pack_weights(const fs_model_desc&, const double*, const double*, const double*, const double*, char*) {}
-size_t workspace_bytes(const fs_model_desc&, int64_t) { return 0; }
-int voxel_convs(const fs_model_desc&, const char*, const float*, const float*, const float*, const float*, int,
-                const __nv_bfloat16*, char*, float*, cudaStream_t) {
-  return FS_ENOTSUP;
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, SWIZZLE_NONE UMMA shared-memory descriptor (sm_100 version 1).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;
+}
+// kind::f16 instruction descriptor: BF16 x BF16 -> F32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__host__ __device__ constexpr int align_to(int x, int a) { return (x + a - 1) / a * a; }
+__host__ __device__ constexpr int pow2_cols(int x) {
+  return x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : x <= 256 ? 256 : 512;
+}
+
+// ---------------------------------------------------------------------------
+// layer configuration
+// ---------------------------------------------------------------------------
+template <int G_, int CIN_, int COUT_, int KS_, int POSES_, bool POOL_, bool RESID_, bool OUT_F32_, int NSPLIT_>
+struct Cfg {
+  static constexpr int G = G_, CIN = CIN_, COUT = COUT_, KS = KS_, POSES = POSES_, NSPLIT = NSPLIT_;
+  static constexpr bool POOL = POOL_, RESID = RESID_, OUT_F32 = OUT_F32_;
+  static constexpr int R = KS / 2;
+  static constexpr int HP = G + 2 * R, WP = G + 2 * R;
+  static constexpr int CHUNKS = CIN / 8;
+  static constexpr int TILES = G / 8;                      // w halves per plane
+  static_assert(G * POSES == 16, "M = 8 w x G h x POSES = 128");
+  static constexpr int BOX_BYTES = HP * POSES * WP * 16;  // one TMA box (8 channels)
+  static constexpr int CHUNK_BYTES = align_to(BOX_BYTES, 128);
+  static constexpr int PLANE_BYTES = CHUNKS * CHUNK_BYTES;
+  static constexpr int RING = KS + 1;
+  static constexpr int NCTA = COUT / NSPLIT;               // output channels per CTA
+  static constexpr int NG = NCTA / 8;
+  static constexpr int STEPS_PER_PLANE = (CIN == 8) ? (KS * KS + 1) / 2 : KS * KS * (CIN / 16);
+  static constexpr int KSTEPS = KS * STEPS_PER_PLANE;
+  static constexpr int W_BYTES = KSTEPS * 2 * NG * 128;    // per N slice
+  static constexpr int ACC_COLS = TILES * NCTA;
+  static constexpr int TMEM_COLS = pow2_cols(2 * ACC_COLS);
+  static constexpr int NPLANES = G + KS - 1;               // padded planes per unit
+  static constexpr uint32_t IDESC = idesc_bf16(128, NCTA);
+  static constexpr uint32_t SBO = WP * 16;
+  static constexpr int RING_OFF = align_to(W_BYTES, 1024);
+  static constexpr int BAR_OFF = RING_OFF + RING * PLANE_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
+// conv1 8->32 k5 on 16^3; conv2 32->32 k3 +pool; conv3 32->64 k3 (pose pairs);
+// conv4 64->64 k3 +residual +pool (pose pairs, N split over 2 CTAs).
+using C1 = Cfg<16, 8, 32, 5, 1, false, false, false, 1>;
+using C2 = Cfg<16, 32, 32, 3, 1, true, false, false, 1>;
+using C3 = Cfg<8, 32, 64, 3, 2, false, false, false, 1>;
+using C4 = Cfg<8, 64, 64, 3, 2, true, true, true, 2>;
+
+struct ConvParams {
+  const char* w;            // packed B operands, NSPLIT slices of W_BYTES
+  const float* bias;        // [COUT]
+  const __nv_bfloat16* residual;   // [P][G^3][COUT] (conv4: h3)
+  void* out;
+  int n_poses;
+};
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+template <class L>
+__global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant__ CUtensorMap tmap, ConvParams prm) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wsm = smem;
+  unsigned char* ring = smem + L::RING_OFF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* full = bars;                   // [RING]
+  uint64_t* empty = bars + L::RING;        // [RING]
+  uint64_t* tfull = bars + 2 * L::RING;    // [2]
+  uint64_t* tempty = tfull + 2;            // [2]
+  uint64_t* wbar = tempty + 2;             // [1]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wbar + 1);
+
+  const int nsl = blockIdx.y;              // N slice
+  const int n_units = (prm.n_poses + L::POSES - 1) / L::POSES;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < L::RING; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
+    mbar_init(wbar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const char* wsrc = prm.w + static_cast<size_t>(nsl) * L::W_BYTES;
+      mbar_expect_tx(wbar, L::W_BYTES);
+      for (int off = 0; off < L::W_BYTES; off += 32768) {
+        const int n = min(32768, L::W_BYTES - off);
+        bulk_load(wsm + off, wsrc + off, n, wbar);
+      }
+      uint32_t gq = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int p0 = u * L::POSES;
+        for (int q = 0; q < L::NPLANES; ++q, ++gq) {
+          const int slot = gq % L::RING;
+          mbar_wait(&empty[slot], ((gq / L::RING) & 1) ^ 1);
+          mbar_expect_tx(&full[slot], L::CHUNKS * L::BOX_BYTES);
+          unsigned char* dst = ring + slot * L::PLANE_BYTES;
+          for (int c = 0; c < L::CHUNKS; ++c)
+            tma_load_5d(dst + c * L::CHUNK_BYTES, &tmap, &full[slot], 8 * c, -L::R, p0, -L::R, q - L::R);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== UMMA issuer =====================
+    if (lane == 0) {
+      mbar_wait(wbar, 0);
+      const uint32_t wbase = smem_u32(wsm);
+      const uint32_t rbase = smem_u32(ring);
+      uint32_t gq0 = 0, ac = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        for (int d = 0; d < L::G; ++d, ++ac) {
+          // planes d .. d+KS-1 of this unit must be resident
+          const int qlo = d == 0 ? 0 : d + L::KS - 1;
+          for (int q = qlo; q <= d + L::KS - 1; ++q) {
+            const uint32_t g = gq0 + q;
+            mbar_wait(&full[g % L::RING], (g / L::RING) & 1);
+          }
+          const int a = ac & 1;
+          mbar_wait(&tempty[a], ((ac >> 1) & 1) ^ 1);
+          tc_fence_after();
+          for (int wh = 0; wh < L::TILES; ++wh) {
+            const uint32_t dtm = tmem_base + a * L::ACC_COLS + wh * L::NCTA;
+            uint32_t acc = 0;
+#pragma unroll 1
+            for (int kd = 0; kd < L::KS; ++kd) {
+              const uint32_t pbase = rbase + ((gq0 + d + kd) % L::RING) * L::PLANE_BYTES;
+#pragma unroll 1
+              for (int s = 0; s < L::STEPS_PER_PLANE; ++s) {
+                uint32_t a_addr, lbo;
+                if constexpr (L::CIN == 8) {
+                  const int oa = 2 * s, ob = 2 * s + 1;
+                  const int kha = oa / L::KS, kwa = oa % L::KS;
+                  a_addr = pbase + ((kha * L::POSES * L::WP) + wh * 8 + kwa) * 16;
+                  if (ob < L::KS * L::KS) {
+                    const int khb = ob / L::KS, kwb = ob % L::KS;
+                    lbo = ((khb - kha) * L::POSES * L::WP + (kwb - kwa)) * 16;
+                  } else {
+                    lbo = 16;   // zero-weight dummy chunk: any readable address
+                  }
+                } else {
+                  constexpr int CP = L::CIN / 16;
+                  const int cp = s % CP, off = s / CP;
+                  const int kh = off / L::KS, kw = off % L::KS;
+                  a_addr = pbase + (2 * cp) * L::CHUNK_BYTES + ((kh * L::POSES * L::WP) + wh * 8 + kw) * 16;
+                  lbo = L::CHUNK_BYTES;
+                }
+                const int ks = kd * L::STEPS_PER_PLANE + s;
+                const uint64_t ad = sdesc(a_addr, lbo, L::SBO);
+                const uint64_t bd = sdesc(wbase + ks * 2 * L::NG * 128, L::NG * 128, 128);
+                umma_bf16(dtm, ad, bd, L::IDESC, acc);
+                acc = 1;
+              }
+            }
+          }
+          umma_commit(&tfull[a]);
+          // padded plane d is not read by later outputs of this unit
+          umma_commit(&empty[(gq0 + d) % L::RING]);
+        }
+        for (int q = L::G; q < L::NPLANES; ++q) umma_commit(&empty[(gq0 + q) % L::RING]);
+        gq0 += L::NPLANES;
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;                 // tile row == TMEM lane
+    const int grp = r >> 3, wl = r & 7;
+    const int h = grp / L::POSES, ps = grp % L::POSES;
+    const int n0 = nsl * L::NCTA;
+    float bias[L::NCTA];
+#pragma unroll
+    for (int j = 0; j < L::NCTA; ++j) bias[j] = prm.bias[n0 + j];
+    float pmax[L::POOL ? L::TILES * L::NCTA : 1];
+    uint32_t ac = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int pose = u * L::POSES + ps;
+      const bool live = pose < prm.n_poses;
+      for (int d = 0; d < L::G; ++d, ++ac) {
+        const int a = ac & 1;
+        mbar_wait(&tfull[a], (ac >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int wh = 0; wh < L::TILES; ++wh) {
+          const int w = wh * 8 + wl;
+          float v[L::NCTA];
+#pragma unroll
+          for (int c0 = 0; c0 < L::NCTA; c0 += 32)
+            tmem_ld32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * L::ACC_COLS + wh * L::NCTA + c0,
+                      v + c0);
+#pragma unroll
+          for (int j = 0; j < L::NCTA; ++j) v[j] = fmaxf(v[j] + bias[j], 0.0f);
+          const size_t vox = ((static_cast<size_t>(pose) * L::G + d) * L::G + h) * L::G + w;
+          if constexpr (L::RESID) {
+            if (live) {
+              const uint4* rp = reinterpret_cast<const uint4*>(prm.residual + vox * L::COUT + n0);
+#pragma unroll
+              for (int q = 0; q < L::NCTA / 8; ++q) {
+                uint4 pk = rp[q];
+                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&pk);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  float2 f = __bfloat1622float2(b2[t]);
+                  v[q * 8 + 2 * t] += f.x;
+                  v[q * 8 + 2 * t + 1] += f.y;
+                }
+              }
+            }
+          }
+          if constexpr (L::POOL) {
+            constexpr int HX = 8 * L::POSES;        // lane distance of the h partner
+#pragma unroll
+            for (int j = 0; j < L::NCTA; ++j) {
+              float x = v[j];
+              x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 1));
+              x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, HX));
+              if (d & 1) x = fmaxf(x, pmax[wh * L::NCTA + j]);
+              pmax[wh * L::NCTA + j] = x;
+            }
+            if ((d & 1) && live && !(wl & 1) && !(h & 1)) {
+              constexpr int GO = L::G / 2;
+              const size_t ov = ((static_cast<size_t>(pose) * GO + d / 2) * GO + h / 2) * GO + w / 2;
+              if constexpr (L::OUT_F32) {
+                float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) + ov * L::COUT + n0);
+#pragma unroll
+                for (int q = 0; q < L::NCTA / 4; ++q)
+                  op[q] = make_float4(pmax[wh * L::NCTA + 4 * q], pmax[wh * L::NCTA + 4 * q + 1],
+                                      pmax[wh * L::NCTA + 4 * q + 2], pmax[wh * L::NCTA + 4 * q + 3]);
+              } else {
+                uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) + ov * L::COUT + n0);
+#pragma unroll
+                for (int q = 0; q < L::NCTA / 8; ++q) {
+                  uint4 pk;
+                  __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+                  for (int t = 0; t < 4; ++t)
+                    b2[t] = __floats2bfloat162_rn(pmax[wh * L::NCTA + q * 8 + 2 * t],
+                                                  pmax[wh * L::NCTA + q * 8 + 2 * t + 1]);
+                  op[q] = pk;
+                }
+              }
+            }
+          } else if (live) {
+            uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) + vox * L::COUT + n0);
+#pragma unroll
+            for (int q = 0; q < L::NCTA / 8; ++q) {
+              uint4 pk;
+              __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+              for (int t = 0; t < 4; ++t) b2[t] = __floats2bfloat162_rn(v[q * 8 + 2 * t], v[q * 8 + 2 * t + 1]);
+              op[q] = pk;
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[a]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 5-D map over an NDHWC bf16 activation [P][G][G][G][C] with dimension order
+// (c, w, pose, h, d) so one box fills the (h, pose, w) interleave directly.
+template <class L>
+static int make_map(CUtensorMap* map, const void* base, int n_poses) {
+  auto fn = encode_fn();
+  if (!fn) return FS_ECUDA;
+  const cuuint64_t G = L::G, C = L::CIN;
+  cuuint64_t dims[5] = {C, G, static_cast<cuuint64_t>(n_poses), G, G};
+  cuuint64_t strides[4] = {C * 2, G * G * G * C * 2, G * C * 2, G * G * C * 2};
+  cuuint32_t box[5] = {8, static_cast<cuuint32_t>(L::WP), static_cast<cuuint32_t>(L::POSES),
+                       static_cast<cuuint32_t>(L::HP), 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? FS_OK : FS_ECUDA;
+}
+
+static int g_num_sms = 0;
+
+template <class L>
+static int launch_layer(const void* in, ConvParams prm, cudaStream_t st) {
+  if (prm.n_poses <= 0) return FS_OK;
+  CUtensorMap map;
+  int rc = make_map<L>(&map, in, prm.n_poses);
+  if (rc) return rc;
+  if (!g_num_sms) {
+    int dev = 0;
+    FS_CUDA_CHECK(cudaGetDevice(&dev));
+    FS_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  FS_CUDA_CHECK(cudaFuncSetAttribute(conv_umma_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
+  const int units = (prm.n_poses + L::POSES - 1) / L::POSES;
+  const int per_sm = (227 * 1024) / (L::SMEM + 1024) >= 2 ? 2 : 1;
+  const int ctas = max(1, min(units, g_num_sms * per_sm / L::NSPLIT));
+  dim3 grid(ctas, L::NSPLIT);
+  conv_umma_kernel<L><<<grid, 192, L::SMEM, st>>>(map, prm);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
+bool supports(const fs_model_desc& d) {
+  return d.grid_extent == 16 && d.in_channels == 8 && d.conv_filters_1 == 32 && d.conv_filters_2 == 64 &&
+         d.kernel_1 == 5 && d.kernel_2 == 3 && !d.residual_1 && d.residual_2 && !d.batch_norm;
+}
+
+static constexpr size_t OFF_W1 = 0;
+static constexpr size_t OFF_W2 = align_to(C1::W_BYTES * C1::NSPLIT, 1024);
+static constexpr size_t OFF_W3 = OFF_W2 + align_to(C2::W_BYTES * C2::NSPLIT, 1024);
+static constexpr size_t OFF_W4 = OFF_W3 + align_to(C3::W_BYTES * C3::NSPLIT, 1024);
+static constexpr size_t W_TOTAL = OFF_W4 + align_to(C4::W_BYTES * C4::NSPLIT, 1024);
+
+size_t weights_bytes(const fs_model_desc& d) { return supports(d) ? W_TOTAL : 0; }
+
+static uint16_t to_bf16(double x) {
+  float f = static_cast<float>(x);
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return static_cast<uint16_t>(u >> 16);   // inf/nan
+  u += 0x7fffu + ((u >> 16) & 1u);                                                  // RNE
+  return static_cast<uint16_t>(u >> 16);
+}
+
+// B operand layout per N slice: [kstep][kchunk 2][n-group][8 rows][8 ch] bf16.
+template <class L>
+static void pack_layer(const double* w, char* out) {
+  // w: reference [O][C][k][k][k]
+  const int K = L::KS, C = L::CIN;
+  for (int sl = 0; sl < L::NSPLIT; ++sl) {
+    uint16_t* o = reinterpret_cast<uint16_t*>(out + static_cast<size_t>(sl) * L::W_BYTES);
+    std::memset(o, 0, L::W_BYTES);
+    for (int kd = 0; kd < K; ++kd)
+      for (int s = 0; s < L::STEPS_PER_PLANE; ++s)
+        for (int kc = 0; kc < 2; ++kc) {
+          int kh, kw, c0;
+          if constexpr (L::CIN == 8) {
+            const int off = 2 * s + kc;
+            if (off >= K * K) continue;     // zero-weight dummy chunk
+            kh = off / K; kw = off % K; c0 = 0;
+          } else {
+            constexpr int CP = L::CIN / 16;
+            const int cp = s % CP, off = s / CP;
+            kh = off / K; kw = off % K; c0 = 16 * cp + 8 * kc;
+          }
+          const int ks = kd * L::STEPS_PER_PLANE + s;
+          for (int n = 0; n < L::NCTA; ++n) {
+            const int oc = sl * L::NCTA + n;
+            const size_t core = (static_cast<size_t>(ks) * 2 + kc) * L::NG + n / 8;
+            for (int e = 0; e < 8; ++e) {
+              const int ic = c0 + e;
+              const double v = w[((((size_t)oc * C + ic) * K + kd) * K + kh) * K + kw];
+              o[core * 64 + (n % 8) * 8 + e] = to_bf16(v);
+            }
+          }
+        }
+  }
+}
+
+void pack_weights(const fs_model_desc& d, const double* c1, const double* c2, const double* c3, const double* c4,
+                  char* out) {
+  if (!supports(d) || !c1 || !c2 || !c3 || !c4) return;
+  pack_layer<C1>(c1, out + OFF_W1);
+  pack_layer<C2>(c2, out + OFF_W2);
+  pack_layer<C3>(c3, out + OFF_W3);
+  pack_layer<C4>(c4, out + OFF_W4);
+}
+
+// act1 [P][16^3][32] bf16, act2 (pooled) [P][8^3][32] bf16, act3 [P][8^3][64] bf16
+static size_t act1_bytes(int64_t P) { return static_cast<size_t>(P) * 4096 * 32 * 2; }
+static size_t act2_bytes(int64_t P) { return static_cast<size_t>(P + 1) * 512 * 32 * 2; }
+static size_t act3_bytes(int64_t P) { return static_cast<size_t>(P + 1) * 512 * 64 * 2; }
+
+size_t workspace_bytes(const fs_model_desc& d, int64_t P) {
+  if (!supports(d)) return 0;
+  return act1_bytes(P) + act2_bytes(P) + act3_bytes(P) + 4096;
+}
+
+int voxel_convs(const fs_model_desc& d, const char* wblob, const float* b1, const float* b2, const float* b3,
+                const float* b4, int P, const __nv_bfloat16* grid, char* ws, float* flat_out, cudaStream_t st) {
+  if (!supports(d)) return FS_ENOTSUP;
+  if (P <= 0) return FS_OK;
+  char* a1 = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 1023) & ~static_cast<uintptr_t>(1023));
+  char* a2 = a1 + act1_bytes(P);
+  char* a3 = a2 + act2_bytes(P);
+  int rc;
+  ConvParams p{};
+  p.n_poses = P;
+  mark_stage(ST_CONV1, st);
+  p.w = wblob + OFF_W1; p.bias = b1; p.out = a1;
+  if ((rc = launch_layer<C1>(grid, p, st))) return rc;
+  mark_stage(ST_CONV2, st);
+  p.w = wblob + OFF_W2; p.bias = b2; p.out = a2;
+  if ((rc = launch_layer<C2>(a1, p, st))) return rc;
+  mark_stage(ST_CONV3, st);
+  p.w = wblob + OFF_W3; p.bias = b3; p.out = a3;
+  if ((rc = launch_layer<C3>(a2, p, st))) return rc;
+  mark_stage(ST_CONV4, st);
+  p.w = wblob + OFF_W4; p.bias = b4; p.out = flat_out; p.residual = reinterpret_cast<const __nv_bfloat16*>(a3);
+  if ((rc = launch_layer<C4>(a3, p, st))) return rc;
+  return FS_OK;
+}
+
+int debug_layer(const fs_model_desc& d, const char* wblob, const float* bias, const float* residual_unused,
+                int layer, int P, const void* in, const void* residual, void* out, cudaStream_t st) {
+  (void)residual_unused;
+  if (!supports(d)) return FS_ENOTSUP;
+  ConvParams p{};
+  p.n_poses = P; p.bias = bias; p.out = out;
+  p.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
+  switch (layer) {
+    case 1: p.w = wblob + OFF_W1; return launch_layer<C1>(in, p, st);
+    case 2: p.w = wblob + OFF_W2; return launch_layer<C2>(in, p, st);
+    case 3: p.w = wblob + OFF_W3; return launch_layer<C3>(in, p, st);
+    case 4: p.w = wblob + OFF_W4; return launch_layer<C4>(in, p, st);
+    default: return FS_EINVAL;
+  }
 }
 
 }  // namespace umma

@@ -24,5 +24,9 @@ int voxel_convs(const fs_model_desc& d, const char* wblob, const float* b1, cons
                 const float* b3, const float* b4, int n_poses, const __nv_bfloat16* grid, char* ws,
                 float* flat_out, cudaStream_t st);
 
+// One layer (1..4) on explicit buffers, for per-layer parity tests.
+int debug_layer(const fs_model_desc& d, const char* wblob, const float* bias, const float* unused, int layer, int P,
+                const void* in, const void* residual, void* out, cudaStream_t st);
+
 }  // namespace umma
 }  // namespace fs

@@ -1,0 +1,116 @@
+"""tcgen05 (UMMA) Conv3d layers and the bf16 tensor-core scoring path.
+
+Per layer: the CUDA kernel (through fs_debug_conv) against a plain PyTorch
+float64 reference of the same op on the same bf16-rounded operands.  bf16
+products are exact in fp32, so the only differences are fp32 accumulation
+order (~1e-6) and the bf16 rounding of stored outputs (<= 2^-8 relative).
+End to end: bf16 scores within the stated tolerance of the fp32 path."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def setup():
+    import torch
+
+    from paper_2104_04547_b200 import _native as N
+    from paper_2104_04547_b200 import models
+    m = models.FusionModel(models.VoxelHeadConfig(), models.GraphHeadConfig(),
+                           models.table_coherent_fusion_config(), seed=0)
+    dm = m.device_model()
+    if not dm.supports("bf16"):
+        pytest.skip("bf16 tcgen05 path not available")
+    return torch, N, m, dm
+
+
+def _ref_layer(torch, w, b, x, pool=False, residual=None):
+    """float64 conv3d (cross-correlation, same padding) + bias + relu [+res] [+pool]."""
+    import torch.nn.functional as F
+    wt = torch.from_numpy(w).to(torch.bfloat16).to(torch.float64)
+    xt = x.to(torch.float64).permute(0, 4, 1, 2, 3).cpu()
+    y = F.conv3d(xt, wt, torch.from_numpy(b).to(torch.float32).to(torch.float64), padding=w.shape[2] // 2)
+    y = torch.relu(y)
+    if residual is not None:
+        y = y + residual.to(torch.float64).permute(0, 4, 1, 2, 3).cpu()
+    if pool:
+        y = F.max_pool3d(y, 2)
+    return y.permute(0, 2, 3, 4, 1).contiguous()
+
+
+@pytest.mark.parametrize("layer", [1, 2, 3, 4])
+def test_umma_layer_matches_torch_reference(setup, layer):
+    torch, N, m, dm = setup
+    P = 5                          # odd: exercises the pose-pair tail of layers 3/4
+    g = torch.Generator(device="cpu").manual_seed(layer)
+    vp = m.voxel_params
+    if layer == 1:
+        x = torch.randint(0, 3, (P, 16, 16, 16, 8), generator=g).to(torch.bfloat16)
+        out = torch.empty((P, 16, 16, 16, 32), dtype=torch.bfloat16, device="cuda")
+        want = _ref_layer(torch, vp["conv1_w"], vp["conv1_b"], x)
+    elif layer == 2:
+        x = torch.rand((P, 16, 16, 16, 32), generator=g).to(torch.bfloat16)
+        out = torch.empty((P, 8, 8, 8, 32), dtype=torch.bfloat16, device="cuda")
+        want = _ref_layer(torch, vp["conv2_w"], vp["conv2_b"], x, pool=True)
+    elif layer == 3:
+        x = torch.rand((P, 8, 8, 8, 32), generator=g).to(torch.bfloat16)
+        out = torch.empty((P, 8, 8, 8, 64), dtype=torch.bfloat16, device="cuda")
+        want = _ref_layer(torch, vp["conv3_w"], vp["conv3_b"], x)
+    else:
+        x = torch.rand((P, 8, 8, 8, 64), generator=g).to(torch.bfloat16)
+        res = torch.rand((P, 8, 8, 8, 64), generator=g).to(torch.bfloat16)
+        out = torch.empty((P, 4, 4, 4, 64), dtype=torch.float32, device="cuda")
+        want = _ref_layer(torch, vp["conv4_w"], vp["conv4_b"], x, pool=True, residual=res)
+    xd = x.cuda()
+    rd = res.cuda() if layer == 4 else None
+    L = N.lib()
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    N.check(L.fs_debug_conv(dm.handle, layer, P, C.c_void_p(xd.data_ptr()),
+                            C.c_void_p(rd.data_ptr() if rd is not None else 0), C.c_void_p(out.data_ptr()),
+                            stream), "fs_debug_conv")
+    torch.cuda.synchronize()
+    got = out.to(torch.float64).cpu()
+    err = (got - want).abs()
+    tol = (2.0 ** -8) * want.abs() + 2e-3 if layer < 4 else 1e-4 * want.abs() + 1e-4
+    bad = int((err > tol).sum())
+    assert bad == 0, f"layer {layer}: {bad} of {err.numel()} outside tol; max err {float(err.max()):.3e}"
+
+
+def test_bf16_scores_within_stated_tolerance(setup):
+    """Stated bf16 tolerance: max relative error <= 3e-2 vs the
+    fp32 path and centred-score Pearson >= 0.99 over a 512-pose screen."""
+    torch, N, m, dm = setup
+    from paper_2104_04547_b200 import engine as E
+    from paper_2104_04547_b200 import synth
+    pocket = synth.make_pocket(1000, seed=5)
+    lib = synth.make_poses(52, poses_per_compound=10, seed=6).slice(0, 512)
+    b = E.batch_from_arrays(lib.xyz, lib.elem, lib.role, lib.atom_off,
+                            pocket=(pocket.xyz, pocket.elem, pocket.role, np.array([0, 1000])),
+                            pose_target=lib.target)
+    s32 = dm.score_poses(b, "fp32")["scores"].cpu().numpy().astype(np.float64)
+    s16 = dm.score_poses(b, "bf16")["scores"].cpu().numpy().astype(np.float64)
+    rel = np.max(np.abs(s16 - s32) / np.abs(s32))
+    pear = np.corrcoef(s16 - s16.mean(), s32 - s32.mean())[0, 1]
+    print(f"bf16 vs fp32: max rel {rel:.3e}, centred Pearson {pear:.5f}")
+    assert rel <= 3e-2
+    assert pear >= 0.99
+
+
+def test_bf16_batch_invariance_bitwise(setup):
+    torch, N, m, dm = setup
+    from paper_2104_04547_b200 import engine as E
+    from paper_2104_04547_b200 import synth
+    pocket = synth.make_pocket(1000, seed=7)
+    lib = synth.make_poses(3, poses_per_compound=3, seed=8)
+    pk = (pocket.xyz, pocket.elem, pocket.role, np.array([0, 1000]))
+    whole = dm.score_poses(E.batch_from_arrays(lib.xyz, lib.elem, lib.role, lib.atom_off, pocket=pk,
+                                               pose_target=lib.target), "bf16")["scores"].cpu().numpy()
+    for s, e in ((0, 1), (2, 5), (8, 9)):
+        part = lib.slice(s, e)
+        got = dm.score_poses(E.batch_from_arrays(part.xyz, part.elem, part.role, part.atom_off, pocket=pk,
+                                                 pose_target=part.target), "bf16")["scores"].cpu().numpy()
+        assert np.array_equal(got, whole[s:e])
