@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -266,7 +267,10 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
                     const int khb = ob / L::KS, kwb = ob % L::KS;
                     lbo = ((khb - kha) * L::POSES * L::WP + (kwb - kwa)) * 16;
                   } else {
-                    lbo = 16;   // zero-weight dummy chunk: any readable address
+                    // zero-weight dummy chunk: LBO 0 re-reads chunk 0, which is
+                    // finite data (a past-the-plane read could hit mbarrier words
+                    // whose bit patterns are NaN, and 0*NaN = NaN)
+                    lbo = 0;
                   }
                 } else {
                   constexpr int CP = L::CIN / 16;
@@ -443,7 +447,8 @@ static int launch_layer(const void* in, ConvParams prm, cudaStream_t st) {
   }
   FS_CUDA_CHECK(cudaFuncSetAttribute(conv_umma_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
   const int units = (prm.n_poses + L::POSES - 1) / L::POSES;
-  const int per_sm = (227 * 1024) / (L::SMEM + 1024) >= 2 ? 2 : 1;
+  static const bool one_per_sm = getenv("FS_UMMA_ONE_CTA_PER_SM") != nullptr;
+  const int per_sm = (!one_per_sm && (227 * 1024) / (L::SMEM + 1024) >= 2) ? 2 : 1;
   const int ctas = max(1, min(units, g_num_sms * per_sm / L::NSPLIT));
   dim3 grid(ctas, L::NSPLIT);
   conv_umma_kernel<L><<<grid, 192, L::SMEM, st>>>(map, prm);
