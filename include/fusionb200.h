@@ -214,9 +214,11 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses,
                       void* stream);
 
 /* Test hook: one tcgen05 Conv3d layer (1..4) of the bf16 voxel head on
- * explicit buffers (bf16 NDHWC input).  Outputs: 1 -> bf16 [P,16^3,32];
- * 2 -> bf16 max-pooled [P,8^3,32]; 3 -> bf16 [P,8^3,64]; 4 -> f32 pooled
- * [P,4^3,64] with `residual` = bf16 [P,8^3,64] (h3) added after ReLU. */
+ * explicit buffers.  bf16 activations are chunk-major [P][C/8][D][H][W][8]
+ * (layer 1 input = the NDHWC bf16 voxel grid, C = 8).  Outputs: 1 -> bf16
+ * [P,4,16,16,16,8]; 2 -> bf16 max-pooled [P,4,8,8,8,8]; 3 -> bf16
+ * [P,8,8,8,8,8]; 4 -> f32 pooled NDHWC [P,4,4,4,64] with `residual` = layer-3
+ * output (h3) added after ReLU. */
 int fs_debug_conv(const fs_model* m, int layer, int32_t n_poses, const void* in,
                   const void* residual, void* out, void* stream);
 

@@ -166,6 +166,30 @@ using C2 = Cfg<16, 32, 32, 3, 1, true, false, false, 1>;
 using C3 = Cfg<8, 32, 64, 3, 2, false, false, false, 1>;
 using C4 = Cfg<8, 64, 64, 3, 2, true, true, true, 2>;
 
+// Per K-step A-descriptor low word (start-address and LBO fields, 16-byte
+// units) relative to the plane base of the step's kd.
+template <class L>
+__host__ __device__ constexpr uint32_t a_step_lo(int s) {
+  if constexpr (L::CIN == 8) {
+    // two kernel offsets of the same kd plane per MMA (8 channels each)
+    const int oa = 2 * s, ob = 2 * s + 1;
+    const int kha = oa / L::KS, kwa = oa % L::KS;
+    const int off = (kha * L::POSES * L::WP + kwa) * 16;
+    // zero-weight dummy second chunk: LBO 0 re-reads chunk 0, which is finite
+    // data (a past-the-plane read could hit mbarrier words whose bit patterns
+    // are NaN, and 0*NaN = NaN)
+    const int lbo = ob < L::KS * L::KS
+                        ? ((ob / L::KS - kha) * L::POSES * L::WP + (ob % L::KS - kwa)) * 16 : 0;
+    return static_cast<uint32_t>(off >> 4) | (static_cast<uint32_t>(lbo >> 4) << 16);
+  } else {
+    // one kernel offset, channel chunks (2cp, 2cp+1) per MMA (LBO = chunk stride)
+    constexpr int CP = L::CIN / 16;
+    const int cp = s % CP, o = s / CP;
+    const int off = (2 * cp) * L::CHUNK_BYTES + ((o / L::KS) * L::POSES * L::WP + (o % L::KS)) * 16;
+    return static_cast<uint32_t>(off >> 4);
+  }
+}
+
 struct ConvParams {
   const char* w;            // packed B operands, NSPLIT slices of W_BYTES
   const float* bias;        // [COUT]
@@ -228,72 +252,65 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
           mbar_expect_tx(&full[slot], L::CHUNKS * L::BOX_BYTES);
           unsigned char* dst = ring + slot * L::PLANE_BYTES;
           for (int c = 0; c < L::CHUNKS; ++c)
-            tma_load_5d(dst + c * L::CHUNK_BYTES, &tmap, &full[slot], 8 * c, -L::R, p0, -L::R, q - L::R);
+            tma_load_5d(dst + c * L::CHUNK_BYTES, &tmap, &full[slot], -8 * L::R, p0, -L::R, q - L::R, c);
         }
       }
     }
   } else if (warp == 1) {
     // ===================== UMMA issuer =====================
-    if (lane == 0) {
-      mbar_wait(wbar, 0);
-      const uint32_t wbase = smem_u32(wsm);
-      const uint32_t rbase = smem_u32(ring);
-      uint32_t gq0 = 0, ac = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        for (int d = 0; d < L::G; ++d, ++ac) {
-          // planes d .. d+KS-1 of this unit must be resident
-          const int qlo = d == 0 ? 0 : d + L::KS - 1;
-          for (int q = qlo; q <= d + L::KS - 1; ++q) {
-            const uint32_t g = gq0 + q;
-            mbar_wait(&full[g % L::RING], (g / L::RING) & 1);
-          }
-          const int a = ac & 1;
-          mbar_wait(&tempty[a], ((ac >> 1) & 1) ^ 1);
-          tc_fence_after();
-          for (int wh = 0; wh < L::TILES; ++wh) {
-            const uint32_t dtm = tmem_base + a * L::ACC_COLS + wh * L::NCTA;
-            uint32_t acc = 0;
-#pragma unroll 1
-            for (int kd = 0; kd < L::KS; ++kd) {
-              const uint32_t pbase = rbase + ((gq0 + d + kd) % L::RING) * L::PLANE_BYTES;
-#pragma unroll 1
-              for (int s = 0; s < L::STEPS_PER_PLANE; ++s) {
-                uint32_t a_addr, lbo;
-                if constexpr (L::CIN == 8) {
-                  const int oa = 2 * s, ob = 2 * s + 1;
-                  const int kha = oa / L::KS, kwa = oa % L::KS;
-                  a_addr = pbase + ((kha * L::POSES * L::WP) + wh * 8 + kwa) * 16;
-                  if (ob < L::KS * L::KS) {
-                    const int khb = ob / L::KS, kwb = ob % L::KS;
-                    lbo = ((khb - kha) * L::POSES * L::WP + (kwb - kwa)) * 16;
-                  } else {
-                    // zero-weight dummy chunk: LBO 0 re-reads chunk 0, which is
-                    // finite data (a past-the-plane read could hit mbarrier words
-                    // whose bit patterns are NaN, and 0*NaN = NaN)
-                    lbo = 0;
-                  }
-                } else {
-                  constexpr int CP = L::CIN / 16;
-                  const int cp = s % CP, off = s / CP;
-                  const int kh = off / L::KS, kw = off % L::KS;
-                  a_addr = pbase + (2 * cp) * L::CHUNK_BYTES + ((kh * L::POSES * L::WP) + wh * 8 + kw) * 16;
-                  lbo = L::CHUNK_BYTES;
-                }
-                const int ks = kd * L::STEPS_PER_PLANE + s;
-                const uint64_t ad = sdesc(a_addr, lbo, L::SBO);
-                const uint64_t bd = sdesc(wbase + ks * 2 * L::NG * 128, L::NG * 128, 128);
-                umma_bf16(dtm, ad, bd, L::IDESC, acc);
-                acc = 1;
-              }
+    // The whole warp walks the schedule (so descriptor math stays warp-
+    // uniform) and lane 0 issues.  Descriptor words are built from
+    // compile-time per-step offsets: one integer add per MMA.
+    mbar_wait(wbar, 0);
+    const uint32_t wbase = smem_u32(wsm);
+    const uint32_t rbase = smem_u32(ring);
+    constexpr uint32_t A_HI = ((L::SBO >> 4) & 0x3FFFu) | (1u << 14);
+    constexpr uint32_t B_HI = (128u >> 4) | (1u << 14);
+    constexpr uint32_t A_LBO = (L::CIN == 8) ? 0u : ((static_cast<uint32_t>(L::CHUNK_BYTES) >> 4) << 16);
+    constexpr uint32_t B_STEP = (2u * L::NG * 128u) >> 4;
+    const uint32_t b_lo0 = ((wbase >> 4) & 0x3FFFu) | (((L::NG * 128u) >> 4) << 16);
+    uint32_t gq0 = 0, ac = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      for (int d = 0; d < L::G; ++d, ++ac) {
+        // planes d .. d+KS-1 of this unit must be resident
+        const int qlo = d == 0 ? 0 : d + L::KS - 1;
+        for (int q = qlo; q <= d + L::KS - 1; ++q) {
+          const uint32_t g = gq0 + q;
+          mbar_wait(&full[g % L::RING], (g / L::RING) & 1);
+        }
+        const int a = ac & 1;
+        mbar_wait(&tempty[a], ((ac >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t slot0 = (gq0 + d) % L::RING;
+#pragma unroll
+        for (int wh = 0; wh < L::TILES; ++wh) {
+          const uint32_t dtm = tmem_base + a * L::ACC_COLS + wh * L::NCTA;
+#pragma unroll
+          for (int kd = 0; kd < L::KS; ++kd) {
+            uint32_t slot = slot0 + kd;
+            if (slot >= static_cast<uint32_t>(L::RING)) slot -= L::RING;
+            const uint32_t a_lo0 = (((rbase + slot * L::PLANE_BYTES + wh * 128u) >> 4) & 0x3FFFu) | A_LBO;
+#pragma unroll
+            for (int s2 = 0; s2 < L::STEPS_PER_PLANE; ++s2) {
+              const uint32_t a_lo = a_lo0 + a_step_lo<L>(s2);
+              const uint32_t b_lo = b_lo0 + (kd * L::STEPS_PER_PLANE + s2) * B_STEP;
+              if (lane == 0)
+                umma_bf16(dtm, (static_cast<uint64_t>(A_HI) << 32) | a_lo,
+                          (static_cast<uint64_t>(B_HI) << 32) | b_lo, L::IDESC, (kd | s2) != 0 ? 1u : 0u);
             }
           }
+        }
+        if (lane == 0) {
           umma_commit(&tfull[a]);
           // padded plane d is not read by later outputs of this unit
-          umma_commit(&empty[(gq0 + d) % L::RING]);
+          umma_commit(&empty[slot0]);
         }
-        for (int q = L::G; q < L::NPLANES; ++q) umma_commit(&empty[(gq0 + q) % L::RING]);
-        gq0 += L::NPLANES;
+        __syncwarp();
       }
+      if (lane == 0)
+        for (int q = L::G; q < L::NPLANES; ++q) umma_commit(&empty[(gq0 + q) % L::RING]);
+      __syncwarp();
+      gq0 += L::NPLANES;
     }
   } else {
     // ===================== epilogue (warps 2..5) =====================
@@ -324,13 +341,16 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
                       v + c0);
 #pragma unroll
           for (int j = 0; j < L::NCTA; ++j) v[j] = fmaxf(v[j] + bias[j], 0.0f);
-          const size_t vox = ((static_cast<size_t>(pose) * L::G + d) * L::G + h) * L::G + w;
+          // chunk-major activations: [pose][C/8][d][h][w][8]
+          constexpr size_t G3 = static_cast<size_t>(L::G) * L::G * L::G;
+          const size_t vox = (static_cast<size_t>(d) * L::G + h) * L::G + w;
           if constexpr (L::RESID) {
             if (live) {
-              const uint4* rp = reinterpret_cast<const uint4*>(prm.residual + vox * L::COUT + n0);
+              const uint4* rp = reinterpret_cast<const uint4*>(prm.residual) +
+                                (static_cast<size_t>(pose) * (L::COUT / 8) + n0 / 8) * G3 + vox;
 #pragma unroll
               for (int q = 0; q < L::NCTA / 8; ++q) {
-                uint4 pk = rp[q];
+                uint4 pk = rp[q * G3];
                 const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&pk);
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
@@ -353,15 +373,19 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
             }
             if ((d & 1) && live && !(wl & 1) && !(h & 1)) {
               constexpr int GO = L::G / 2;
-              const size_t ov = ((static_cast<size_t>(pose) * GO + d / 2) * GO + h / 2) * GO + w / 2;
               if constexpr (L::OUT_F32) {
+                // final layer: NDHWC float32 (the dense1 flatten order)
+                const size_t ov = ((static_cast<size_t>(pose) * GO + d / 2) * GO + h / 2) * GO + w / 2;
                 float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) + ov * L::COUT + n0);
 #pragma unroll
                 for (int q = 0; q < L::NCTA / 4; ++q)
                   op[q] = make_float4(pmax[wh * L::NCTA + 4 * q], pmax[wh * L::NCTA + 4 * q + 1],
                                       pmax[wh * L::NCTA + 4 * q + 2], pmax[wh * L::NCTA + 4 * q + 3]);
               } else {
-                uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) + ov * L::COUT + n0);
+                constexpr size_t GO3 = static_cast<size_t>(GO) * GO * GO;
+                const size_t ovx = (static_cast<size_t>(d / 2) * GO + h / 2) * GO + w / 2;
+                uint4* op = reinterpret_cast<uint4*>(prm.out) +
+                            (static_cast<size_t>(pose) * (L::COUT / 8) + n0 / 8) * GO3 + ovx;
 #pragma unroll
                 for (int q = 0; q < L::NCTA / 8; ++q) {
                   uint4 pk;
@@ -370,19 +394,19 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
                   for (int t = 0; t < 4; ++t)
                     b2[t] = __floats2bfloat162_rn(pmax[wh * L::NCTA + q * 8 + 2 * t],
                                                   pmax[wh * L::NCTA + q * 8 + 2 * t + 1]);
-                  op[q] = pk;
+                  op[q * GO3] = pk;
                 }
               }
             }
           } else if (live) {
-            uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) + vox * L::COUT + n0);
+            uint4* op = reinterpret_cast<uint4*>(prm.out) + (static_cast<size_t>(pose) * (L::COUT / 8) + n0 / 8) * G3 + vox;
 #pragma unroll
             for (int q = 0; q < L::NCTA / 8; ++q) {
               uint4 pk;
               __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&pk);
 #pragma unroll
               for (int t = 0; t < 4; ++t) b2[t] = __floats2bfloat162_rn(v[q * 8 + 2 * t], v[q * 8 + 2 * t + 1]);
-              op[q] = pk;
+              op[q * G3] = pk;
             }
           }
         }
@@ -414,17 +438,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 5-D map over an NDHWC bf16 activation [P][G][G][G][C] with dimension order
-// (c, w, pose, h, d) so one box fills the (h, pose, w) interleave directly.
+// 5-D map over a chunk-major bf16 activation [P][C/8][G][G][G][8] with
+// dimension order ((w,c8), pose, h, d, chunk): the innermost box row is a
+// whole padded w-row of one chunk (WP*16 bytes, not 16), and putting pose
+// between (w,c8) and h makes one box fill the (h, pose, w) interleave.
 template <class L>
 static int make_map(CUtensorMap* map, const void* base, int n_poses) {
   auto fn = encode_fn();
   if (!fn) return FS_ECUDA;
-  const cuuint64_t G = L::G, C = L::CIN;
-  cuuint64_t dims[5] = {C, G, static_cast<cuuint64_t>(n_poses), G, G};
-  cuuint64_t strides[4] = {C * 2, G * G * G * C * 2, G * C * 2, G * G * C * 2};
-  cuuint32_t box[5] = {8, static_cast<cuuint32_t>(L::WP), static_cast<cuuint32_t>(L::POSES),
-                       static_cast<cuuint32_t>(L::HP), 1};
+  const cuuint64_t G = L::G, CH = L::CIN / 8;
+  cuuint64_t dims[5] = {G * 8, static_cast<cuuint64_t>(n_poses), G, G, CH};
+  cuuint64_t strides[4] = {CH * G * G * G * 16, G * 16, G * G * 16, G * G * G * 16};
+  cuuint32_t box[5] = {static_cast<cuuint32_t>(L::WP * 8), static_cast<cuuint32_t>(L::POSES),
+                       static_cast<cuuint32_t>(L::HP), 1, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,

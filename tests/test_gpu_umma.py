@@ -71,8 +71,13 @@ def test_umma_layer_matches_torch_reference(setup, layer, P):
         out = torch.empty((P, 4, 4, 4, 64), dtype=torch.float32, device="cuda")
         ref = lambda sel: _ref_layer(torch, vp["conv4_w"], vp["conv4_b"], x, pool=True, residual=res,  # noqa: E731
                                      sel=sel)
-    xd = x.cuda()
-    rd = res.cuda() if layer == 4 else None
+    # device layout of bf16 activations is chunk-major [P][C/8][D][H][W][8]
+    to_cm = lambda t: t.view(*t.shape[:4], t.shape[4] // 8, 8).permute(0, 4, 1, 2, 3, 5).contiguous()  # noqa: E731
+    xd = to_cm(x).cuda()
+    rd = to_cm(res).cuda() if layer == 4 else None
+    if layer < 4:
+        shp = out.shape
+        out = torch.empty((shp[0], shp[4] // 8, shp[1], shp[2], shp[3], 8), dtype=torch.bfloat16, device="cuda")
     sel = list(range(min(P, 8))) + list(range(max(8, P - 8), P))    # check head and tail poses
     L = N.lib()
     stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -87,6 +92,8 @@ def test_umma_layer_matches_torch_reference(setup, layer, P):
     assert torch.equal(runs[0], runs[1]), "run-to-run nondeterminism"
     assert not torch.isnan(runs[0].float()).any()
     want = ref(sel)
+    if layer < 4:
+        out = out.permute(0, 2, 3, 4, 1, 5).reshape(shp)
     got = out[sel].to(torch.float64).cpu()
     err = (got - want).abs()
     tol = (2.0 ** -8) * want.abs() + 2e-3 if layer < 4 else 1e-4 * want.abs() + 1e-4
