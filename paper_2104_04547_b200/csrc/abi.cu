@@ -7,6 +7,7 @@
 // voxelize / build_graph (complexes.py:171-254).
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -64,6 +65,16 @@ struct GnnArgs {
   int k_steps[2]; int gn; float* state; float* lat; int64_t ld_lat; const int32_t* err; int smem_state;
 };
 int gnn_padded_width(int d);
+struct GnnMmaArgs {
+  const float* feats; int F; const int64_t* node_off;
+  const int64_t* row_cov; const int32_t* col_cov; const int64_t* row_ncov; const int32_t* col_ncov;
+  const float* we; const float* be; const uint32_t* wfrag[2]; const float* wbias[2];
+  const uint32_t* gfrag; const float* gbias; int k_steps[2]; float* lat; int64_t ld_lat; const int32_t* err;
+};
+int gnn_mma_phase_words();
+int gnn_mma_gather_words();
+bool gnn_mma_fits(int max_nodes);
+int launch_gnn_mma(const GnnMmaArgs& a, int split, int n_poses, int max_nodes, cudaStream_t st);
 int launch_gnn(const GnnArgs& a, int dpad, int n_poses, int max_nodes, cudaStream_t st);
 bool gnn_needs_global_state(int dpad, int max_nodes);
 
@@ -94,6 +105,8 @@ struct fs_model {
   size_t msg, msgb, msv, msvb, fw[8], fb[8];
   size_t umma_off = 0;   // byte offset of the bf16 UMMA conv weights
   bool umma_ok = false;
+  bool gmma_ok = false;  // tensor-core SG-CNN (widths 24 / 128)
+  size_t gm_wf[2], gm_wb[2], gm_gf, gm_gb;
   const float* P(size_t off) const { return blob + off; }
 };
 
@@ -154,6 +167,12 @@ static size_t plan_model(fs_model& m) {
       m.fw[i] = L.take((size_t)width * out); m.fb[i] = L.take(out);
       width = out;
     }
+  }
+  m.gmma_ok = m.dg == 24 && m.gn == 128;
+  if (m.gmma_ok) {
+    for (int ph = 0; ph < 2; ++ph) { m.gm_wf[ph] = L.take(gnn_mma_phase_words()); m.gm_wb[ph] = L.take(72); }
+    m.gm_gf = L.take(gnn_mma_gather_words());
+    m.gm_gb = L.take(256);
   }
   size_t bytes = L.n * 4;
   m.umma_ok = umma::supports(d);
@@ -281,6 +300,86 @@ static int pack_model(fs_model& m, const ParamMap& pm, std::vector<float>& h) {
         h[m.gf + (size_t)c * m.gn + k] = (float)gfw[(size_t)c * m.gn + k];
       }
     for (int k = 0; k < m.gn; ++k) { h[m.bg + k] = (float)ggb[k]; h[m.bf + k] = (float)gfb[k]; }
+  }
+  if (m.gmma_ok) {
+    // m16n8k16 B fragments (bf16 hi/lo): word0 = (W[16kt+2t][8nt+g], W[16kt+2t+1][8nt+g]),
+    // word1 = (W[16kt+2t+8][8nt+g], W[16kt+2t+9][8nt+g]); lane = 4g + t.
+    auto bf16_bits = [](double x) -> uint32_t {
+      float f = (float)x;
+      uint32_t u;
+      std::memcpy(&u, &f, 4);
+      if ((u & 0x7f800000u) != 0x7f800000u) u += 0x7fffu + ((u >> 16) & 1u);
+      return u >> 16;
+    };
+    auto bf16_val = [&](double x) -> double {
+      uint32_t b = bf16_bits(x) << 16;
+      float f;
+      std::memcpy(&f, &b, 4);
+      return (double)f;
+    };
+    auto frags = [&](const std::vector<double>& W, int K, int N, uint32_t* out_hi, uint32_t* out_lo) {
+      const int KT = K / 16, NT = N / 8;
+      for (int kt = 0; kt < KT; ++kt)
+        for (int nt = 0; nt < NT; ++nt)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int g = lane >> 2, t = lane & 3;
+            const int n = 8 * nt + g;
+            const int ks[4] = {16 * kt + 2 * t, 16 * kt + 2 * t + 1, 16 * kt + 2 * t + 8, 16 * kt + 2 * t + 9};
+            uint32_t hi[4], lo[4];
+            for (int e = 0; e < 4; ++e) {
+              const double w = W[(size_t)ks[e] * N + n];
+              hi[e] = bf16_bits(w);
+              lo[e] = bf16_bits(w - bf16_val(w));
+            }
+            const size_t o = ((size_t)(kt * NT + nt) * 32 + lane) * 2;
+            out_hi[o] = hi[0] | (hi[1] << 16);
+            out_hi[o + 1] = hi[2] | (hi[3] << 16);
+            out_lo[o] = lo[0] | (lo[1] << 16);
+            out_lo[o + 1] = lo[2] | (lo[3] << 16);
+          }
+    };
+    const char* phases[2] = {"cov", "noncov"};
+    const int dg = 24;
+    for (int ph = 0; ph < 2; ++ph) {
+      char nm[64];
+      auto g = [&](const char* s) { snprintf(nm, sizeof nm, "graph/%s_%s", phases[ph], s); return need(nm); };
+      const double* msg = g("msg_w");
+      const double* W[3] = {g("wz"), g("wr"), g("wh")};
+      const double* U[3] = {g("uz"), g("ur"), g("uh")};
+      const double* B[3] = {g("bz"), g("br"), g("bh")};
+      auto fold = [&](int q, int c, int k) {
+        double acc = 0.0;
+        for (int t2 = 0; t2 < dg; ++t2) acc += msg[(size_t)c * dg + t2] * W[q][(size_t)t2 * dg + k];
+        return acc;
+      };
+      std::vector<double> Wzr((size_t)48 * 48), Whh((size_t)48 * 24);
+      for (int c = 0; c < 24; ++c)
+        for (int k = 0; k < 24; ++k) {
+          Wzr[(size_t)c * 48 + k] = fold(0, c, k);
+          Wzr[(size_t)c * 48 + 24 + k] = fold(1, c, k);
+          Wzr[(size_t)(24 + c) * 48 + k] = U[0][(size_t)c * dg + k];
+          Wzr[(size_t)(24 + c) * 48 + 24 + k] = U[1][(size_t)c * dg + k];
+          Whh[(size_t)c * 24 + k] = fold(2, c, k);
+          Whh[(size_t)(24 + c) * 24 + k] = U[2][(size_t)c * dg + k];
+        }
+      uint32_t* wf = reinterpret_cast<uint32_t*>(&h[m.gm_wf[ph]]);
+      const int zr = 3 * 6 * 64, hh = 3 * 3 * 64;
+      frags(Wzr, 48, 48, wf, wf + zr);
+      frags(Whh, 48, 24, wf + 2 * zr, wf + 2 * zr + hh);
+      for (int q = 0; q < 3; ++q)
+        for (int k = 0; k < 24; ++k) h[m.gm_wb[ph] + q * 24 + k] = (float)B[q][k];
+    }
+    const double* ggw = need("graph/gather_gate_w"); const double* ggb = need("graph/gather_gate_b");
+    const double* gfw = need("graph/gather_feat_w"); const double* gfb = need("graph/gather_feat_b");
+    std::vector<double> Gm((size_t)32 * 256, 0.0);
+    for (int c = 0; c < 24; ++c)
+      for (int k = 0; k < 128; ++k) {
+        Gm[(size_t)c * 256 + k] = ggw[(size_t)c * 128 + k];
+        Gm[(size_t)c * 256 + 128 + k] = gfw[(size_t)c * 128 + k];
+      }
+    uint32_t* gf = reinterpret_cast<uint32_t*>(&h[m.gm_gf]);
+    frags(Gm, 32, 256, gf, gf + gnn_mma_gather_words() / 2);
+    for (int k = 0; k < 128; ++k) { h[m.gm_gb + k] = (float)ggb[k]; h[m.gm_gb + 128 + k] = (float)gfb[k]; }
   }
   if ((rc = copy("graph/dense1_w", m.gd1w, (size_t)m.gn * m.w1))) return rc;
   if ((rc = copy("graph/dense1_b", m.gd1b, m.w1))) return rc;
@@ -418,7 +517,7 @@ static int voxel_tail(const fs_model& m, int P, char* ws, const WsPlan& w, bool 
 }
 
 static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const WsPlan& w,
-                      const int32_t* err, bool want_pred, cudaStream_t st) {
+                      const int32_t* err, bool want_pred, int precision, cudaStream_t st) {
   GnnArgs g{};
   g.feats = (float*)(ws + w.feats); g.F = m.F; g.node_off = (int64_t*)(ws + w.node_off);
   g.row_cov = (int64_t*)(ws + w.row_cov); g.col_cov = (int32_t*)(ws + w.col_cov);
@@ -428,7 +527,24 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
   g.k_steps[0] = m.d.k_cov; g.k_steps[1] = m.d.k_noncov; g.gn = m.gn;
   g.state = (float*)(ws + w.state); g.lat = (float*)(ws + w.lat); g.ld_lat = m.LW; g.err = err;
   mark_stage(ST_GNN, st);
-  int rc = launch_gnn(g, m.dpad, P, max_nodes, st);
+  int rc;
+  static const bool force_ffma = getenv("FS_GNN_FFMA") != nullptr;
+  if (precision == FS_PREC_BF16 && m.gmma_ok && !force_ffma && gnn_mma_fits(max_nodes)) {
+    GnnMmaArgs q{};
+    q.feats = g.feats; q.F = g.F; q.node_off = g.node_off;
+    q.row_cov = g.row_cov; q.col_cov = g.col_cov; q.row_ncov = g.row_ncov; q.col_ncov = g.col_ncov;
+    q.we = g.we; q.be = g.be;
+    for (int ph = 0; ph < 2; ++ph) {
+      q.wfrag[ph] = reinterpret_cast<const uint32_t*>(m.P(m.gm_wf[ph]));
+      q.wbias[ph] = m.P(m.gm_wb[ph]);
+    }
+    q.gfrag = reinterpret_cast<const uint32_t*>(m.P(m.gm_gf)); q.gbias = m.P(m.gm_gb);
+    q.k_steps[0] = m.d.k_cov; q.k_steps[1] = m.d.k_noncov;
+    q.lat = g.lat; q.ld_lat = g.ld_lat; q.err = err;
+    rc = launch_gnn_mma(q, 3, P, max_nodes, st);
+  } else {
+    rc = launch_gnn(g, m.dpad, P, max_nodes, st);
+  }
   mark_stage(ST_FUSION, st);
   if (rc || !want_pred) return rc;
   float* lat = (float*)(ws + w.lat);
@@ -668,7 +784,7 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
     if ((rc = voxel_head_fp32(*m, P, W, w, st))) return rc;
   }
   if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st))) return rc;
-  if ((rc = graph_head(*m, P, max_atoms, W, w, err, late || pred_g, st))) return rc;
+  if ((rc = graph_head(*m, P, max_atoms, W, w, err, late || pred_g, precision, st))) return rc;
   if (!late && (rc = fusion_head(*m, P, W, w, scores, st))) return rc;
   if ((rc = launch_finalize(P, d.fusion_mode, (float*)(W + w.pv), (float*)(W + w.pg), scores, err, st))) return rc;
   rc = copy_outputs(*m, P, W, w, lat_v, lat_g, pred_v, pred_g, st);
@@ -730,7 +846,7 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const d
     // max nodes per pose bounds the GNN's shared-memory state; the host
     // passes it implicitly via n_nodes (worst case: one pose holds them all)
     int max_nodes = (int)(n_nodes < FS_MAX_POSE_ATOMS ? n_nodes : FS_MAX_POSE_ATOMS);
-    if ((rc = graph_head(*m, P, max_nodes, W, w, err, late || pred_g, st))) return rc;
+    if ((rc = graph_head(*m, P, max_nodes, W, w, err, late || pred_g, precision, st))) return rc;
   }
   if (want_f) {
     if (!late && (rc = fusion_head(*m, P, W, w, scores, st))) return rc;

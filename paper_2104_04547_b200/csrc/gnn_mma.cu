@@ -1,0 +1,353 @@
+// SG-CNN head on the tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate)
+// for the reference widths (gather_width_cov 24, gather_width_noncov 128).
+//
+// Same math as gnn.cu (models.py:334-371): per step
+//   [z|r] = sigma([s|h] . [[Wmsg.Wz  Wmsg.Wr]; [Uz Ur]] + [bz|br])
+//   hh    = tanh ([s|r*h] . [[Wmsg.Wh]; [Uh]] + bh);   h <- h + z*(hh-h)
+// with s = sum of neighbour h rows (CSR order).  A warp owns 16-node tiles.
+// The m16n8k16 fragment layouts line up so that each lane holds, for rows
+// g and g+8 (g = lane/4), exactly the columns {2t,2t+1,8+2t,9+2t,16+2t,17+2t}
+// (t = lane%4) of s, h, z, r, hh and h': the whole GRU update is lane-local
+// and r*h feeds the second GEMM without any data exchange.
+// SPLIT = 3 keeps fp32-class accuracy: x = hi + lo (bf16 each) and
+// A.B ~ Ahi.Bhi + Ahi.Blo + Alo.Bhi (relative error ~2^-16); SPLIT = 1 is a
+// single bf16 pass.  Node states stay fp32 in shared memory.
+// Determinism: fixed tile->warp assignment, CSR-order sums, fixed reduction
+// trees -> a pose's latent is bitwise independent of its batch.
+#include "common.cuh"
+
+namespace fs {
+
+struct GnnMmaArgs {
+  const float* feats; int F;
+  const int64_t* node_off;
+  const int64_t* row_cov; const int32_t* col_cov;
+  const int64_t* row_ncov; const int32_t* col_ncov;
+  const float* we; const float* be;       // [F][24], [24]
+  const uint32_t* wfrag[2];               // per phase, see gnn_mma_phase_words()
+  const float* wbias[2];                  // per phase [72] = bz | br | bh
+  const uint32_t* gfrag;                  // gather fragments [2 hi/lo][2 kt][32 nt][32][2]
+  const float* gbias;                     // [256] = bg | bf
+  int k_steps[2];
+  float* lat; int64_t ld_lat;             // [P][ld_lat], columns 0..127
+  const int32_t* err;
+};
+
+constexpr int kMmaWarps = 16;
+constexpr int kZrWords = 3 * 6 * 64;      // [kt][nt][lane][2] per hi/lo
+constexpr int kHhWords = 3 * 3 * 64;
+constexpr int kPhaseWords = 2 * (kZrWords + kHhWords);   // hi and lo
+constexpr int kGatherWords = 2 * 2 * 32 * 64;
+
+int gnn_mma_phase_words() { return kPhaseWords; }
+int gnn_mma_gather_words() { return kGatherWords; }
+
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo_idx, float hi_idx) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo_idx, hi_idx);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// split a pair into (hi, lo) bf16x2 words
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+  float2 hf = __bfloat1622float2(h);
+  __nv_bfloat162 l = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<uint32_t*>(&h);
+  lo = *reinterpret_cast<uint32_t*>(&l);
+}
+
+// A fragments of a 16x48 tile [left(24) | right(24)] from the lane's values:
+// L[r][c] / R[r][c]: r in {row g, row g+8}, c in {2t,2t+1,8+2t,9+2t,16+2t,17+2t}
+template <int SPLIT>
+__device__ __forceinline__ void put_a(uint32_t (&hi)[4], uint32_t (&lo)[4], int q, float x0, float x1) {
+  if (SPLIT == 3) split2(x0, x1, hi[q], lo[q]);
+  else hi[q] = pack_bf16(x0, x1);
+}
+
+// A fragments of a 16x48 tile [left(24) | right(24)] from the lane's values
+// L[r][c], R[r][c] (r: rows g, g+8; c indexes cols 2t,2t+1,8+2t,9+2t,16+2t,17+2t):
+// k-tile 0 = L[0..15]; k-tile 1 = L[16..23] | R[0..7]; k-tile 2 = R[8..23].
+template <int SPLIT>
+__device__ __forceinline__ void build_a48(const float (&L)[2][6], const float (&R)[2][6], uint32_t (&hi)[3][4],
+                                          uint32_t (&lo)[3][4]) {
+  put_a<SPLIT>(hi[0], lo[0], 0, L[0][0], L[0][1]);
+  put_a<SPLIT>(hi[0], lo[0], 1, L[1][0], L[1][1]);
+  put_a<SPLIT>(hi[0], lo[0], 2, L[0][2], L[0][3]);
+  put_a<SPLIT>(hi[0], lo[0], 3, L[1][2], L[1][3]);
+  put_a<SPLIT>(hi[1], lo[1], 0, L[0][4], L[0][5]);
+  put_a<SPLIT>(hi[1], lo[1], 1, L[1][4], L[1][5]);
+  put_a<SPLIT>(hi[1], lo[1], 2, R[0][0], R[0][1]);
+  put_a<SPLIT>(hi[1], lo[1], 3, R[1][0], R[1][1]);
+  put_a<SPLIT>(hi[2], lo[2], 0, R[0][2], R[0][3]);
+  put_a<SPLIT>(hi[2], lo[2], 1, R[1][2], R[1][3]);
+  put_a<SPLIT>(hi[2], lo[2], 2, R[0][4], R[0][5]);
+  put_a<SPLIT>(hi[2], lo[2], 3, R[1][4], R[1][5]);
+}
+
+template <int SPLIT, int NT>
+__device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[3][4], const uint32_t (&alo)[3][4],
+                                       const uint32_t* __restrict__ fhi, const uint32_t* __restrict__ flo,
+                                       int lane) {
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) { D[nt][0] = D[nt][1] = D[nt][2] = D[nt][3] = 0.f; }
+#pragma unroll
+  for (int kt = 0; kt < 3; ++kt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const uint2 bh = *reinterpret_cast<const uint2*>(fhi + ((kt * NT + nt) * 32 + lane) * 2);
+      if (SPLIT == 3) {
+        const uint2 bl = *reinterpret_cast<const uint2*>(flo + ((kt * NT + nt) * 32 + lane) * 2);
+        mma_bf16(D[nt], alo[kt], bh.x, bh.y);
+        mma_bf16(D[nt], ahi[kt], bl.x, bl.y);
+      }
+      mma_bf16(D[nt], ahi[kt], bh.x, bh.y);
+    }
+}
+
+template <int SPLIT>
+__global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  const int p = blockIdx.x;
+  const int64_t base = a.node_off[p];
+  const int n = static_cast<int>(a.node_off[p + 1] - base);
+  float* lat = a.lat + static_cast<int64_t>(p) * a.ld_lat;
+  if (a.err && a.err[p]) {
+    for (int k = threadIdx.x; k < 128; k += blockDim.x) lat[k] = __int_as_float(0x7fc00000);
+    return;
+  }
+  const int ntiles = (n + 15) / 16, npad = ntiles * 16;
+  float* H = sm;                                   // [npad][24] node state (fp32)
+  float* S = H + npad * 24;                        // [npad][24] neighbour sums
+  uint32_t* WF = reinterpret_cast<uint32_t*>(S + npad * 24);   // phase fragments
+  float* WB = reinterpret_cast<float*>(WF + kPhaseWords);      // phase biases [72]
+  float* RED = WB + 72;                                        // [warps][128]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+#define COLS(c) ((c) < 2 ? 2 * t + (c) : (c) < 4 ? 6 + 2 * t + (c) : 12 + 2 * t + (c))
+
+  // ---- embedding h0 = tanh(X.We + be); padded rows are zero ----
+  for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+    float acc[24];
+#pragma unroll
+    for (int k = 0; k < 24; ++k) acc[k] = i < n ? a.be[k] : 0.f;
+    if (i < n) {
+      const float* x = a.feats + (base + i) * a.F;
+      for (int f = 0; f < a.F; ++f) {
+        const float xv = x[f];
+#pragma unroll
+        for (int k = 0; k < 24; ++k) acc[k] = fmaf(xv, __ldg(a.we + f * 24 + k), acc[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 24; k += 4)
+      *reinterpret_cast<float4*>(H + i * 24 + k) =
+          i < n ? make_float4(fs_tanh(acc[k]), fs_tanh(acc[k + 1]), fs_tanh(acc[k + 2]), fs_tanh(acc[k + 3]))
+                : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+
+  for (int ph = 0; ph < 2; ++ph) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kPhaseWords; i += blockDim.x) WF[i] = a.wfrag[ph][i];
+    for (int i = threadIdx.x; i < 72; i += blockDim.x) WB[i] = a.wbias[ph][i];
+    __syncthreads();
+    const int64_t* rows = ph == 0 ? a.row_cov : a.row_ncov;
+    const int32_t* colv = ph == 0 ? a.col_cov : a.col_ncov;
+    const uint32_t* zr_hi = WF;
+    const uint32_t* zr_lo = WF + kZrWords;
+    const uint32_t* hh_hi = WF + 2 * kZrWords;
+    const uint32_t* hh_lo = WF + 2 * kZrWords + kHhWords;
+    float bz[6], br[6], bh[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) { bz[c] = WB[COLS(c)]; br[c] = WB[24 + COLS(c)]; bh[c] = WB[48 + COLS(c)]; }
+
+    for (int step = 0; step < a.k_steps[ph]; ++step) {
+      // (A) neighbour sums, CSR order
+      for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int row = tile * 16 + g + 8 * rr;
+          float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0;
+          if (row < n) {
+            const int64_t qb = rows[base + row], qe = rows[base + row + 1];
+            for (int64_t q = qb; q < qe; ++q) {
+              const float* hj = H + colv[q] * 24;
+              const float2 v0 = *reinterpret_cast<const float2*>(hj + 2 * t);
+              const float2 v1 = *reinterpret_cast<const float2*>(hj + 8 + 2 * t);
+              const float2 v2 = *reinterpret_cast<const float2*>(hj + 16 + 2 * t);
+              s0.x += v0.x; s0.y += v0.y; s1.x += v1.x; s1.y += v1.y; s2.x += v2.x; s2.y += v2.y;
+            }
+          }
+          float* sr = S + row * 24;
+          *reinterpret_cast<float2*>(sr + 2 * t) = s0;
+          *reinterpret_cast<float2*>(sr + 8 + 2 * t) = s1;
+          *reinterpret_cast<float2*>(sr + 16 + 2 * t) = s2;
+        }
+      }
+      __syncthreads();
+      // (B) gates and update, lane-local
+      for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
+        float s[2][6], h[2][6];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int row = tile * 16 + g + 8 * rr;
+#pragma unroll
+          for (int c = 0; c < 6; c += 2) {
+            const float2 sv = *reinterpret_cast<const float2*>(S + row * 24 + COLS(c));
+            const float2 hv = *reinterpret_cast<const float2*>(H + row * 24 + COLS(c));
+            s[rr][c] = sv.x; s[rr][c + 1] = sv.y; h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
+          }
+        }
+        uint32_t ahi[3][4], alo[3][4];
+        build_a48<SPLIT>(s, h, ahi, alo);
+        float Dzr[6][4];
+        gemm48<SPLIT, 6>(Dzr, ahi, alo, zr_hi, zr_lo, lane);
+        // D n-tile j holds (row g: cols 8j+2t, 8j+2t+1; row g+8: same)
+        float z[2][6], rh[2][6];
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+              const int c = 2 * j + e;
+              z[rr][c] = fs_sigmoid(Dzr[j][2 * rr + e] + bz[c]);
+              rh[rr][c] = fs_sigmoid(Dzr[3 + j][2 * rr + e] + br[c]) * h[rr][c];
+            }
+        build_a48<SPLIT>(s, rh, ahi, alo);
+        float Dh[3][4];
+        gemm48<SPLIT, 3>(Dh, ahi, alo, hh_hi, hh_lo, lane);
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int row = tile * 16 + g + 8 * rr;
+          float hn[6];
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int c = 2 * j + e;
+              const float hh = fs_tanh(Dh[j][2 * rr + e] + bh[c]);
+              hn[c] = fmaf(z[rr][c], hh - h[rr][c], h[rr][c]);
+            }
+          if (row < n) {
+#pragma unroll
+            for (int c = 0; c < 6; c += 2)
+              *reinterpret_cast<float2*>(H + row * 24 + COLS(c)) = make_float2(hn[c], hn[c + 1]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- gated gather + mean pool: [gate|val] = h.[Gg|Gf] (K 24->32, N 256) ----
+  float acc[16][2];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) { acc[j][0] = 0.f; acc[j][1] = 0.f; }
+  const uint32_t* g_hi = a.gfrag;
+  const uint32_t* g_lo = a.gfrag + kGatherWords / 2;
+  for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
+    float h[2][6];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int row = tile * 16 + g + 8 * rr;
+#pragma unroll
+      for (int c = 0; c < 6; c += 2) {
+        const float2 hv = *reinterpret_cast<const float2*>(H + row * 24 + COLS(c));
+        h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
+      }
+    }
+    // k-tile 0: h[0..15]; k-tile 1: h[16..23] | zero padding
+    uint32_t ahi[2][4], alo[2][4];
+    put_a<SPLIT>(ahi[0], alo[0], 0, h[0][0], h[0][1]);
+    put_a<SPLIT>(ahi[0], alo[0], 1, h[1][0], h[1][1]);
+    put_a<SPLIT>(ahi[0], alo[0], 2, h[0][2], h[0][3]);
+    put_a<SPLIT>(ahi[0], alo[0], 3, h[1][2], h[1][3]);
+    put_a<SPLIT>(ahi[1], alo[1], 0, h[0][4], h[0][5]);
+    put_a<SPLIT>(ahi[1], alo[1], 1, h[1][4], h[1][5]);
+    put_a<SPLIT>(ahi[1], alo[1], 2, 0.f, 0.f);
+    put_a<SPLIT>(ahi[1], alo[1], 3, 0.f, 0.f);
+    const bool v0 = tile * 16 + g < n, v1 = tile * 16 + g + 8 < n;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float Dg[4] = {0.f, 0.f, 0.f, 0.f}, Dv[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kt = 0; kt < 2; ++kt) {
+        const uint2 bgh = __ldg(reinterpret_cast<const uint2*>(g_hi + ((kt * 32 + j) * 32 + lane) * 2));
+        const uint2 bvh = __ldg(reinterpret_cast<const uint2*>(g_hi + ((kt * 32 + 16 + j) * 32 + lane) * 2));
+        if (SPLIT == 3) {
+          const uint2 bgl = __ldg(reinterpret_cast<const uint2*>(g_lo + ((kt * 32 + j) * 32 + lane) * 2));
+          const uint2 bvl = __ldg(reinterpret_cast<const uint2*>(g_lo + ((kt * 32 + 16 + j) * 32 + lane) * 2));
+          mma_bf16(Dg, alo[kt], bgh.x, bgh.y);
+          mma_bf16(Dg, ahi[kt], bgl.x, bgl.y);
+          mma_bf16(Dv, alo[kt], bvh.x, bvh.y);
+          mma_bf16(Dv, ahi[kt], bvl.x, bvl.y);
+        }
+        mma_bf16(Dg, ahi[kt], bgh.x, bgh.y);
+        mma_bf16(Dv, ahi[kt], bvh.x, bvh.y);
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = 8 * j + 2 * t + e;
+        const float bgv = __ldg(a.gbias + col), bfv = __ldg(a.gbias + 128 + col);
+        const float x0 = v0 ? fs_sigmoid(Dg[e] + bgv) * fs_tanh(Dv[e] + bfv) : 0.f;
+        const float x1 = v1 ? fs_sigmoid(Dg[2 + e] + bgv) * fs_tanh(Dv[2 + e] + bfv) : 0.f;
+        acc[j][e] += x0 + x1;
+      }
+    }
+  }
+  // reduce over g (lane bits 2..4), fixed tree
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      float v = acc[j][e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      acc[j][e] = v;
+    }
+  __syncthreads();
+  if (g == 0) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) RED[warp * 128 + 8 * j + 2 * t + e] = acc[j][e];
+  }
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    float tot = 0.f;
+    for (int w = 0; w < kMmaWarps; ++w) tot += RED[w * 128 + threadIdx.x];
+    lat[threadIdx.x] = tot / static_cast<float>(max(n, 1));
+  }
+}
+
+size_t gnn_mma_smem_bytes(int max_nodes) {
+  const int npad = (max_nodes + 15) / 16 * 16;
+  return static_cast<size_t>(2) * npad * 24 * 4 + kPhaseWords * 4 + 72 * 4 + kMmaWarps * 128 * 4 + 64;
+}
+
+bool gnn_mma_fits(int max_nodes) { return gnn_mma_smem_bytes(max_nodes) <= 227 * 1024; }
+
+int launch_gnn_mma(const GnnMmaArgs& a, int split, int n_poses, int max_nodes, cudaStream_t st) {
+  if (n_poses <= 0) return FS_OK;
+  if (!gnn_mma_fits(max_nodes)) return FS_ECAPACITY;
+  const size_t smem = gnn_mma_smem_bytes(max_nodes);
+  if (split == 3) {
+    FS_CUDA_CHECK(cudaFuncSetAttribute(gnn_mma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gnn_mma_kernel<3><<<n_poses, kMmaWarps * 32, smem, st>>>(a);
+  } else {
+    FS_CUDA_CHECK(cudaFuncSetAttribute(gnn_mma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gnn_mma_kernel<1><<<n_poses, kMmaWarps * 32, smem, st>>>(a);
+  }
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
+}  // namespace fs

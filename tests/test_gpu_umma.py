@@ -135,3 +135,22 @@ def test_bf16_batch_invariance_bitwise(setup):
         got = dm.score_poses(E.batch_from_arrays(part.xyz, part.elem, part.role, part.atom_off, pocket=pk,
                                                  pose_target=part.target), "bf16")["scores"].cpu().numpy()
         assert np.array_equal(got, whole[s:e])
+
+
+def test_tensorcore_gnn_matches_ffma_gnn(setup):
+    """mma.sync SG-CNN (bf16 hi/lo split, fp32 accumulate) vs the FFMA fp32
+    kernel on the same graphs: latent_g within 1e-4 absolute (|lat| ~ 0.1)."""
+    torch, N, m, dm = setup
+    from paper_2104_04547_b200 import engine as E
+    from paper_2104_04547_b200 import synth
+    pocket = synth.make_pocket(1000, seed=9)
+    lib = synth.make_poses(40, poses_per_compound=10, seed=10).slice(0, 397)
+    b = E.batch_from_arrays(lib.xyz, lib.elem, lib.role, lib.atom_off,
+                            pocket=(pocket.xyz, pocket.elem, pocket.role, np.array([0, 1000])),
+                            pose_target=lib.target)
+    g32 = dm.score_poses(b, "fp32", outputs=("lat_g",))["lat_g"]
+    g16 = dm.score_poses(b, "bf16", outputs=("lat_g",))["lat_g"]
+    torch.cuda.synchronize()
+    diff = float((g32 - g16).abs().max())
+    print(f"tensor-core GNN vs FFMA GNN: max |dlat_g| = {diff:.3e}")
+    assert diff < 1e-4
