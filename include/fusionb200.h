@@ -191,8 +191,9 @@ size_t fs_workspace_bytes(const fs_model* m, int32_t max_poses,
  * path: models.featurize (:638-651) then predict_batch).  Outputs (nullable
  * except scores) are float32 device arrays: scores[P], lat_v[P,latent_v],
  * lat_g[P,latent_g], pred_v[P], pred_g[P].  err[P] bit mask; poses with
- * err != 0 get NaN score.  max_edges bounds the directed CSR entries of the
- * whole batch per edge type; overflow sets FS_ERR_EDGE_CAP (host retries). */
+ * err != 0 get NaN score.  max_edges bounds the directed CSR entries of ONE
+ * pose per edge type (size the workspace with P*max_edges); a pose above it
+ * gets FS_ERR_EDGE_CAP (host retries with a larger bound). */
 int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b,
                    int64_t max_edges, void* ws, size_t ws_bytes,
                    float* scores, float* lat_v, float* lat_g, float* pred_v,

@@ -38,6 +38,9 @@ int launch_graph_fill(const fs_pose_batch& b, const int64_t* node_off, double tc
 int launch_rows(const int32_t* deg, int64_t n, int64_t* row_ptr, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_edge_counts(const int64_t* node_off, int n_poses, const int64_t* row_ptr, const int32_t* col, int64_t* edge_off, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_edges(const int64_t* node_off, int n_poses, const int64_t* row_ptr, const int32_t* col, const double* dist, const int64_t* edge_off, int64_t* edges, double* dists, cudaStream_t st);
+int launch_graph_csr(const fs_pose_batch& b, const int64_t* node_off, double tc, double tn, int64_t* row_cov,
+                     int32_t* deg_cov, int32_t* col_cov, double* dist_cov, int64_t* row_ncov, int32_t* deg_ncov,
+                     int32_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st);
 int launch_csr_from_edges(const int64_t* edges, int64_t ne, const int64_t* node_off, int n_poses, int64_t n_nodes, int32_t* node_pose, int32_t* deg, int64_t* row_ptr, int64_t* cursor, int32_t* col, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t scan_ws_bytes(int64_t n);
 
@@ -59,7 +62,8 @@ int launch_f64_to_f32(const double* in, float* out, int64_t n, int row, const in
 
 struct GnnArgs {
   const float* feats; int F; const int64_t* node_off;
-  const int64_t* row_cov; const int32_t* col_cov; const int64_t* row_ncov; const int32_t* col_ncov;
+  const int64_t* row_cov; const int32_t* deg_cov; const int32_t* col_cov;
+  const int64_t* row_ncov; const int32_t* deg_ncov; const int32_t* col_ncov;
   const float* we; const float* be; const float* phase[2];
   const float* gg; const float* bg; const float* gf; const float* bf;
   int k_steps[2]; int gn; float* state; float* lat; int64_t ld_lat; const int32_t* err; int smem_state;
@@ -67,7 +71,8 @@ struct GnnArgs {
 int gnn_padded_width(int d);
 struct GnnMmaArgs {
   const float* feats; int F; const int64_t* node_off;
-  const int64_t* row_cov; const int32_t* col_cov; const int64_t* row_ncov; const int32_t* col_ncov;
+  const int64_t* row_cov; const int32_t* deg_cov; const int32_t* col_cov;
+  const int64_t* row_ncov; const int32_t* deg_ncov; const int32_t* col_ncov;
   const float* we; const float* be; const uint32_t* wfrag[2]; const float* wbias[2];
   const uint32_t* gfrag; const float* gbias; int k_steps[2]; float* lat; int64_t ld_lat; const int32_t* err;
 };
@@ -522,6 +527,7 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
   g.feats = (float*)(ws + w.feats); g.F = m.F; g.node_off = (int64_t*)(ws + w.node_off);
   g.row_cov = (int64_t*)(ws + w.row_cov); g.col_cov = (int32_t*)(ws + w.col_cov);
   g.row_ncov = (int64_t*)(ws + w.row_ncov); g.col_ncov = (int32_t*)(ws + w.col_ncov);
+  g.deg_cov = (int32_t*)(ws + w.deg_cov); g.deg_ncov = (int32_t*)(ws + w.deg_ncov);
   g.we = m.P(m.we); g.be = m.P(m.be); g.phase[0] = m.P(m.ph[0]); g.phase[1] = m.P(m.ph[1]);
   g.gg = m.P(m.gg); g.bg = m.P(m.bg); g.gf = m.P(m.gf); g.bf = m.P(m.bf);
   g.k_steps[0] = m.d.k_cov; g.k_steps[1] = m.d.k_noncov; g.gn = m.gn;
@@ -533,6 +539,7 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
     GnnMmaArgs q{};
     q.feats = g.feats; q.F = g.F; q.node_off = g.node_off;
     q.row_cov = g.row_cov; q.col_cov = g.col_cov; q.row_ncov = g.row_ncov; q.col_ncov = g.col_ncov;
+    q.deg_cov = g.deg_cov; q.deg_ncov = g.deg_ncov;
     q.we = g.we; q.be = g.be;
     for (int ph = 0; ph < 2; ++ph) {
       q.wfrag[ph] = reinterpret_cast<const uint32_t*>(m.P(m.gm_wf[ph]));
@@ -747,7 +754,8 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   if (P <= 0) return FS_OK;
   const int max_atoms = b->max_pose_atoms > 0 ? b->max_pose_atoms : FS_MAX_POSE_ATOMS;
   const int64_t N = (int64_t)P * max_atoms;
-  WsPlan w = plan_ws(*m, P, N, max_edges, precision);
+  if (max_edges <= 0) return FS_EINVAL;
+  WsPlan w = plan_ws(*m, P, N, (int64_t)P * max_edges, precision);
   if (w.total > ws_bytes) return FS_ECAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
   char* W = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
@@ -761,17 +769,11 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   const bool late = d.fusion_mode == FS_MODE_LATE;
   // featurize (models.py:638-651)
   if ((rc = launch_node_features(*b, node_off, d.c_elem, d.box_size, W + w.feats, false, st))) return rc;
-  int32_t* dc = (int32_t*)(W + w.deg_cov); int32_t* dnc = (int32_t*)(W + w.deg_ncov);
-  FS_CUDA_CHECK(cudaMemsetAsync(dc, 0, 4 * (size_t)N, st));
-  FS_CUDA_CHECK(cudaMemsetAsync(dnc, 0, 4 * (size_t)N, st));
-  if ((rc = launch_graph_count(*b, node_off, d.cov_thresh, d.noncov_thresh, dc, dnc, err, st))) return rc;
-  // rows over the exact node count: N is an upper bound; unused tail rows are
-  // never read (node_off bounds every pose).
-  int64_t* rcv = (int64_t*)(W + w.row_cov); int64_t* rnc = (int64_t*)(W + w.row_ncov);
-  if ((rc = launch_rows(dc, N, rcv, W + w.scan, scan_ws_bytes(N) + 1024, st))) return rc;
-  if ((rc = launch_rows(dnc, N, rnc, W + w.scan, scan_ws_bytes(N) + 1024, st))) return rc;
-  if ((rc = launch_graph_fill(*b, node_off, d.cov_thresh, d.noncov_thresh, rcv, rnc, (int32_t*)(W + w.col_cov),
-                              (int32_t*)(W + w.col_ncov), nullptr, nullptr, max_edges, max_edges, err, st)))
+  // radius graph: one fused launch, pose-private CSR slices of max_edges
+  // entries per edge type (rows = start offset + degree)
+  if ((rc = launch_graph_csr(*b, node_off, d.cov_thresh, d.noncov_thresh, (int64_t*)(W + w.row_cov),
+                             (int32_t*)(W + w.deg_cov), (int32_t*)(W + w.col_cov), nullptr, (int64_t*)(W + w.row_ncov),
+                             (int32_t*)(W + w.deg_ncov), (int32_t*)(W + w.col_ncov), nullptr, max_edges, err, st)))
     return rc;
   if (precision == FS_PREC_BF16) {
     if ((rc = launch_voxelize(*b, d.grid_extent, m->cgrid, d.box_size, FS_GRID_NDHWC_BF16, W + w.grid, err, st))) return rc;
@@ -832,13 +834,13 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const d
     int64_t* noff = (int64_t*)(W + w.node_off);
     FS_CUDA_CHECK(cudaMemcpyAsync(noff, node_off, 8 * (size_t)(P + 1), cudaMemcpyDeviceToDevice, st));
     int32_t* node_pose = (int32_t*)(W + w.node_pose);
-    int32_t* deg = (int32_t*)(W + w.deg_cov);
     int64_t* cursor = (int64_t*)(W + w.cursor);
     const size_t scan_b = scan_ws_bytes(n_nodes > P ? n_nodes : P) + 1024;
-    if ((rc = launch_csr_from_edges(cov_edges, n_cov, noff, P, n_nodes, node_pose, deg, (int64_t*)(W + w.row_cov),
-                                    cursor, (int32_t*)(W + w.col_cov), W + w.scan, scan_b, st)))
+    if ((rc = launch_csr_from_edges(cov_edges, n_cov, noff, P, n_nodes, node_pose, (int32_t*)(W + w.deg_cov),
+                                    (int64_t*)(W + w.row_cov), cursor, (int32_t*)(W + w.col_cov), W + w.scan, scan_b,
+                                    st)))
       return rc;
-    if ((rc = launch_csr_from_edges(ncov_edges, n_ncov, noff, P, n_nodes, node_pose, deg,
+    if ((rc = launch_csr_from_edges(ncov_edges, n_ncov, noff, P, n_nodes, node_pose, (int32_t*)(W + w.deg_ncov),
                                     (int64_t*)(W + w.row_ncov), cursor, (int32_t*)(W + w.col_ncov), W + w.scan,
                                     scan_b, st)))
       return rc;

@@ -21,8 +21,8 @@ namespace fs {
 struct GnnMmaArgs {
   const float* feats; int F;
   const int64_t* node_off;
-  const int64_t* row_cov; const int32_t* col_cov;
-  const int64_t* row_ncov; const int32_t* col_ncov;
+  const int64_t* row_cov; const int32_t* deg_cov; const int32_t* col_cov;     // row start + degree
+  const int64_t* row_ncov; const int32_t* deg_ncov; const int32_t* col_ncov;
   const float* we; const float* be;       // [F][24], [24]
   const uint32_t* wfrag[2];               // per phase, see gnn_mma_phase_words()
   const float* wbias[2];                  // per phase [72] = bz | br | bh
@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     for (int i = threadIdx.x; i < 72; i += blockDim.x) WB[i] = a.wbias[ph][i];
     __syncthreads();
     const int64_t* rows = ph == 0 ? a.row_cov : a.row_ncov;
+    const int32_t* degs = ph == 0 ? a.deg_cov : a.deg_ncov;
     const int32_t* colv = ph == 0 ? a.col_cov : a.col_ncov;
     const uint32_t* zr_hi = WF;
     const uint32_t* zr_lo = WF + kZrWords;
@@ -175,9 +176,26 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           const int row = tile * 16 + g + 8 * rr;
           float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0;
           if (row < n) {
-            const int64_t qb = rows[base + row], qe = rows[base + row + 1];
-            for (int64_t q = qb; q < qe; ++q) {
-              const float* hj = H + colv[q] * 24;
+            const int64_t qb = rows[base + row];
+            const int deg = degs[base + row];
+            // column ids come from global memory: fetch 4 ahead so the loads
+            // overlap (sums stay in CSR order)
+            int q = 0;
+            for (; q + 4 <= deg; q += 4) {
+              int j[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) j[u] = __ldg(colv + qb + q + u);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float* hj = H + j[u] * 24;
+                const float2 v0 = *reinterpret_cast<const float2*>(hj + 2 * t);
+                const float2 v1 = *reinterpret_cast<const float2*>(hj + 8 + 2 * t);
+                const float2 v2 = *reinterpret_cast<const float2*>(hj + 16 + 2 * t);
+                s0.x += v0.x; s0.y += v0.y; s1.x += v1.x; s1.y += v1.y; s2.x += v2.x; s2.y += v2.y;
+              }
+            }
+            for (; q < deg; ++q) {
+              const float* hj = H + __ldg(colv + qb + q) * 24;
               const float2 v0 = *reinterpret_cast<const float2*>(hj + 2 * t);
               const float2 v1 = *reinterpret_cast<const float2*>(hj + 8 + 2 * t);
               const float2 v2 = *reinterpret_cast<const float2*>(hj + 16 + 2 * t);
@@ -250,8 +268,17 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   float acc[16][2];
 #pragma unroll
   for (int j = 0; j < 16; ++j) { acc[j][0] = 0.f; acc[j][1] = 0.f; }
-  const uint32_t* g_hi = a.gfrag;
-  const uint32_t* g_lo = a.gfrag + kGatherWords / 2;
+  // gather fragments: stage into the (now free) neighbour-sum buffer when it
+  // is large enough, else read them through L1
+  const uint32_t* gsrc = a.gfrag;
+  if (npad * 24 >= kGatherWords) {
+    uint32_t* gs = reinterpret_cast<uint32_t*>(S);
+    for (int i = threadIdx.x; i < kGatherWords; i += blockDim.x) gs[i] = a.gfrag[i];
+    gsrc = gs;
+  }
+  __syncthreads();
+  const uint32_t* g_hi = gsrc;
+  const uint32_t* g_lo = gsrc + kGatherWords / 2;
   for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
     float h[2][6];
 #pragma unroll
@@ -279,11 +306,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       float Dg[4] = {0.f, 0.f, 0.f, 0.f}, Dv[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int kt = 0; kt < 2; ++kt) {
-        const uint2 bgh = __ldg(reinterpret_cast<const uint2*>(g_hi + ((kt * 32 + j) * 32 + lane) * 2));
-        const uint2 bvh = __ldg(reinterpret_cast<const uint2*>(g_hi + ((kt * 32 + 16 + j) * 32 + lane) * 2));
+        const uint2 bgh = *reinterpret_cast<const uint2*>(g_hi + ((kt * 32 + j) * 32 + lane) * 2);
+        const uint2 bvh = *reinterpret_cast<const uint2*>(g_hi + ((kt * 32 + 16 + j) * 32 + lane) * 2);
         if (SPLIT == 3) {
-          const uint2 bgl = __ldg(reinterpret_cast<const uint2*>(g_lo + ((kt * 32 + j) * 32 + lane) * 2));
-          const uint2 bvl = __ldg(reinterpret_cast<const uint2*>(g_lo + ((kt * 32 + 16 + j) * 32 + lane) * 2));
+          const uint2 bgl = *reinterpret_cast<const uint2*>(g_lo + ((kt * 32 + j) * 32 + lane) * 2);
+          const uint2 bvl = *reinterpret_cast<const uint2*>(g_lo + ((kt * 32 + 16 + j) * 32 + lane) * 2);
           mma_bf16(Dg, alo[kt], bgh.x, bgh.y);
           mma_bf16(Dg, ahi[kt], bgl.x, bgl.y);
           mma_bf16(Dv, alo[kt], bvh.x, bvh.y);

@@ -1,0 +1,431 @@
+// Fused single-launch radius graph for the scoring path: one CTA per pose
+// builds both CSR adjacencies (covalent / non-covalent) of its pose in a
+// private slice [p*cap, (p+1)*cap) of the column arrays.  Same exact edge
+// predicate as featurize.cu (complexes.py:237-246):
+//   d2 = (dx*dx+dy*dy)+dz*dz (float64, no FMA); candidate iff d2 <= rmax^2;
+//   keep iff sqrt(d2) <= t_cov (same role) / t_ncov (different role).
+// Rows are ascending in the neighbour id (canonical), written as (start, deg).
+//
+// Work split:
+//  * non-covalent pairs are bipartite (role S x role L, S the smaller role):
+//    each warp scans one S atom against the L list 32 candidates at a time
+//    (index-ascending, ballot-compacted) and sets bit s in an L-row bitmask.
+//    Every S-L pair is tested exactly once; L rows are read back from the
+//    masks in ascending S order (the S list is index-sorted).
+//  * covalent pairs: cell list with cells >= t_cov (27-cell stencil), one
+//    thread per row, counted then filled and insertion-sorted.
+//  * all scans are parallel (no serial per-cell loops).
+#include "common.cuh"
+
+namespace fs {
+
+struct GraphCsrArgs {
+  fs_pose_batch b;
+  const int64_t* node_off;
+  double tc, tn;
+  int64_t* row_cov; int32_t* deg_cov; int32_t* col_cov; double* dist_cov;
+  int64_t* row_ncov; int32_t* deg_ncov; int32_t* col_ncov; double* dist_ncov;
+  int64_t cap;          // entries per pose per edge type
+  int32_t* err;
+  int smem_atoms;
+};
+
+constexpr int kCsrThreads = 256;
+constexpr int kCsrWarps = kCsrThreads / 32;
+constexpr int kCellsAxis = 12;
+constexpr int kMaskWords = 4;         // bipartite bitmask path for |S| <= 128
+
+__host__ __device__ inline size_t graph_csr_smem_bytes(int n) {
+  const size_t cells = 2 * kCellsAxis * kCellsAxis * kCellsAxis + 2;
+  return (size_t)n * 16 + (size_t)n * 4 * 4 + (size_t)(n + 1) * 4 * 2 + (size_t)n * kMaskWords * 4 + cells * 4 + 512;
+}
+
+// in-place exclusive scan of a[0..n) (n+1-th entry receives the total)
+__device__ void block_exclusive_scan(int* a, int n, int* warp_tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  int sum = 0;
+  for (int i = lo; i < hi; ++i) sum += a[i];
+  int incl = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { int v = warp_tot[w]; warp_tot[w] = run; run += v; }
+    warp_tot[31] = run;
+  }
+  __syncthreads();
+  int run = warp_tot[warp] + incl - sum;
+  for (int i = lo; i < hi; ++i) { int v = a[i]; a[i] = run; run += v; }
+  __syncthreads();
+  if (threadIdx.x == 0) a[n] = warp_tot[31];
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool exact_edge(const PoseView& pv, double xi, double yi, double zi, int j,
+                                           double rmax2, double t, double* dout) {
+  double xj, yj, zj; int32_t ej, rj;
+  pv.atom(j, xj, yj, zj, ej, rj);
+  const double d2 = dist2_exact(xi - xj, yi - yj, zi - zj);
+  if (!(d2 <= rmax2)) return false;
+  const double d = __dsqrt_rn(d2);
+  if (!(d <= t)) return false;
+  *dout = d;
+  return true;
+}
+
+template <bool DIST>
+__global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[33];
+  __shared__ double s_min[3];
+  __shared__ int s_flags, s_role_cnt[2], s_tot[2];
+  __shared__ int warp_tot[32];
+  __shared__ int warp_cnt[2][kCsrWarps];
+
+  const int p = blockIdx.x;
+  const PoseView pv = pose_view(a.b, p);
+  const int n = (int)pv.n();
+  const int64_t base = a.node_off[p];
+  const int64_t cbase = (int64_t)p * a.cap;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  auto fail = [&](int flags) {
+    if (threadIdx.x == 0) atomicOr(&a.err[p], flags);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      a.deg_cov[base + i] = 0; a.deg_ncov[base + i] = 0;
+      a.row_cov[base + i] = cbase; a.row_ncov[base + i] = cbase;
+    }
+  };
+  if (threadIdx.x == 0) { s_flags = 0; s_role_cnt[0] = 0; s_role_cnt[1] = 0; }
+  if (n > a.smem_atoms) { fail(FS_ERR_TOO_LARGE); return; }
+  const int SA = a.smem_atoms;
+  float4* pf = reinterpret_cast<float4*>(smem_raw);
+  int* keys = reinterpret_cast<int*>(pf + SA);
+  int* cell_list = keys + SA;
+  int* role_list = cell_list + SA;      // role 0 ids ascending, then role 1 ids ascending
+  int* rank = role_list + SA;           // position of atom i inside its role's list
+  int* offc = rank + SA;                // [n+1]
+  int* offn = offc + SA + 1;            // [n+1]
+  uint32_t* mask = reinterpret_cast<uint32_t*>(offn + SA + 1);   // [|L|][kMaskWords]
+  int* cell_start = reinterpret_cast<int*>(mask + (size_t)SA * kMaskWords);
+  __syncthreads();
+
+  // ---- atoms, validation, bounding box ----
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  int flags = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double x, y, z; int32_t e, r;
+    pv.atom(i, x, y, z, e, r);
+    if (r != 0 && r != 1) flags |= FS_ERR_ROLE;
+    if (!isfinite(x) || !isfinite(y) || !isfinite(z)) flags |= FS_ERR_NONFINITE;
+    pf[i] = make_float4((float)x, (float)y, (float)z, (float)r);
+    lo[0] = fmin(lo[0], x); lo[1] = fmin(lo[1], y); lo[2] = fmin(lo[2], z);
+    hi[0] = fmax(hi[0], x); hi[1] = fmax(hi[1], y); hi[2] = fmax(hi[2], z);
+  }
+  if (flags) atomicOr(&s_flags, flags);
+  double ext_max = 0.0, absmax = 0.0;
+  for (int ax = 0; ax < 3; ++ax) {
+    double l = lo[ax], h = hi[ax];
+    for (int o = 16; o > 0; o >>= 1) {
+      l = fmin(l, __shfl_xor_sync(0xffffffffu, l, o));
+      h = fmax(h, __shfl_xor_sync(0xffffffffu, h, o));
+    }
+    __syncthreads();
+    if (lane == 0) { red[warp] = l; red[16 + warp] = h; }
+    __syncthreads();
+    l = red[0]; h = red[16];
+    for (int w = 1; w < kCsrWarps; ++w) { l = fmin(l, red[w]); h = fmax(h, red[16 + w]); }
+    if (threadIdx.x == 0) s_min[ax] = l;
+    ext_max = fmax(ext_max, h - l);
+    absmax = fmax(absmax, fmax(fabs(l), fabs(h)));
+  }
+  __syncthreads();
+  if (s_flags) { fail(s_flags); return; }
+  if (n == 0) return;
+  const bool prefilter = absmax < 1024.0;            // fp32 coordinate error <= 6.1e-5 A
+  const double cs = fmax(a.tc * 1.0001, ext_max / (kCellsAxis - 1));
+  const int nca = min(kCellsAxis, (int)floor(ext_max / cs) + 1);
+  const int NC = nca * nca * nca;
+  for (int i = threadIdx.x; i < 2 * NC + 1; i += blockDim.x) cell_start[i] = 0;
+  __syncthreads();
+  auto cell_coord = [&](double x, int ax) -> int {
+    int c = (int)floor(__ddiv_rn(__dsub_rn(x, s_min[ax]), cs));
+    return min(max(c, 0), nca - 1);
+  };
+
+  // ---- counting sort by (role, cell); role lists ascending by id ----
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double x, y, z; int32_t e, r;
+    pv.atom(i, x, y, z, e, r);
+    const int key = r * NC + (cell_coord(x, 0) * nca + cell_coord(y, 1)) * nca + cell_coord(z, 2);
+    keys[i] = key;
+    atomicAdd(&cell_start[key], 1);
+  }
+  {
+    int run[2] = {0, 0};
+    for (int t0 = 0; t0 < n; t0 += blockDim.x) {
+      const int i = t0 + threadIdx.x;
+      const int r = (i < n) ? (int)pf[i].w : -1;
+      const unsigned m0 = __ballot_sync(0xffffffffu, r == 0), m1 = __ballot_sync(0xffffffffu, r == 1);
+      if (lane == 0) { warp_cnt[0][warp] = __popc(m0); warp_cnt[1][warp] = __popc(m1); }
+      __syncthreads();
+      if (r >= 0) {
+        int pos = run[r] + __popc((r == 0 ? m0 : m1) & ((1u << lane) - 1u));
+        for (int w = 0; w < warp; ++w) pos += warp_cnt[r][w];
+        keys[i] |= pos << 16;            // stash rank (n <= 4096 < 2^15, key < 2^16)
+      }
+      for (int w = 0; w < kCsrWarps; ++w) { run[0] += warp_cnt[0][w]; run[1] += warp_cnt[1][w]; }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) { s_role_cnt[0] = run[0]; s_role_cnt[1] = run[1]; }
+  }
+  __syncthreads();
+  const int n0 = s_role_cnt[0];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = (int)pf[i].w, rk = keys[i] >> 16;
+    rank[i] = rk;
+    role_list[(r == 0 ? 0 : n0) + rk] = i;
+    keys[i] &= 0xffff;
+  }
+  block_exclusive_scan(cell_start, 2 * NC, warp_tot);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int slot = atomicAdd(&cell_start[keys[i]], 1);   // becomes the cell end
+    cell_list[slot] = i;
+  }
+  __syncthreads();
+  // cell k spans [cell_start[k-1], cell_start[k]) now (cell_start[-1] := 0)
+
+  const float tcf = (float)a.tc + 1e-3f, tnf = (float)a.tn + 1e-3f;
+  const float tcf2 = tcf * tcf, tnf2 = tnf * tnf;
+  const double rmax = fmax(a.tc, a.tn);
+  const double rmax2 = __dmul_rn(rmax, rmax);
+
+  // ---- non-covalent: bipartite S x L ----
+  const int n1 = n - n0;
+  const int sr = n0 <= n1 ? 0 : 1;                 // smaller role
+  const int nS = sr == 0 ? n0 : n1, nL = n - nS;
+  const int* Slist = role_list + (sr == 0 ? 0 : n0);
+  const int* Llist = role_list + (sr == 0 ? n0 : 0);
+  const bool use_mask = nS <= 32 * kMaskWords;
+  const int W = (nS + 31) / 32;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) { offc[i] = 0; offn[i] = 0; }
+  if (use_mask) {
+    for (int i = threadIdx.x; i < nL * W; i += blockDim.x) mask[i] = 0u;
+    __syncthreads();
+    for (int si = warp; si < nS; si += kCsrWarps) {
+      const int i = Slist[si];
+      double xi, yi, zi; int32_t ei, ri;
+      pv.atom(i, xi, yi, zi, ei, ri);
+      const float4 fi = pf[i];
+      int cnt = 0;
+      for (int l0 = 0; l0 < nL; l0 += 32) {
+        const int lj = l0 + lane;
+        bool hit = false;
+        if (lj < nL) {
+          const int j = Llist[lj];
+          const float4 fj = pf[j];
+          const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+          double d;
+          if (!prefilter || dx * dx + dy * dy + dz * dz <= tnf2) hit = exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        cnt += __popc(m);
+        if (hit) atomicOr(&mask[lj * W + (si >> 5)], 1u << (si & 31));
+      }
+      if (lane == 0) offn[i] = cnt;
+    }
+    __syncthreads();
+    for (int lj = threadIdx.x; lj < nL; lj += blockDim.x) {
+      int c = 0;
+      for (int w = 0; w < W; ++w) c += __popc(mask[lj * W + w]);
+      offn[Llist[lj]] = c;
+    }
+  } else {
+    // large bipartite sides: one thread per row scans the other role's list
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double xi, yi, zi; int32_t ei, ri;
+      pv.atom(i, xi, yi, zi, ei, ri);
+      const float4 fi = pf[i];
+      const int ob = ri == 0 ? n0 : 0, oe = ri == 0 ? n : n0;
+      int c = 0;
+      for (int q = ob; q < oe; ++q) {
+        const int j = role_list[q];
+        const float4 fj = pf[j];
+        const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+        double d;
+        if (prefilter && dx * dx + dy * dy + dz * dz > tnf2) continue;
+        c += exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d);
+      }
+      offn[i] = c;
+    }
+  }
+
+  // ---- covalent degrees: 27-cell stencil, one thread per row ----
+  auto cov_scan = [&](int i, auto&& emit) {
+    double xi, yi, zi; int32_t ei, ri;
+    pv.atom(i, xi, yi, zi, ei, ri);
+    const float4 fi = pf[i];
+    const int key = keys[i] - ri * NC;
+    const int cz = key % nca, cy = (key / nca) % nca, cx = key / (nca * nca);
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int ax = cx + dx;
+      if (ax < 0 || ax >= nca) continue;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int ay = cy + dy;
+        if (ay < 0 || ay >= nca) continue;
+        // the three z-neighbour cells are contiguous in cell order
+        const int z0 = max(cz - 1, 0), z1 = min(cz + 1, nca - 1);
+        const int k0 = ri * NC + (ax * nca + ay) * nca + z0, k1 = ri * NC + (ax * nca + ay) * nca + z1;
+        const int qb = k0 == 0 ? 0 : cell_start[k0 - 1], qe = cell_start[k1];
+        for (int q = qb; q < qe; ++q) {
+          const int j = cell_list[q];
+          if (j == i) continue;
+          const float4 fj = pf[j];
+          const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
+          if (prefilter && ddx * ddx + ddy * ddy + ddz * ddz > tcf2) continue;
+          double d;
+          if (exact_edge(pv, xi, yi, zi, j, rmax2, a.tc, &d)) emit(j, d);
+        }
+      }
+    }
+  };
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int c = 0;
+    cov_scan(i, [&](int, double) { ++c; });
+    offc[i] = c;
+  }
+  __syncthreads();
+  // ---- degrees -> pose-local offsets, capacity check, row pointers ----
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    a.deg_cov[base + i] = offc[i];
+    a.deg_ncov[base + i] = offn[i];
+  }
+  block_exclusive_scan(offc, n, warp_tot);
+  block_exclusive_scan(offn, n, warp_tot);
+  if (offc[n] > a.cap || offn[n] > a.cap) {
+    fail(FS_ERR_EDGE_CAP);
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    a.row_cov[base + i] = cbase + offc[i];
+    a.row_ncov[base + i] = cbase + offn[i];
+  }
+
+  // ---- fill non-covalent rows (ascending neighbour id) ----
+  int32_t* coln = a.col_ncov + cbase;
+  double* distn = DIST ? a.dist_ncov + cbase : nullptr;
+  if (use_mask) {
+    for (int si = warp; si < nS; si += kCsrWarps) {          // S rows: L ids ascending
+      const int i = Slist[si];
+      double xi, yi, zi; int32_t ei, ri;
+      pv.atom(i, xi, yi, zi, ei, ri);
+      int w = offn[i];
+      for (int l0 = 0; l0 < nL; l0 += 32) {
+        const int lj = l0 + lane;
+        const bool hit = lj < nL && ((mask[lj * W + (si >> 5)] >> (si & 31)) & 1u);
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int o = w + __popc(m & ((1u << lane) - 1u));
+          const int j = Llist[lj];
+          coln[o] = j;
+          if (DIST) { double d; exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
+        }
+        w += __popc(m);
+      }
+    }
+    for (int lj = threadIdx.x; lj < nL; lj += blockDim.x) {  // L rows: S ids ascending
+      const int i = Llist[lj];
+      int o = offn[i];
+      double xi = 0, yi = 0, zi = 0; int32_t ei, ri;
+      if (DIST) pv.atom(i, xi, yi, zi, ei, ri);
+      for (int w = 0; w < W; ++w) {
+        uint32_t bits = mask[lj * W + w];
+        while (bits) {
+          const int b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int j = Slist[32 * w + b];
+          coln[o] = j;
+          if (DIST) { double d; exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
+          ++o;
+        }
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double xi, yi, zi; int32_t ei, ri;
+      pv.atom(i, xi, yi, zi, ei, ri);
+      const float4 fi = pf[i];
+      const int ob = ri == 0 ? n0 : 0, oe = ri == 0 ? n : n0;
+      int o = offn[i];
+      for (int q = ob; q < oe; ++q) {
+        const int j = role_list[q];
+        const float4 fj = pf[j];
+        const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+        if (prefilter && dx * dx + dy * dy + dz * dz > tnf2) continue;
+        double d;
+        if (exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d)) {
+          coln[o] = j;
+          if (DIST) distn[o] = d;
+          ++o;
+        }
+      }
+    }
+  }
+  // ---- fill covalent rows, then insertion-sort each (short) row ----
+  int32_t* colc = a.col_cov + cbase;
+  double* distc = DIST ? a.dist_cov + cbase : nullptr;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int rb = offc[i];
+    int o = rb;
+    cov_scan(i, [&](int j, double d) {
+      colc[o] = j;
+      if (DIST) distc[o] = d;
+      ++o;
+    });
+    for (int x = rb + 1; x < o; ++x) {
+      const int v = colc[x];
+      const double dv = DIST ? distc[x] : 0.0;
+      int y = x - 1;
+      while (y >= rb && colc[y] > v) {
+        colc[y + 1] = colc[y];
+        if (DIST) distc[y + 1] = distc[y];
+        --y;
+      }
+      colc[y + 1] = v;
+      if (DIST) distc[y + 1] = dv;
+    }
+  }
+}
+
+int launch_graph_csr(const fs_pose_batch& b, const int64_t* node_off, double tc, double tn, int64_t* row_cov,
+                     int32_t* deg_cov, int32_t* col_cov, double* dist_cov, int64_t* row_ncov, int32_t* deg_ncov,
+                     int32_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st) {
+  if (!(tc >= 1.2 && tc <= 5.9) || !(tn >= 1.2 && tn <= 5.9)) return FS_EINVAL;   // complexes.py:228-231
+  if (b.n_poses <= 0) return FS_OK;
+  GraphCsrArgs a;
+  a.b = b; a.node_off = node_off; a.tc = tc; a.tn = tn;
+  a.row_cov = row_cov; a.deg_cov = deg_cov; a.col_cov = col_cov; a.dist_cov = dist_cov;
+  a.row_ncov = row_ncov; a.deg_ncov = deg_ncov; a.col_ncov = col_ncov; a.dist_ncov = dist_ncov;
+  a.cap = cap; a.err = err;
+  int atoms = b.max_pose_atoms > 0 ? b.max_pose_atoms : FS_MAX_POSE_ATOMS;
+  if (atoms > FS_MAX_POSE_ATOMS) atoms = FS_MAX_POSE_ATOMS;
+  a.smem_atoms = atoms;
+  const size_t smem = graph_csr_smem_bytes(atoms);
+  if (dist_cov || dist_ncov) {
+    FS_CUDA_CHECK(cudaFuncSetAttribute(graph_csr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    graph_csr_kernel<true><<<b.n_poses, kCsrThreads, smem, st>>>(a);
+  } else {
+    FS_CUDA_CHECK(cudaFuncSetAttribute(graph_csr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    graph_csr_kernel<false><<<b.n_poses, kCsrThreads, smem, st>>>(a);
+  }
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
+}  // namespace fs

@@ -347,10 +347,10 @@ class DeviceModel:
             out["pred_v"] = torch.empty(P, dtype=torch.float32, device=dev)
         if "pred_g" in outputs:
             out["pred_g"] = torch.empty(P, dtype=torch.float32, device=dev)
-        cap = max(1, P) * int(max_edges_per_pose)
+        cap = int(max_edges_per_pose)
         s = batch.cstruct()
         while True:
-            nbytes = L.fs_workspace_bytes(self.handle, P, P * batch.max_pose_atoms, cap, prec)
+            nbytes = L.fs_workspace_bytes(self.handle, P, P * batch.max_pose_atoms, max(1, P) * cap, prec)
             ws = self.workspace(nbytes)
             N.check(L.fs_score_poses(self.handle, prec, C.byref(s), cap, _ptr(ws), ws.numel(),
                                      _ptr(out["scores"]), _ptr(out.get("lat_v")), _ptr(out.get("lat_g")),
