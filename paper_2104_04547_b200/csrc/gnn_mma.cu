@@ -123,9 +123,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     return;
   }
   const int ntiles = (n + 15) / 16, npad = ntiles * 16;
-  float* H = sm;                                   // [npad][24] node state (fp32)
-  float* S = H + npad * 24;                        // [npad][24] neighbour sums
-  uint32_t* WF = reinterpret_cast<uint32_t*>(S + npad * 24);   // phase fragments
+  float* Hc = sm;                                  // [npad][24] node state (fp32), current
+  float* Hn = Hc + npad * 24;                      // [npad][24] next (double buffer)
+  uint32_t* WF = reinterpret_cast<uint32_t*>(Hn + npad * 24);  // phase fragments
   float* WB = reinterpret_cast<float*>(WF + kPhaseWords);      // phase biases [72]
   float* RED = WB + 72;                                        // [warps][128]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     }
 #pragma unroll
     for (int k = 0; k < 24; k += 4)
-      *reinterpret_cast<float4*>(H + i * 24 + k) =
+      *reinterpret_cast<float4*>(Hc + i * 24 + k) =
           i < n ? make_float4(fs_tanh(acc[k]), fs_tanh(acc[k + 1]), fs_tanh(acc[k + 2]), fs_tanh(acc[k + 3]))
                 : make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -169,8 +169,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     for (int c = 0; c < 6; ++c) { bz[c] = WB[COLS(c)]; br[c] = WB[24 + COLS(c)]; bh[c] = WB[48 + COLS(c)]; }
 
     for (int step = 0; step < a.k_steps[ph]; ++step) {
-      // (A) neighbour sums, CSR order
+      // one pass per tile: neighbour sums (CSR order) of the old states land
+      // directly in this lane's A-fragment positions, the update is written
+      // to the other buffer -> one barrier per step
       for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
+        float s[2][6], h[2][6];
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           const int row = tile * 16 + g + 8 * rr;
@@ -178,16 +181,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           if (row < n) {
             const int64_t qb = rows[base + row];
             const int deg = degs[base + row];
-            // column ids come from global memory: fetch 4 ahead so the loads
-            // overlap (sums stay in CSR order)
             int q = 0;
-            for (; q + 4 <= deg; q += 4) {
+            for (; q + 4 <= deg; q += 4) {     // fetch 4 ids ahead; sums stay in CSR order
               int j[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) j[u] = __ldg(colv + qb + q + u);
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                const float* hj = H + j[u] * 24;
+                const float* hj = Hc + j[u] * 24;
                 const float2 v0 = *reinterpret_cast<const float2*>(hj + 2 * t);
                 const float2 v1 = *reinterpret_cast<const float2*>(hj + 8 + 2 * t);
                 const float2 v2 = *reinterpret_cast<const float2*>(hj + 16 + 2 * t);
@@ -195,31 +196,18 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
               }
             }
             for (; q < deg; ++q) {
-              const float* hj = H + __ldg(colv + qb + q) * 24;
+              const float* hj = Hc + __ldg(colv + qb + q) * 24;
               const float2 v0 = *reinterpret_cast<const float2*>(hj + 2 * t);
               const float2 v1 = *reinterpret_cast<const float2*>(hj + 8 + 2 * t);
               const float2 v2 = *reinterpret_cast<const float2*>(hj + 16 + 2 * t);
               s0.x += v0.x; s0.y += v0.y; s1.x += v1.x; s1.y += v1.y; s2.x += v2.x; s2.y += v2.y;
             }
           }
-          float* sr = S + row * 24;
-          *reinterpret_cast<float2*>(sr + 2 * t) = s0;
-          *reinterpret_cast<float2*>(sr + 8 + 2 * t) = s1;
-          *reinterpret_cast<float2*>(sr + 16 + 2 * t) = s2;
-        }
-      }
-      __syncthreads();
-      // (B) gates and update, lane-local
-      for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
-        float s[2][6], h[2][6];
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int row = tile * 16 + g + 8 * rr;
+          s[rr][0] = s0.x; s[rr][1] = s0.y; s[rr][2] = s1.x; s[rr][3] = s1.y; s[rr][4] = s2.x; s[rr][5] = s2.y;
 #pragma unroll
           for (int c = 0; c < 6; c += 2) {
-            const float2 sv = *reinterpret_cast<const float2*>(S + row * 24 + COLS(c));
-            const float2 hv = *reinterpret_cast<const float2*>(H + row * 24 + COLS(c));
-            s[rr][c] = sv.x; s[rr][c + 1] = sv.y; h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
+            const float2 hv = *reinterpret_cast<const float2*>(Hc + row * 24 + COLS(c));
+            h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
           }
         }
         uint32_t ahi[3][4], alo[3][4];
@@ -251,16 +239,15 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             for (int e = 0; e < 2; ++e) {
               const int c = 2 * j + e;
               const float hh = fs_tanh(Dh[j][2 * rr + e] + bh[c]);
-              hn[c] = fmaf(z[rr][c], hh - h[rr][c], h[rr][c]);
+              hn[c] = row < n ? fmaf(z[rr][c], hh - h[rr][c], h[rr][c]) : 0.f;
             }
-          if (row < n) {
 #pragma unroll
-            for (int c = 0; c < 6; c += 2)
-              *reinterpret_cast<float2*>(H + row * 24 + COLS(c)) = make_float2(hn[c], hn[c + 1]);
-          }
+          for (int c = 0; c < 6; c += 2)
+            *reinterpret_cast<float2*>(Hn + row * 24 + COLS(c)) = make_float2(hn[c], hn[c + 1]);
         }
       }
       __syncthreads();
+      float* tmp = Hc; Hc = Hn; Hn = tmp;
     }
   }
 
@@ -272,7 +259,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   // is large enough, else read them through L1
   const uint32_t* gsrc = a.gfrag;
   if (npad * 24 >= kGatherWords) {
-    uint32_t* gs = reinterpret_cast<uint32_t*>(S);
+    uint32_t* gs = reinterpret_cast<uint32_t*>(Hn);
     for (int i = threadIdx.x; i < kGatherWords; i += blockDim.x) gs[i] = a.gfrag[i];
     gsrc = gs;
   }
@@ -286,7 +273,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       const int row = tile * 16 + g + 8 * rr;
 #pragma unroll
       for (int c = 0; c < 6; c += 2) {
-        const float2 hv = *reinterpret_cast<const float2*>(H + row * 24 + COLS(c));
+        const float2 hv = *reinterpret_cast<const float2*>(Hc + row * 24 + COLS(c));
         h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
       }
     }

@@ -133,10 +133,12 @@ class Screen:
         return res
 
 
-def merge_topk_across_ranks(top_s, top_i, k, group=None):
+def merge_topk_across_ranks(top_s, top_i, k, group=None, merge=None):
     """All-gather every rank's top-k (NCCL over NVLink) and merge on device.
-    Ranks holding fewer than k entries pad with NaN (ranked last)."""
+    Ranks holding fewer than k entries pad with NaN (ranked last).  `merge`
+    defaults to the device kernel fs_topk_merge (tests pass a CPU rule)."""
     import torch.distributed as dist
+    merge = merge or (lambda s, i, kk: E.topk_merge(s, i, None, None, kk))
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return top_s, top_i
     ws = dist.get_world_size(group)
@@ -148,4 +150,4 @@ def merge_topk_across_ranks(top_s, top_i, k, group=None):
     gi = torch.empty(ws * k, dtype=torch.int64, device=top_s.device)
     dist.all_gather_into_tensor(gs, pad_s, group=group)
     dist.all_gather_into_tensor(gi, pad_i, group=group)
-    return E.topk_merge(gs, gi, None, None, k)
+    return merge(gs, gi, k)
