@@ -203,10 +203,23 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   __syncthreads();
   // cell k spans [cell_start[k-1], cell_start[k]) now (cell_start[-1] := 0)
 
-  const float tcf = (float)a.tc + 1e-3f, tnf = (float)a.tn + 1e-3f;
-  const float tcf2 = tcf * tcf, tnf2 = tnf * tnf;
   const double rmax = fmax(a.tc, a.tn);
   const double rmax2 = __dmul_rn(rmax, rmax);
+  // fp32 decision band.  With |coords| <= M the fp32 distance differs from
+  // the float64 one by < 2^-21*M + 4 ulp; outside [t - delta, t + delta] the
+  // fp32 test decides exactly, inside it the float64 predicate runs.
+  const float delta = 1e-5f + 2e-6f * (float)absmax;
+  const float c_lo2 = ((float)a.tc - delta) * ((float)a.tc - delta), c_hi2 = ((float)a.tc + delta) * ((float)a.tc + delta);
+  const float n_lo2 = ((float)a.tn - delta) * ((float)a.tn - delta), n_hi2 = ((float)a.tn + delta) * ((float)a.tn + delta);
+  // 1: edge, 0: not, decided in fp32; otherwise the exact float64 predicate
+  auto decide = [&](float d2f, float lo2, float hi2, double xi, double yi, double zi, int j, double t) -> bool {
+    if (prefilter) {
+      if (d2f > hi2) return false;
+      if (d2f <= lo2) return true;
+    }
+    double d;
+    return exact_edge(px, xi, yi, zi, j, rmax2, t, &d);
+  };
 
   // ---- non-covalent: bipartite S x L ----
   const int n1 = n - n0;
@@ -232,8 +245,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
           const int j = Llist[lj];
           const float4 fj = pf[j];
           const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
-          double d;
-          if (!prefilter || dx * dx + dy * dy + dz * dz <= tnf2) hit = exact_edge(px, xi, yi, zi, j, rmax2, a.tn, &d);
+          hit = decide(dx * dx + dy * dy + dz * dz, n_lo2, n_hi2, xi, yi, zi, j, a.tn);
         }
         const unsigned m = __ballot_sync(0xffffffffu, hit);
         cnt += __popc(m);
@@ -259,9 +271,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         const int j = role_list[q];
         const float4 fj = pf[j];
         const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
-        double d;
-        if (prefilter && dx * dx + dy * dy + dz * dz > tnf2) continue;
-        c += exact_edge(px, xi, yi, zi, j, rmax2, a.tn, &d);
+        c += decide(dx * dx + dy * dy + dz * dz, n_lo2, n_hi2, xi, yi, zi, j, a.tn);
       }
       offn[i] = c;
     }
@@ -289,16 +299,14 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
           if (j == i) continue;
           const float4 fj = pf[j];
           const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
-          if (prefilter && ddx * ddx + ddy * ddy + ddz * ddz > tcf2) continue;
-          double d;
-          if (exact_edge(px, xi, yi, zi, j, rmax2, a.tc, &d)) emit(j, d);
+          if (decide(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, xi, yi, zi, j, a.tc)) emit(j);
         }
       }
     }
   };
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     int c = 0;
-    cov_scan(i, [&](int, double) { ++c; });
+    cov_scan(i, [&](int) { ++c; });
     offc[i] = c;
   }
   __syncthreads();
@@ -366,11 +374,9 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         const int j = role_list[q];
         const float4 fj = pf[j];
         const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
-        if (prefilter && dx * dx + dy * dy + dz * dz > tnf2) continue;
-        double d;
-        if (exact_edge(px, xi, yi, zi, j, rmax2, a.tn, &d)) {
+        if (decide(dx * dx + dy * dy + dz * dz, n_lo2, n_hi2, xi, yi, zi, j, a.tn)) {
           coln[o] = j;
-          if (DIST) distn[o] = d;
+          if (DIST) { double d; exact_edge(px, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
           ++o;
         }
       }
@@ -382,9 +388,13 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int rb = offc[i];
     int o = rb;
-    cov_scan(i, [&](int j, double d) {
+    cov_scan(i, [&](int j) {
       colc[o] = j;
-      if (DIST) distc[o] = d;
+      if (DIST) {
+        double d;
+        exact_edge(px, px[3 * i], px[3 * i + 1], px[3 * i + 2], j, rmax2, a.tc, &d);
+        distc[o] = d;
+      }
       ++o;
     });
     for (int x = rb + 1; x < o; ++x) {
