@@ -548,7 +548,9 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
     q.gfrag = reinterpret_cast<const uint32_t*>(m.P(m.gm_gf)); q.gbias = m.P(m.gm_gb);
     q.k_steps[0] = m.d.k_cov; q.k_steps[1] = m.d.k_noncov;
     q.lat = g.lat; q.ld_lat = g.ld_lat; q.err = err;
-    rc = launch_gnn_mma(q, 3, P, max_nodes, st);
+    // bf16 hi/lo 3-pass (fp32-class, default) or single bf16 pass (FS_GNN_SPLIT=1)
+    static const int split = (getenv("FS_GNN_SPLIT") && atoi(getenv("FS_GNN_SPLIT")) == 1) ? 1 : 3;
+    rc = launch_gnn_mma(q, split, P, max_nodes, st);
   } else {
     rc = launch_gnn(g, m.dpad, P, max_nodes, st);
   }

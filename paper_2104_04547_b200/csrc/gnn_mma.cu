@@ -95,8 +95,12 @@ template <int SPLIT, int NT>
 __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[3][4], const uint32_t (&alo)[3][4],
                                        const uint32_t* __restrict__ fhi, const uint32_t* __restrict__ flo,
                                        int lane) {
+  float C[NT][4];   // small cross terms accumulate separately: independent MMA chains
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) { D[nt][0] = D[nt][1] = D[nt][2] = D[nt][3] = 0.f; }
+  for (int nt = 0; nt < NT; ++nt) {
+    D[nt][0] = D[nt][1] = D[nt][2] = D[nt][3] = 0.f;
+    C[nt][0] = C[nt][1] = C[nt][2] = C[nt][3] = 0.f;
+  }
 #pragma unroll
   for (int kt = 0; kt < 3; ++kt)
 #pragma unroll
@@ -104,11 +108,17 @@ __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[
       const uint2 bh = *reinterpret_cast<const uint2*>(fhi + ((kt * NT + nt) * 32 + lane) * 2);
       if (SPLIT == 3) {
         const uint2 bl = *reinterpret_cast<const uint2*>(flo + ((kt * NT + nt) * 32 + lane) * 2);
-        mma_bf16(D[nt], alo[kt], bh.x, bh.y);
-        mma_bf16(D[nt], ahi[kt], bl.x, bl.y);
+        mma_bf16(C[nt], alo[kt], bh.x, bh.y);
+        mma_bf16(C[nt], ahi[kt], bl.x, bl.y);
       }
       mma_bf16(D[nt], ahi[kt], bh.x, bh.y);
     }
+  if (SPLIT == 3) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) D[nt][q] += C[nt][q];
+  }
 }
 
 template <int SPLIT>
@@ -152,6 +162,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
                 : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 
+  int* tile_ctr = reinterpret_cast<int*>(RED);   // 2 counters; RED is free until the pool
+  if (threadIdx.x == 0) { tile_ctr[0] = 0; tile_ctr[1] = 0; }
+  int gstep = 0;
   for (int ph = 0; ph < 2; ++ph) {
     __syncthreads();
     for (int i = threadIdx.x; i < kPhaseWords; i += blockDim.x) WF[i] = a.wfrag[ph][i];
@@ -172,7 +185,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       // one pass per tile: neighbour sums (CSR order) of the old states land
       // directly in this lane's A-fragment positions, the update is written
       // to the other buffer -> one barrier per step
-      for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
+      // tiles are handed out dynamically (warp-granular atomic counter) so
+      // the slowest warp finishes within ~one tile of the others
+      int* ctr = tile_ctr + (gstep & 1);
+      for (int tile = warp;;) {
+        if (tile >= ntiles) break;
         float s[2][6], h[2][6];
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
@@ -226,7 +243,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
               z[rr][c] = fs_sigmoid(Dzr[j][2 * rr + e] + bz[c]);
               rh[rr][c] = fs_sigmoid(Dzr[3 + j][2 * rr + e] + br[c]) * h[rr][c];
             }
-        build_a48<SPLIT>(s, rh, ahi, alo);
+        // A = [s | r*h]: the s part (k-tile 0 and half of k-tile 1) is reused
+        put_a<SPLIT>(ahi[1], alo[1], 2, rh[0][0], rh[0][1]);
+        put_a<SPLIT>(ahi[1], alo[1], 3, rh[1][0], rh[1][1]);
+        put_a<SPLIT>(ahi[2], alo[2], 0, rh[0][2], rh[0][3]);
+        put_a<SPLIT>(ahi[2], alo[2], 1, rh[1][2], rh[1][3]);
+        put_a<SPLIT>(ahi[2], alo[2], 2, rh[0][4], rh[0][5]);
+        put_a<SPLIT>(ahi[2], alo[2], 3, rh[1][4], rh[1][5]);
         float Dh[3][4];
         gemm48<SPLIT, 3>(Dh, ahi, alo, hh_hi, hh_lo, lane);
 #pragma unroll
@@ -245,7 +268,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           for (int c = 0; c < 6; c += 2)
             *reinterpret_cast<float2*>(Hn + row * 24 + COLS(c)) = make_float2(hn[c], hn[c + 1]);
         }
+        int next = 0;
+        if (lane == 0) next = atomicAdd(ctr, 1) + kMmaWarps;
+        tile = __shfl_sync(0xffffffffu, next, 0);
       }
+      if (threadIdx.x == 0) tile_ctr[(gstep + 1) & 1] = 0;   // next step's counter (last used 2 steps ago)
+      ++gstep;
       __syncthreads();
       float* tmp = Hc; Hc = Hn; Hn = tmp;
     }
