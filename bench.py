@@ -323,7 +323,9 @@ def main():
                     "peak": bf16_sus, "unit": "TFLOP/s", "traffic": None}
         elif dom_name == "gnn":
             flop = graph_flop(n_mean, 5152, 9094) * B
-            roof = {"kernel": "gnn (fused GRU message passing, FFMA fp32)", "bound": "tensor",
+            gk = ("gnn_mma_kernel (GRU message passing on mma.sync, bf16 hi/lo split)" if precision == "bf16"
+                  else "gnn_kernel (GRU message passing, FFMA fp32)")
+            roof = {"kernel": gk, "bound": "tensor",
                     "achieved": flop / (avg_ms / 1e3) / 1e12, "peak": bf16_sus, "unit": "TFLOP/s",
                     "traffic": None}
         else:

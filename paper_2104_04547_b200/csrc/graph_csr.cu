@@ -32,13 +32,13 @@ struct GraphCsrArgs {
 
 constexpr int kCsrThreads = 256;
 constexpr int kCsrWarps = kCsrThreads / 32;
-constexpr int kCellsAxis = 12;
-constexpr int kMaskWords = 4;         // bipartite bitmask path for |S| <= 128
+constexpr int kCellsAxis = 9;           // cells grow past t_cov for boxes > 9*t_cov
+constexpr int kMaskWords = 2;         // bipartite bitmask path for |S| <= 64
 
 __host__ __device__ inline size_t graph_csr_smem_bytes(int n) {
   n = (n + 3) & ~3;   // keeps every sub-array 16-byte aligned
   const size_t cells = 2 * kCellsAxis * kCellsAxis * kCellsAxis + 2;
-  return (size_t)n * 24 + (size_t)n * 16 + (size_t)n * 4 * 4 + (size_t)(n + 1) * 4 * 2 + (size_t)n * kMaskWords * 4 + cells * 4 + 512;
+  return (size_t)n * 16 + (size_t)n * 4 * 4 + (size_t)(n + 1) * 4 * 2 + (size_t)n * kMaskWords * 4 + cells * 4 + 512;
 }
 
 // in-place exclusive scan of a[0..n) (n+1-th entry receives the total)
@@ -68,10 +68,13 @@ __device__ void block_exclusive_scan(int* a, int n, int* warp_tot) {
   __syncthreads();
 }
 
-// exact float64 predicate on coordinates staged in shared memory (px = xyz)
-__device__ __forceinline__ bool exact_edge(const double* __restrict__ px, double xi, double yi, double zi, int j,
+// exact float64 predicate; coordinates come from global memory (the fp32
+// band test makes this path rare on the scoring path)
+__device__ __forceinline__ bool exact_edge(const PoseView& pv, double xi, double yi, double zi, int j,
                                            double rmax2, double t, double* dout) {
-  const double d2 = dist2_exact(xi - px[3 * j], yi - px[3 * j + 1], zi - px[3 * j + 2]);
+  double xj, yj, zj; int32_t ej, rj;
+  pv.atom(j, xj, yj, zj, ej, rj);
+  const double d2 = dist2_exact(xi - xj, yi - yj, zi - zj);
   if (!(d2 <= rmax2)) return false;
   const double d = __dsqrt_rn(d2);
   if (!(d <= t)) return false;
@@ -105,8 +108,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   if (threadIdx.x == 0) { s_flags = 0; s_role_cnt[0] = 0; s_role_cnt[1] = 0; }
   if (n > a.smem_atoms) { fail(FS_ERR_TOO_LARGE); return; }
   const int SA = (a.smem_atoms + 3) & ~3;   // 16-byte aligned sub-arrays
-  double* px = reinterpret_cast<double*>(smem_raw);                  // [n][3] float64
-  float4* pf = reinterpret_cast<float4*>(px + 3 * SA);
+  float4* pf = reinterpret_cast<float4*>(smem_raw);
   int* keys = reinterpret_cast<int*>(pf + SA);
   int* cell_list = keys + SA;
   int* role_list = cell_list + SA;      // role 0 ids ascending, then role 1 ids ascending
@@ -126,7 +128,6 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     if (r != 0 && r != 1) flags |= FS_ERR_ROLE;
     if (!isfinite(x) || !isfinite(y) || !isfinite(z)) flags |= FS_ERR_NONFINITE;
     pf[i] = make_float4((float)x, (float)y, (float)z, (float)r);
-    px[3 * i] = x; px[3 * i + 1] = y; px[3 * i + 2] = z;
     lo[0] = fmin(lo[0], x); lo[1] = fmin(lo[1], y); lo[2] = fmin(lo[2], z);
     hi[0] = fmax(hi[0], x); hi[1] = fmax(hi[1], y); hi[2] = fmax(hi[2], z);
   }
@@ -163,9 +164,9 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
 
   // ---- counting sort by (role, cell); role lists ascending by id ----
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int r = (int)pf[i].w;
-    const int key = r * NC + (cell_coord(px[3 * i], 0) * nca + cell_coord(px[3 * i + 1], 1)) * nca +
-                    cell_coord(px[3 * i + 2], 2);
+    double x, y, z; int32_t e, r;
+    pv.atom(i, x, y, z, e, r);
+    const int key = r * NC + (cell_coord(x, 0) * nca + cell_coord(y, 1)) * nca + cell_coord(z, 2);
     keys[i] = key;
     atomicAdd(&cell_start[key], 1);
   }
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       if (d2f <= lo2) return true;
     }
     double d;
-    return exact_edge(px, xi, yi, zi, j, rmax2, t, &d);
+    return exact_edge(pv, xi, yi, zi, j, rmax2, t, &d);
   };
 
   // ---- non-covalent: bipartite S x L ----
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     __syncthreads();
     for (int si = warp; si < nS; si += kCsrWarps) {
       const int i = Slist[si];
-      const double xi = px[3 * i], yi = px[3 * i + 1], zi = px[3 * i + 2];
+      double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
       const float4 fi = pf[i];
       int cnt = 0;
       for (int l0 = 0; l0 < nL; l0 += 32) {
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   } else {
     // large bipartite sides: one thread per row scans the other role's list
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const double xi = px[3 * i], yi = px[3 * i + 1], zi = px[3 * i + 2];
+      double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
       const float4 fi = pf[i];
       const int ri = (int)fi.w;
       const int ob = ri == 0 ? n0 : 0, oe = ri == 0 ? n : n0;
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
 
   // ---- covalent degrees: 27-cell stencil, one thread per row ----
   auto cov_scan = [&](int i, auto&& emit) {
-    const double xi = px[3 * i], yi = px[3 * i + 1], zi = px[3 * i + 2];
+    double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
     const float4 fi = pf[i];
     const int ri = (int)fi.w;
     const int key = keys[i] - ri * NC;
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   if (use_mask) {
     for (int si = warp; si < nS; si += kCsrWarps) {          // S rows: L ids ascending
       const int i = Slist[si];
-      const double xi = px[3 * i], yi = px[3 * i + 1], zi = px[3 * i + 2];
+      double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
       int w = offn[i];
       for (int l0 = 0; l0 < nL; l0 += 32) {
         const int lj = l0 + lane;
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
           const int o = w + __popc(m & ((1u << lane) - 1u));
           const int j = Llist[lj];
           coln[o] = j;
-          if (DIST) { double d; exact_edge(px, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
+          if (DIST) { double d; exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
         }
         w += __popc(m);
       }
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     for (int lj = threadIdx.x; lj < nL; lj += blockDim.x) {  // L rows: S ids ascending
       const int i = Llist[lj];
       int o = offn[i];
-      const double xi = px[3 * i], yi = px[3 * i + 1], zi = px[3 * i + 2];
+      double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
       for (int w = 0; w < W; ++w) {
         uint32_t bits = mask[lj * W + w];
         while (bits) {
@@ -358,14 +359,14 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
           bits &= bits - 1;
           const int j = Slist[32 * w + b];
           coln[o] = j;
-          if (DIST) { double d; exact_edge(px, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
+          if (DIST) { double d; exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
           ++o;
         }
       }
     }
   } else {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const double xi = px[3 * i], yi = px[3 * i + 1], zi = px[3 * i + 2];
+      double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
       const float4 fi = pf[i];
       const int ri = (int)fi.w;
       const int ob = ri == 0 ? n0 : 0, oe = ri == 0 ? n : n0;
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
         if (decide(dx * dx + dy * dy + dz * dz, n_lo2, n_hi2, xi, yi, zi, j, a.tn)) {
           coln[o] = j;
-          if (DIST) { double d; exact_edge(px, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
+          if (DIST) { double d; exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
           ++o;
         }
       }
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       colc[o] = j;
       if (DIST) {
         double d;
-        exact_edge(px, px[3 * i], px[3 * i + 1], px[3 * i + 2], j, rmax2, a.tc, &d);
+        double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_); exact_edge(pv, xi, yi, zi, j, rmax2, a.tc, &d);
         distc[o] = d;
       }
       ++o;
