@@ -133,17 +133,19 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     return;
   }
   const int ntiles = (n + 15) / 16, npad = ntiles * 16;
-  float* Hc = sm;                                  // [npad][24] node state (fp32), current
-  float* Hn = Hc + npad * 24;                      // [npad][24] next (double buffer)
-  uint32_t* WF = reinterpret_cast<uint32_t*>(Hn + npad * 24);  // phase fragments
+  // node states, double buffered: [npad + 1][24] each; row npad stays zero
+  float* Hc = sm;
+  float* Hn = Hc + (npad + 1) * 24;
+  uint32_t* WF = reinterpret_cast<uint32_t*>(Hn + (npad + 1) * 24);  // phase fragments
   float* WB = reinterpret_cast<float*>(WF + kPhaseWords);      // phase biases [72]
   float* RED = WB + 72;                                        // [warps][128]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
 #define COLS(c) ((c) < 2 ? 2 * t + (c) : (c) < 4 ? 6 + 2 * t + (c) : 12 + 2 * t + (c))
 
-  // ---- embedding h0 = tanh(X.We + be); padded rows are zero ----
-  for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+  // ---- embedding h0 = tanh(X.We + be); padded rows (and row npad) are zero ----
+  for (int i = threadIdx.x; i < 24; i += blockDim.x) Hn[npad * 24 + i] = 0.f;
+  for (int i = threadIdx.x; i <= npad; i += blockDim.x) {
     float acc[24];
 #pragma unroll
     for (int k = 0; k < 24; ++k) acc[k] = i < n ? a.be[k] : 0.f;
@@ -191,40 +193,45 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       for (int tile = warp;;) {
         if (tile >= ntiles) break;
         float s[2][6], h[2][6];
+        {
+          // Both rows of the lane, 8 neighbours at a time: 16 id loads are in
+          // flight before the shared-memory gathers; exhausted slots read the
+          // all-zero row `npad` (x + 0 == x, so sums stay exactly CSR-ordered).
+          const int r0 = tile * 16 + g, r1 = r0 + 8;
+          const int d0 = r0 < n ? degs[base + r0] : 0, d1 = r1 < n ? degs[base + r1] : 0;
+          const int32_t* c0 = colv + (r0 < n ? rows[base + r0] : 0);
+          const int32_t* c1 = colv + (r1 < n ? rows[base + r1] : 0);
+          const int dm = max(d0, d1);
+          float a0[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, a1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          for (int q = 0; q < dm; q += 8) {
+            int j0[8], j1[8];
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int row = tile * 16 + g + 8 * rr;
-          float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0;
-          if (row < n) {
-            const int64_t qb = rows[base + row];
-            const int deg = degs[base + row];
-            int q = 0;
-            for (; q + 4 <= deg; q += 4) {     // fetch 4 ids ahead; sums stay in CSR order
-              int j[4];
+            for (int u = 0; u < 8; ++u) j0[u] = q + u < d0 ? __ldg(c0 + q + u) : npad;
 #pragma unroll
-              for (int u = 0; u < 4; ++u) j[u] = __ldg(colv + qb + q + u);
+            for (int u = 0; u < 8; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const float* hj = Hc + j[u] * 24;
-                const float2 v0 = *reinterpret_cast<const float2*>(hj + 2 * t);
-                const float2 v1 = *reinterpret_cast<const float2*>(hj + 8 + 2 * t);
-                const float2 v2 = *reinterpret_cast<const float2*>(hj + 16 + 2 * t);
-                s0.x += v0.x; s0.y += v0.y; s1.x += v1.x; s1.y += v1.y; s2.x += v2.x; s2.y += v2.y;
+            for (int u = 0; u < 8; ++u) {
+              const float* p0 = Hc + j0[u] * 24 + 2 * t;
+              const float* p1 = Hc + j1[u] * 24 + 2 * t;
+#pragma unroll
+              for (int k = 0; k < 3; ++k) {
+                const float2 v0 = *reinterpret_cast<const float2*>(p0 + 8 * k);
+                const float2 v1 = *reinterpret_cast<const float2*>(p1 + 8 * k);
+                a0[2 * k] += v0.x; a0[2 * k + 1] += v0.y;
+                a1[2 * k] += v1.x; a1[2 * k + 1] += v1.y;
               }
             }
-            for (; q < deg; ++q) {
-              const float* hj = Hc + __ldg(colv + qb + q) * 24;
-              const float2 v0 = *reinterpret_cast<const float2*>(hj + 2 * t);
-              const float2 v1 = *reinterpret_cast<const float2*>(hj + 8 + 2 * t);
-              const float2 v2 = *reinterpret_cast<const float2*>(hj + 16 + 2 * t);
-              s0.x += v0.x; s0.y += v0.y; s1.x += v1.x; s1.y += v1.y; s2.x += v2.x; s2.y += v2.y;
-            }
           }
-          s[rr][0] = s0.x; s[rr][1] = s0.y; s[rr][2] = s1.x; s[rr][3] = s1.y; s[rr][4] = s2.x; s[rr][5] = s2.y;
 #pragma unroll
-          for (int c = 0; c < 6; c += 2) {
-            const float2 hv = *reinterpret_cast<const float2*>(Hc + row * 24 + COLS(c));
-            h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
+          for (int c = 0; c < 6; ++c) { s[0][c] = a0[c]; s[1][c] = a1[c]; }
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const int row = rr ? r1 : r0;
+#pragma unroll
+            for (int c = 0; c < 6; c += 2) {
+              const float2 hv = *reinterpret_cast<const float2*>(Hc + row * 24 + COLS(c));
+              h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
+            }
           }
         }
         uint32_t ahi[3][4], alo[3][4];
@@ -372,7 +379,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 
 size_t gnn_mma_smem_bytes(int max_nodes) {
   const int npad = (max_nodes + 15) / 16 * 16;
-  return static_cast<size_t>(2) * npad * 24 * 4 + kPhaseWords * 4 + 72 * 4 + kMmaWarps * 128 * 4 + 64;
+  return static_cast<size_t>(2) * (npad + 1) * 24 * 4 + kPhaseWords * 4 + 72 * 4 + kMmaWarps * 128 * 4 + 64;
 }
 
 bool gnn_mma_fits(int max_nodes) { return gnn_mma_smem_bytes(max_nodes) <= 227 * 1024; }
