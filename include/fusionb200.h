@@ -243,6 +243,19 @@ int fs_best_pose(const int64_t* compound, const int64_t* pose_id,
                  int32_t direction, int64_t* best_idx, uint64_t* best_key,
                  void* stream);
 
+/* Streaming best pose for screens: fold a batch of (compound, pose_id, score)
+ * rows into best_key[n_compounds] (row compound c -> slot c - compound_base;
+ * rows outside the range are ignored).  best_key must start all-ones
+ * (0xff bytes).  Same rule as evaluate.aggregate_best_pose (:67-83).  Then
+ * decode to (best_score, best_pose) per compound (-1 / NaN: no rows). */
+int fs_best_pose_update(const int64_t* compound, int64_t compound_base,
+                        const int64_t* pose_id, const float* scores, int64_t n,
+                        int64_t n_compounds, int32_t direction, uint64_t* best_key,
+                        void* stream);
+int fs_best_pose_decode(const uint64_t* best_key, int64_t n_compounds,
+                        int32_t direction, float* best_score, int64_t* best_pose,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,7 +32,7 @@ EXPORTS = (
     "fs_voxelize", "fs_node_features", "fs_graph_count", "fs_graph_rows", "fs_graph_rows_ws_bytes",
     "fs_graph_fill", "fs_graph_edge_counts", "fs_graph_edges", "fs_workspace_bytes",
     "fs_score_poses", "fs_score_features", "fs_debug_conv", "fs_topk_ws_bytes", "fs_topk_merge",
-    "fs_best_pose",
+    "fs_best_pose", "fs_best_pose_update", "fs_best_pose_decode",
 )
 
 
@@ -107,6 +107,8 @@ def _sig(lib):
         "fs_topk_ws_bytes": (_SZ, [_I64]),
         "fs_topk_merge": (C.c_int, [_P, _P, _I64, _P, _P, _I64, _I32, _P, _P, _P, _SZ, _P]),
         "fs_best_pose": (C.c_int, [_P, _P, _P, _I64, _I64, _I32, _P, _P, _P]),
+        "fs_best_pose_update": (C.c_int, [_P, _I64, _P, _P, _I64, _I64, _I32, _P, _P]),
+        "fs_best_pose_decode": (C.c_int, [_P, _I64, _I32, _P, _P, _P]),
     }
     for name, (res, args) in t.items():
         f = getattr(lib, name)

@@ -86,6 +86,8 @@ bool gnn_needs_global_state(int dpad, int max_nodes);
 size_t topk_ws_bytes(int64_t n);
 int launch_topk_merge(const float* as, const int64_t* ai, int64_t na, const float* bs, const int64_t* bi, int64_t nb, int k, float* os, int64_t* oi, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_best_pose(const int64_t* compound, const int64_t* pose_id, const float* s, int64_t n, int64_t n_compounds, int dir, int64_t* best_idx, uint64_t* best_key, cudaStream_t st);
+int launch_best_update(const int64_t* compound, int64_t base, const int64_t* pose_id, const float* s, int64_t n, int64_t n_compounds, int dir, uint64_t* best_key, cudaStream_t st);
+int launch_best_decode(const uint64_t* best_key, int64_t n, int dir, float* score, int64_t* pose, cudaStream_t st);
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -885,6 +887,19 @@ int fs_best_pose(const int64_t* compound, const int64_t* pose_id, const float* s
   if (!compound || !pose_id || !scores || !best_idx || !best_key || n < 0) return FS_EINVAL;
   return launch_best_pose(compound, pose_id, scores, n, n_compounds, direction, best_idx, best_key,
                           (cudaStream_t)stream);
+}
+
+int fs_best_pose_update(const int64_t* compound, int64_t compound_base, const int64_t* pose_id, const float* scores,
+                        int64_t n, int64_t n_compounds, int32_t direction, uint64_t* best_key, void* stream) {
+  if (!compound || !pose_id || !scores || !best_key || n < 0 || n_compounds < 0) return FS_EINVAL;
+  return launch_best_update(compound, compound_base, pose_id, scores, n, n_compounds, direction, best_key,
+                            (cudaStream_t)stream);
+}
+
+int fs_best_pose_decode(const uint64_t* best_key, int64_t n_compounds, int32_t direction, float* best_score,
+                        int64_t* best_pose, void* stream) {
+  if (!best_key || !best_score || !best_pose || n_compounds < 0) return FS_EINVAL;
+  return launch_best_decode(best_key, n_compounds, direction, best_score, best_pose, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -106,4 +106,45 @@ int launch_best_pose(const int64_t* compound, const int64_t* pose_id, const floa
   return FS_OK;
 }
 
+// Streaming form: fold a batch into per-compound keys (no reset), then decode.
+__global__ void best_update_kernel(const int64_t* compound, int64_t base, const int64_t* pose_id, const float* s,
+                                   int64_t n, int64_t n_compounds, int dir, unsigned long long* best) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t c = compound[t] - base;
+  if (c < 0 || c >= n_compounds) return;
+  float v = dir > 0 ? s[t] : -s[t];
+  unsigned long long key = ((unsigned long long)score_desc_bits(v) << 32) | (uint32_t)pose_id[t];
+  atomicMin(&best[c], key);
+}
+
+__global__ void best_decode_kernel(const unsigned long long* best, int64_t n, int dir, float* score,
+                                   int64_t* pose) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const unsigned long long k = best[t];
+  if (k == ~0ull) { score[t] = __int_as_float(0x7fc00000); pose[t] = -1; return; }
+  const float v = score_from_bits((uint32_t)(k >> 32));
+  score[t] = dir > 0 ? v : -v;
+  pose[t] = (int64_t)(uint32_t)k;
+}
+
+int launch_best_update(const int64_t* compound, int64_t base, const int64_t* pose_id, const float* s, int64_t n,
+                       int64_t n_compounds, int dir, uint64_t* best_key, cudaStream_t st) {
+  if (dir != 1 && dir != -1) return FS_EINVAL;
+  if (n <= 0) return FS_OK;
+  best_update_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(compound, base, pose_id, s, n, n_compounds, dir,
+                                                            (unsigned long long*)best_key);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
+int launch_best_decode(const uint64_t* best_key, int64_t n, int dir, float* score, int64_t* pose, cudaStream_t st) {
+  if (dir != 1 && dir != -1) return FS_EINVAL;
+  if (n <= 0) return FS_OK;
+  best_decode_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>((const unsigned long long*)best_key, n, dir, score, pose);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
 }  // namespace fs

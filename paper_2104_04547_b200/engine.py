@@ -421,3 +421,28 @@ def best_pose(compound, pose_id, scores, n_compounds, direction="max"):
     N.check(L.fs_best_pose(_ptr(compound), _ptr(pose_id), _ptr(scores), scores.numel(), n_compounds,
                            1 if direction == "max" else -1, _ptr(idx), _ptr(key), _stream()), "fs_best_pose")
     return idx[:n_compounds]
+
+
+class BestPoseAccumulator:
+    """Per-compound best pose folded batch by batch on device
+    (fs_best_pose_update/decode; rule of evaluate.aggregate_best_pose)."""
+
+    def __init__(self, n_compounds, compound_base=0, direction="max", device=None):
+        if direction not in ("max", "min"):
+            raise ValueError(f"direction must be max or min, got {direction!r}")
+        self.n = int(n_compounds)
+        self.base = int(compound_base)
+        self.dir = 1 if direction == "max" else -1
+        dev = _require_cuda(device)
+        self.keys = torch.full((max(self.n, 1),), -1, dtype=torch.int64, device=dev)   # all-ones
+
+    def update(self, compound, pose_id, scores):
+        N.check(N.lib().fs_best_pose_update(_ptr(compound), self.base, _ptr(pose_id), _ptr(scores), scores.numel(),
+                                            self.n, self.dir, _ptr(self.keys), _stream()), "fs_best_pose_update")
+
+    def result(self):
+        s = torch.empty(max(self.n, 1), dtype=torch.float32, device=self.keys.device)
+        p = torch.empty(max(self.n, 1), dtype=torch.int64, device=self.keys.device)
+        N.check(N.lib().fs_best_pose_decode(_ptr(self.keys), self.n, self.dir, _ptr(s), _ptr(p), _stream()),
+                "fs_best_pose_decode")
+        return s[: self.n], p[: self.n]

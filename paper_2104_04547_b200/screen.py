@@ -31,6 +31,8 @@ class DeviceLibrary:
         self.atom_off = torch.from_numpy(np.ascontiguousarray(lib.atom_off, dtype=np.int64)).to(device)
         self.target = torch.from_numpy(np.ascontiguousarray(lib.target, dtype=np.int32)).to(device)
         self.pidx = torch.arange(self.index_base, self.index_base + lib.n_poses, dtype=torch.int64, device=device)
+        self.compound = torch.from_numpy(np.ascontiguousarray(lib.compound, dtype=np.int64)).to(device)
+        self.pose_id = torch.from_numpy(np.ascontiguousarray(lib.pose_id, dtype=np.int64)).to(device)
         p_xyz = np.concatenate([p.xyz for p in pockets])
         p_off = np.concatenate([[0], np.cumsum([len(p.xyz) for p in pockets])]).astype(np.int64)
         self.pocket_xyz = torch.from_numpy(p_xyz).to(device)
@@ -49,6 +51,13 @@ class DeviceLibrary:
         return E.PoseBatch(self.xyz, self.elem, self.role, self.atom_off[s:e + 1], self.max_pose_atoms,
                            self.pocket_xyz, self.pocket_elem, self.pocket_role, self.pocket_off,
                            self.target[s:e])
+
+    def batches(self, batch_size):
+        """(s, e, PoseBatch, compound, pose_id) per batch; same protocol as
+        poselib.StreamingLoader.batches."""
+        for s in range(0, self.n_poses, batch_size):
+            e = min(self.n_poses, s + batch_size)
+            yield s, e, self.batch(s, e), self.compound[s:e], self.pose_id[s:e]
 
 
 class HostStager:
@@ -115,22 +124,50 @@ class Screen:
         # no host sync: overflow shows up in err (checked after the screen)
         return self.model.score_poses(batch, self.precision, self.max_edges_per_pose, outputs, retry=False)
 
-    def run(self, dlib: DeviceLibrary, keep_scores=False):
-        """Score the whole library; returns dict(topk_scores, topk_idx, err,
-        scores?).  Pose indices are global (dlib.index_base + local)."""
+    def run(self, source, keep_scores=False, best_compounds=None, compound_base=0, direction="max"):
+        """Score a whole library -- a DeviceLibrary (resident in HBM) or a
+        poselib.StreamingLoader (pinned host streaming).  Returns
+        dict(topk_scores, topk_idx, err, scores?): the running top-k over
+        poses, pose indices global (source.index_base + local).
+
+        With ``best_compounds=C`` the per-compound best pose (rule of
+        evaluate.aggregate_best_pose, evaluate.py:67-83) is folded batch by
+        batch on device for compounds [compound_base, compound_base + C)
+        and the result adds best_score[C], best_pose[C] and the top-k over
+        compounds (topk_compound_scores, topk_compound_idx)."""
         top_s = top_i = None
         errs, all_s = [], []
-        for s in range(0, dlib.n_poses, self.B):
-            e = min(dlib.n_poses, s + self.B)
-            out = self.score(dlib.batch(s, e))
-            top_s, top_i = E.topk_merge(top_s, top_i, out["scores"], dlib.pidx[s:e], self.k)
+        acc = (E.BestPoseAccumulator(best_compounds, compound_base, direction)
+               if best_compounds is not None else None)
+        base = source.index_base
+        for s, e, batch, compound, pose_id in source.batches(self.B):
+            out = self.score(batch)
+            pidx = torch.arange(base + s, base + e, dtype=torch.int64, device=out["scores"].device)
+            top_s, top_i = E.topk_merge(top_s, top_i, out["scores"], pidx, self.k)
+            if acc is not None:
+                acc.update(compound, pose_id, out["scores"])
             errs.append(out["err"])
             if keep_scores:
                 all_s.append(out["scores"])
         res = {"topk_scores": top_s, "topk_idx": top_i, "err": torch.cat(errs) if errs else None}
         if keep_scores:
             res["scores"] = torch.cat(all_s)
+        if acc is not None:
+            res.update(compound_topk(acc, self.k))
         return res
+
+
+def compound_topk(acc: E.BestPoseAccumulator, k):
+    """Decode a best-pose accumulator and rank its compounds: dict(best_score,
+    best_pose, topk_compound_scores, topk_compound_idx); compound ids are
+    global (acc.base + local), ties to the lower id, compounds without a
+    scored pose last."""
+    bs, bp = acc.result()
+    cid = torch.arange(acc.base, acc.base + acc.n, dtype=torch.int64, device=bs.device)
+    ranked = bs if acc.dir > 0 else -bs
+    cs, ci = E.topk_merge(None, None, ranked, cid, k)
+    return {"best_score": bs, "best_pose": bp, "topk_compound_scores": cs if acc.dir > 0 else -cs,
+            "topk_compound_idx": ci}
 
 
 def merge_topk_across_ranks(top_s, top_i, k, group=None, merge=None):
