@@ -4,7 +4,9 @@
 // Same math as gnn.cu (models.py:334-371): per step
 //   [z|r] = sigma([s|h] . [[Wmsg.Wz  Wmsg.Wr]; [Uz Ur]] + [bz|br])
 //   hh    = tanh ([s|r*h] . [[Wmsg.Wh]; [Uh]] + bh);   h <- h + z*(hh-h)
-// with s = sum of neighbour h rows (CSR order).  A warp owns 16-node tiles.
+// with s = sum of neighbour h rows.  Each step is two passes over shared
+// memory: (1) S = neighbour sums (degree-balanced work items, see kHeavyDeg),
+// (2) the GRU update of 16-node tiles on the tensor cores, in place.
 // The m16n8k16 fragment layouts line up so that each lane holds, for rows
 // g and g+8 (g = lane/4), exactly the columns {2t,2t+1,8+2t,9+2t,16+2t,17+2t}
 // (t = lane%4) of s, h, z, r, hh and h': the whole GRU update is lane-local
@@ -12,8 +14,9 @@
 // SPLIT = 3 keeps fp32-class accuracy: x = hi + lo (bf16 each) and
 // A.B ~ Ahi.Bhi + Ahi.Blo + Alo.Bhi (relative error ~2^-16); SPLIT = 1 is a
 // single bf16 pass.  Node states stay fp32 in shared memory.
-// Determinism: fixed tile->warp assignment, CSR-order sums, fixed reduction
-// trees -> a pose's latent is bitwise independent of its batch.
+// Determinism: every row's sum has a fixed order (CSR order, or for heavy
+// rows 8 CSR-strided partial sums in a fixed tree), fixed reduction trees,
+// fixed pool order -> a pose's latent is bitwise independent of its batch.
 #include "common.cuh"
 
 namespace fs {
@@ -121,6 +124,22 @@ __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[
   }
 }
 
+// Rows with at least kHeavyDeg neighbours are summed by a whole warp (8
+// neighbours per iteration, fixed-tree combine); lighter rows are summed 16
+// at a time in degree-sorted tiles, so a tile's lanes run out of neighbours
+// together.  Both forms read 8 (row, neighbour) pairs per 12 lane-instructions.
+constexpr int kHeavyDeg = 32;
+constexpr int kBins = kHeavyDeg + 1;
+constexpr int kCtlWords = 4 + 2 * kBins;
+
+__device__ __forceinline__ void acc_row(float (&a)[6], const float* __restrict__ src) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float2 v = *reinterpret_cast<const float2*>(src + 8 * k);
+    a[2 * k] += v.x; a[2 * k + 1] += v.y;
+  }
+}
+
 template <int SPLIT>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a) {
   extern __shared__ __align__(16) float sm[];
@@ -133,18 +152,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     return;
   }
   const int ntiles = (n + 15) / 16, npad = ntiles * 16;
-  // node states, double buffered: [npad + 1][24] each; row npad stays zero
-  float* Hc = sm;
-  float* Hn = Hc + (npad + 1) * 24;
-  uint32_t* WF = reinterpret_cast<uint32_t*>(Hn + (npad + 1) * 24);  // phase fragments
-  float* WB = reinterpret_cast<float*>(WF + kPhaseWords);      // phase biases [72]
-  float* RED = WB + 72;                                        // [warps][128]
+  const int srows = max(npad + 1, 86);   // S doubles as the pool's reduction buffer (>= 2048 floats)
+  // H: node states [npad + 1][24], row npad stays zero (padded gathers read it)
+  // S: neighbour sums [srows][24], row npad is the sink of padded tile slots
+  float* H = sm;
+  float* S = H + (npad + 1) * 24;
+  uint32_t* WF = reinterpret_cast<uint32_t*>(S + srows * 24);   // phase fragments
+  float* WB = reinterpret_cast<float*>(WF + kPhaseWords);       // phase biases [72]
+  int* CTL = reinterpret_cast<int*>(WB + 72);                  // counters[2], n_heavy, -, hist[kBins], start[kBins]
+  uint16_t* PERM = reinterpret_cast<uint16_t*>(CTL + kCtlWords);   // gather order [npad]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
 #define COLS(c) ((c) < 2 ? 2 * t + (c) : (c) < 4 ? 6 + 2 * t + (c) : 12 + 2 * t + (c))
 
   // ---- embedding h0 = tanh(X.We + be); padded rows (and row npad) are zero ----
-  for (int i = threadIdx.x; i < 24; i += blockDim.x) Hn[npad * 24 + i] = 0.f;
   for (int i = threadIdx.x; i <= npad; i += blockDim.x) {
     float acc[24];
 #pragma unroll
@@ -159,51 +180,93 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     }
 #pragma unroll
     for (int k = 0; k < 24; k += 4)
-      *reinterpret_cast<float4*>(Hc + i * 24 + k) =
+      *reinterpret_cast<float4*>(H + i * 24 + k) =
           i < n ? make_float4(fs_tanh(acc[k]), fs_tanh(acc[k + 1]), fs_tanh(acc[k + 2]), fs_tanh(acc[k + 3]))
                 : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 
-  int* tile_ctr = reinterpret_cast<int*>(RED);   // 2 counters; RED is free until the pool
-  if (threadIdx.x == 0) { tile_ctr[0] = 0; tile_ctr[1] = 0; }
   int gstep = 0;
   for (int ph = 0; ph < 2; ++ph) {
     __syncthreads();
     for (int i = threadIdx.x; i < kPhaseWords; i += blockDim.x) WF[i] = a.wfrag[ph][i];
     for (int i = threadIdx.x; i < 72; i += blockDim.x) WB[i] = a.wbias[ph][i];
-    __syncthreads();
+    if (threadIdx.x < kBins) CTL[4 + threadIdx.x] = 0;
+    if (threadIdx.x < 2) CTL[threadIdx.x] = 0;
     const int64_t* rows = ph == 0 ? a.row_cov : a.row_ncov;
     const int32_t* degs = ph == 0 ? a.deg_cov : a.deg_ncov;
     const int32_t* colv = ph == 0 ? a.col_cov : a.col_ncov;
+    __syncthreads();
+    // gather order: counting sort by degree, descending (bin 0 = heavy rows).
+    // The order inside a bin is arbitrary: a row's sum never depends on
+    // where it is gathered, so the result stays deterministic.
+    int* key = reinterpret_cast<int*>(S);     // S is scratch until the first step
+    for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+      const int d = i < n ? degs[base + i] : 0;
+      const int bin = kHeavyDeg - min(d, kHeavyDeg);
+      key[i] = (bin << 16) | atomicAdd(&CTL[4 + bin], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int b = 0; b < kBins; ++b) { CTL[4 + kBins + b] = acc; acc += CTL[4 + b]; }
+      CTL[2] = CTL[4];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < npad; i += blockDim.x)
+      PERM[CTL[4 + kBins + (key[i] >> 16)] + (key[i] & 0xffff)] = static_cast<uint16_t>(i);
+    __syncthreads();
+    const int nh = CTL[2];
+    const int nitems = nh + (npad - nh + 15) / 16;
+
     const uint32_t* zr_hi = WF;
     const uint32_t* zr_lo = WF + kZrWords;
     const uint32_t* hh_hi = WF + 2 * kZrWords;
     const uint32_t* hh_lo = WF + 2 * kZrWords + kHhWords;
-    float bz[6], br[6], bh[6];
-#pragma unroll
-    for (int c = 0; c < 6; ++c) { bz[c] = WB[COLS(c)]; br[c] = WB[24 + COLS(c)]; bh[c] = WB[48 + COLS(c)]; }
 
     for (int step = 0; step < a.k_steps[ph]; ++step) {
-      // one pass per tile: neighbour sums (CSR order) of the old states land
-      // directly in this lane's A-fragment positions, the update is written
-      // to the other buffer -> one barrier per step
-      // tiles are handed out dynamically (warp-granular atomic counter) so
-      // the slowest warp finishes within ~one tile of the others
-      int* ctr = tile_ctr + (gstep & 1);
-      for (int tile = warp;;) {
-        if (tile >= ntiles) break;
-        float s[2][6], h[2][6];
-        {
-          // Both rows of the lane, 8 neighbours at a time: 16 id loads are in
-          // flight before the shared-memory gathers; exhausted slots read the
-          // all-zero row `npad` (x + 0 == x, so sums stay exactly CSR-ordered).
-          const int r0 = tile * 16 + g, r1 = r0 + 8;
+      // ---- pass 1: S = neighbour sums of H (items handed out dynamically,
+      // heaviest first) ----
+      int* ctr = CTL + (gstep & 1);
+      for (int item = warp; item < nitems;) {
+        if (item < nh) {
+          // one heavy row: lane (q = lane/4, t) sums neighbours q, q+8, ...
+          const int row = PERM[item];
+          const int d = degs[base + row];
+          const int32_t* c = colv + rows[base + row];
+          float s6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          for (int q = g; q < d; q += 32) {
+            int j[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) j[u] = q + 8 * u < d ? __ldg(c + q + 8 * u) : npad;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc_row(s6, H + j[u] * 24 + 2 * t);
+          }
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            float v = s6[k];
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            s6[k] = v;
+          }
+          if (g == 0) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              *reinterpret_cast<float2*>(S + row * 24 + 2 * t + 8 * k) = make_float2(s6[2 * k], s6[2 * k + 1]);
+          }
+        } else {
+          // 16 degree-sorted light rows; lane (g, t) owns rows g and g+8.
+          // Exhausted slots read the all-zero row `npad` (x + 0 == x, so the
+          // sums stay exactly CSR-ordered).
+          const int k0 = nh + (item - nh) * 16 + g, k1 = k0 + 8;
+          const int r0 = k0 < npad ? PERM[k0] : npad, r1 = k1 < npad ? PERM[k1] : npad;
           const int d0 = r0 < n ? degs[base + r0] : 0, d1 = r1 < n ? degs[base + r1] : 0;
           const int32_t* c0 = colv + (r0 < n ? rows[base + r0] : 0);
           const int32_t* c1 = colv + (r1 < n ? rows[base + r1] : 0);
           const int dm = max(d0, d1);
           float a0[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, a1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          for (int q = 0; q < dm; q += 8) {
+          int q = 0;
+          for (; q + 8 <= dm; q += 8) {
             int j0[8], j1[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) j0[u] = q + u < d0 ? __ldg(c0 + q + u) : npad;
@@ -211,27 +274,51 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             for (int u = 0; u < 8; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-              const float* p0 = Hc + j0[u] * 24 + 2 * t;
-              const float* p1 = Hc + j1[u] * 24 + 2 * t;
+              acc_row(a0, H + j0[u] * 24 + 2 * t);
+              acc_row(a1, H + j1[u] * 24 + 2 * t);
+            }
+          }
+          for (; q < dm; q += 4) {
+            int j0[4], j1[4];
 #pragma unroll
-              for (int k = 0; k < 3; ++k) {
-                const float2 v0 = *reinterpret_cast<const float2*>(p0 + 8 * k);
-                const float2 v1 = *reinterpret_cast<const float2*>(p1 + 8 * k);
-                a0[2 * k] += v0.x; a0[2 * k + 1] += v0.y;
-                a1[2 * k] += v1.x; a1[2 * k + 1] += v1.y;
-              }
+            for (int u = 0; u < 4; ++u) j0[u] = q + u < d0 ? __ldg(c0 + q + u) : npad;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              acc_row(a0, H + j0[u] * 24 + 2 * t);
+              acc_row(a1, H + j1[u] * 24 + 2 * t);
             }
           }
 #pragma unroll
-          for (int c = 0; c < 6; ++c) { s[0][c] = a0[c]; s[1][c] = a1[c]; }
+          for (int k = 0; k < 3; ++k) {
+            *reinterpret_cast<float2*>(S + r0 * 24 + 2 * t + 8 * k) = make_float2(a0[2 * k], a0[2 * k + 1]);
+            *reinterpret_cast<float2*>(S + r1 * 24 + 2 * t + 8 * k) = make_float2(a1[2 * k], a1[2 * k + 1]);
+          }
+        }
+        int next = 0;
+        if (lane == 0) next = atomicAdd(ctr, 1) + kMmaWarps;
+        item = __shfl_sync(0xffffffffu, next, 0);
+      }
+      if (threadIdx.x == 0) CTL[(gstep + 1) & 1] = 0;   // next step's counter (last used 2 steps ago)
+      ++gstep;
+      __syncthreads();
+
+      // ---- pass 2: GRU update of every 16-row tile, in place ----
+      for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
+        float bz[6], br[6], bh[6];
 #pragma unroll
-          for (int rr = 0; rr < 2; ++rr) {
-            const int row = rr ? r1 : r0;
+        for (int c = 0; c < 6; ++c) { bz[c] = WB[COLS(c)]; br[c] = WB[24 + COLS(c)]; bh[c] = WB[48 + COLS(c)]; }
+        float s[2][6], h[2][6];
 #pragma unroll
-            for (int c = 0; c < 6; c += 2) {
-              const float2 hv = *reinterpret_cast<const float2*>(Hc + row * 24 + COLS(c));
-              h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
-            }
+        for (int rr = 0; rr < 2; ++rr) {
+          const int row = tile * 16 + g + 8 * rr;
+#pragma unroll
+          for (int c = 0; c < 6; c += 2) {
+            const float2 sv = *reinterpret_cast<const float2*>(S + row * 24 + COLS(c));
+            const float2 hv = *reinterpret_cast<const float2*>(H + row * 24 + COLS(c));
+            s[rr][c] = sv.x; s[rr][c + 1] = sv.y;
+            h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
           }
         }
         uint32_t ahi[3][4], alo[3][4];
@@ -273,18 +360,15 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             }
 #pragma unroll
           for (int c = 0; c < 6; c += 2)
-            *reinterpret_cast<float2*>(Hn + row * 24 + COLS(c)) = make_float2(hn[c], hn[c + 1]);
+            *reinterpret_cast<float2*>(H + row * 24 + COLS(c)) = make_float2(hn[c], hn[c + 1]);
         }
-        int next = 0;
-        if (lane == 0) next = atomicAdd(ctr, 1) + kMmaWarps;
-        tile = __shfl_sync(0xffffffffu, next, 0);
       }
-      if (threadIdx.x == 0) tile_ctr[(gstep + 1) & 1] = 0;   // next step's counter (last used 2 steps ago)
-      ++gstep;
       __syncthreads();
-      float* tmp = Hc; Hc = Hn; Hn = tmp;
     }
   }
+  float* Hc = H;
+  float* Hn = S;
+  float* RED = S;   // [warps][128], written only after every warp is done with the staged fragments
 
   // ---- gated gather + mean pool: [gate|val] = h.[Gg|Gf] (K 24->32, N 256) ----
   float acc[16][2];
@@ -293,7 +377,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   // gather fragments: stage into the (now free) neighbour-sum buffer when it
   // is large enough, else read them through L1
   const uint32_t* gsrc = a.gfrag;
-  if (npad * 24 >= kGatherWords) {
+  if (srows * 24 >= kGatherWords) {
     uint32_t* gs = reinterpret_cast<uint32_t*>(Hn);
     for (int i = threadIdx.x; i < kGatherWords; i += blockDim.x) gs[i] = a.gfrag[i];
     gsrc = gs;
@@ -379,7 +463,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 
 size_t gnn_mma_smem_bytes(int max_nodes) {
   const int npad = (max_nodes + 15) / 16 * 16;
-  return static_cast<size_t>(2) * (npad + 1) * 24 * 4 + kPhaseWords * 4 + 72 * 4 + kMmaWarps * 128 * 4 + 64;
+  const int srows = npad + 1 > 86 ? npad + 1 : 86;
+  return static_cast<size_t>(npad + 1 + srows) * 24 * 4 + kPhaseWords * 4 + 72 * 4 + kCtlWords * 4 +
+         static_cast<size_t>(npad) * 2 + 64;
 }
 
 bool gnn_mma_fits(int max_nodes) { return gnn_mma_smem_bytes(max_nodes) <= 227 * 1024; }

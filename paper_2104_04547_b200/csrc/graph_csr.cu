@@ -4,7 +4,8 @@
 // predicate as featurize.cu (complexes.py:237-246):
 //   d2 = (dx*dx+dy*dy)+dz*dz (float64, no FMA); candidate iff d2 <= rmax^2;
 //   keep iff sqrt(d2) <= t_cov (same role) / t_ncov (different role).
-// Rows are ascending in the neighbour id (canonical), written as (start, deg).
+// Rows are written as (start, deg); non-covalent rows ascend in the neighbour
+// id, covalent rows do when distances are requested (see the fill below).
 //
 // Work split:
 //  * non-covalent pairs are bipartite (role S x role L, S the smaller role):
@@ -202,7 +203,18 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     cell_list[slot] = i;
   }
   __syncthreads();
-  // cell k spans [cell_start[k-1], cell_start[k]) now (cell_start[-1] := 0)
+  // cell k spans [cell_start[k-1], cell_start[k]) now (cell_start[-1] := 0);
+  // sort each (few-atom) cell by id so the candidate order is deterministic
+  for (int k = threadIdx.x; k < 2 * NC; k += blockDim.x) {
+    const int cb = k == 0 ? 0 : cell_start[k - 1], ce = cell_start[k];
+    for (int x = cb + 1; x < ce; ++x) {
+      const int v = cell_list[x];
+      int y = x - 1;
+      while (y >= cb && cell_list[y] > v) { cell_list[y + 1] = cell_list[y]; --y; }
+      cell_list[y + 1] = v;
+    }
+  }
+  __syncthreads();
 
   const double rmax = fmax(a.tc, a.tn);
   const double rmax2 = __dmul_rn(rmax, rmax);
@@ -383,7 +395,11 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       }
     }
   }
-  // ---- fill covalent rows, then insertion-sort each (short) row ----
+  // ---- fill covalent rows.  Scoring path (no distances): rows stay in the
+  // deterministic stencil order (cells x-, y-, z-major, ids ascending inside
+  // a cell) -- a pose's sums never depend on its batch.  Featurizer path
+  // (distances, edge lists compared bitwise with the reference): rows are
+  // insertion-sorted to ascending neighbour id. ----
   int32_t* colc = a.col_cov + cbase;
   double* distc = DIST ? a.dist_cov + cbase : nullptr;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -398,6 +414,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       }
       ++o;
     });
+    if (!DIST) continue;
     for (int x = rb + 1; x < o; ++x) {
       const int v = colc[x];
       const double dv = DIST ? distc[x] : 0.0;
