@@ -1,0 +1,72 @@
+"""Instruction / stall totals of an ncu report grouped by source-line regions
+of one file (SASS in address order; inlined helpers are charged to the
+region of the nearest preceding line of that file).
+
+    python tools/ncu_regions.py report.ncu-rep file.cu name:lo-hi [name:lo-hi ...]
+"""
+import csv
+import io
+import subprocess
+import sys
+
+
+MIN_LINE = 0
+
+
+def main(path, fname, specs):
+    regions = []
+    for sp in specs:
+        name, rng = sp.split(":")
+        lo, hi = map(int, rng.split("-"))
+        regions.append((name, lo, hi))
+    raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    cur_file, hdr, line = None, None, None
+    sass = []
+    for r in rows:
+        if r and r[0] == "File Path":
+            cur_file = r[1].split("/")[-1]
+            continue
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or not r:
+            continue
+        if r[0]:
+            if r[0].isdigit():
+                line = int(r[0])
+            continue
+        ie = hdr.index("Instructions Executed")
+        st = hdr.index("Warp Stall Sampling (All Samples)")
+        try:
+            addr = int(r[2], 16)
+        except ValueError:
+            continue
+        sass.append((addr, cur_file, line, float(r[ie] or 0), float(r[st] or 0)))
+    sass.sort()
+    tot_i = sum(s[3] for s in sass) or 1
+    tot_s = sum(s[4] for s in sass) or 1
+    acc = {name: [0.0, 0.0] for name, _, _ in regions}
+    acc["other"] = [0.0, 0.0]
+    last = None
+    for addr, f, ln, i, s in sass:
+        if f == fname and ln >= MIN_LINE:
+            last = ln
+        reg = "other"
+        if last is not None:
+            for name, lo, hi in regions:
+                if lo <= last <= hi:
+                    reg = name
+                    break
+        acc[reg][0] += i
+        acc[reg][1] += s
+    for k, (i, s) in acc.items():
+        print(f"{k:12s} instr {i / tot_i:6.1%}  stall {s / tot_s:6.1%}")
+
+
+if __name__ == "__main__":
+    args = sys.argv[1:]
+    if args[0].startswith("--min-line="):
+        MIN_LINE = int(args.pop(0).split("=")[1])
+    main(args[0], args[1], args[2:])
