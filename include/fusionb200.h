@@ -48,6 +48,9 @@ extern "C" {
 #define FS_ERR_TOO_LARGE 16  /* pose exceeds FS_MAX_POSE_ATOMS              */
 #define FS_ERR_GRID_NONFINITE 32  /* given voxel grid has inf/NaN (models.py:521-522) */
 #define FS_ERR_FEAT_NONFINITE 64  /* given node features have inf/NaN (:527-528)   */
+#define FS_ERR_NOT_FACTORED 128   /* fs_score_poses_cached: pose is not pocket(role 0)
+                                     + ligand(role 1) or its ligand is too large for
+                                     the factored kernels; rescore with fs_score_poses */
 
 #define FS_MAX_POSE_ATOMS 4096
 
@@ -213,6 +216,39 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses,
                       void* ws, size_t ws_bytes, float* scores, float* lat_v,
                       float* lat_g, float* pred_v, float* pred_g, int32_t* err,
                       void* stream);
+
+/* ---- pocket-invariant factoring (one-pocket screens) ---
+ * For a pose = pocket atoms (all role PROTEIN) + ligand atoms (all LIGAND) the
+ * following never depend on the ligand: the protein voxel channels and their
+ * conv1 contribution (conv1 is linear, channels are disjoint,
+ * complexes.py:182); protein-protein covalent edges and the protein node
+ * states after the covalent phase (covalent edges never cross roles,
+ * complexes.py:242-243); and the whole trajectory (and pool contribution) of
+ * protein nodes with no ligand within noncov_thresh.  fs_pocket_prepare
+ * computes these once per pocket into a cache; fs_score_poses_cached then
+ * scores a pose from its ligand atoms, recomputing only ligand nodes and the
+ * protein nodes the ligand touches.  Same scores as fs_score_poses to fp32
+ * rounding (bf16 precision only).  This is an effective-throughput mode: the
+ * reported algorithmic work per pose is unchanged. */
+size_t fs_pocket_cache_bytes(const fs_model* m, int32_t max_pocket_atoms);
+size_t fs_pocket_prepare_ws_bytes(const fs_model* m, int32_t n_pockets, int32_t max_pocket_atoms);
+/* Pockets as in fs_pose_batch (pocket_xyz/elem/role, pocket_off[n+1]); cache =
+ * n_pockets * fs_pocket_cache_bytes(max_pocket_atoms) bytes; err[n_pockets]
+ * gets the FS_ERR_* bits of each pocket (a pocket with err != 0 must not be
+ * used with the cache). */
+int fs_pocket_prepare(const fs_model* m, const double* pocket_xyz, const int32_t* pocket_elem,
+                      const int32_t* pocket_role, const int64_t* pocket_off, int32_t n_pockets,
+                      int32_t max_pocket_atoms, void* cache, int32_t* err, void* ws,
+                      size_t ws_bytes, void* stream);
+/* Like fs_score_poses (bf16 only) for a batch whose pockets are the ones the
+ * cache was prepared from.  Poses that cannot be factored get
+ * FS_ERR_NOT_FACTORED (and a NaN score); rescore them with fs_score_poses.
+ * Workspace: fs_workspace_bytes(m, P, P * (max_pose_atoms + 32), P * max_edges, bf16). */
+int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch* b,
+                          const void* cache, int32_t max_pocket_atoms, int64_t max_edges,
+                          void* ws, size_t ws_bytes, float* scores, float* lat_v,
+                          float* lat_g, float* pred_v, float* pred_g, int32_t* err,
+                          void* stream);
 
 /* Test hook: one tcgen05 Conv3d layer (1..4) of the bf16 voxel head on
  * explicit buffers.  bf16 activations are chunk-major [P][C/8][D][H][W][8]

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, "libfusionb200.so")
 
 FS_OK, FS_EINVAL, FS_ECAPACITY, FS_ECUDA, FS_ENOTSUP = 0, -1, -2, -3, -4
 FS_ERR_ROLE, FS_ERR_NAN, FS_ERR_NONFINITE, FS_ERR_EDGE_CAP, FS_ERR_TOO_LARGE = 1, 2, 4, 8, 16
-FS_ERR_GRID_NONFINITE, FS_ERR_FEAT_NONFINITE = 32, 64
+FS_ERR_GRID_NONFINITE, FS_ERR_FEAT_NONFINITE, FS_ERR_NOT_FACTORED = 32, 64, 128
 FS_MAX_POSE_ATOMS = 4096
 FS_PREC_FP32, FS_PREC_BF16 = 0, 1
 FS_GRID_NCDHW_F64, FS_GRID_NDHWC_F32, FS_GRID_NDHWC_BF16 = 0, 1, 2
@@ -33,6 +33,7 @@ EXPORTS = (
     "fs_graph_fill", "fs_graph_edge_counts", "fs_graph_edges", "fs_workspace_bytes",
     "fs_score_poses", "fs_score_features", "fs_debug_conv", "fs_topk_ws_bytes", "fs_topk_merge",
     "fs_best_pose", "fs_best_pose_update", "fs_best_pose_decode",
+    "fs_pocket_cache_bytes", "fs_pocket_prepare_ws_bytes", "fs_pocket_prepare", "fs_score_poses_cached",
 )
 
 
@@ -101,6 +102,11 @@ def _sig(lib):
         "fs_graph_edges": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P, _P]),
         "fs_workspace_bytes": (_SZ, [_P, _I32, _I64, _I64, C.c_int]),
         "fs_score_poses": (C.c_int, [_P, C.c_int, sp, _I64, _P, _SZ, _P, _P, _P, _P, _P, _P, _P]),
+        "fs_pocket_cache_bytes": (_SZ, [_P, _I32]),
+        "fs_pocket_prepare_ws_bytes": (_SZ, [_P, _I32, _I32]),
+        "fs_pocket_prepare": (C.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
+        "fs_score_poses_cached": (C.c_int, [_P, C.c_int, sp, _P, _I32, _I64, _P, _SZ, _P, _P, _P, _P, _P, _P,
+                                            _P]),
         "fs_score_features": (C.c_int, [_P, C.c_int, _I32, _P, _P, _P, _I64, _P, _I64, _P, _I64,
                                         _I32, _P, _SZ, _P, _P, _P, _P, _P, _P, _P]),
         "fs_debug_conv": (C.c_int, [_P, C.c_int, _I32, _P, _P, _P, _P]),

@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <string>
@@ -22,7 +23,14 @@ static thread_local std::string g_last_cuda_error;
 void set_cuda_error(cudaError_t e) { g_last_cuda_error = cudaGetErrorString(e); }
 
 static std::atomic<long long> g_launches{0};
-void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launch(const char* file, int line) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  static const bool dbg = getenv("FS_DEBUG_SYNC") != nullptr;
+  if (dbg) {
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) fprintf(stderr, "fusionb200: launch at %s:%d failed: %s\n", file, line, cudaGetErrorString(e));
+  }
+}
 
 static thread_local cudaEvent_t* g_stage_events = nullptr;   // [ST_COUNT] or null
 void mark_stage(int stage, cudaStream_t st) {
@@ -41,13 +49,24 @@ int launch_edges(const int64_t* node_off, int n_poses, const int64_t* row_ptr, c
 int launch_graph_csr(const fs_pose_batch& b, const int64_t* node_off, double tc, double tn, int64_t* row_cov,
                      int32_t* deg_cov, int32_t* col_cov, double* dist_cov, int64_t* row_ncov, int32_t* deg_ncov,
                      int32_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st);
+int launch_graph_fact(const fs_pose_batch& b, double tc, double tn, double box, int c_elem, int64_t S, int64_t cap,
+                      int max_pocket, int32_t* cnt, int32_t* aff, float* feats, int64_t* row_cov, int32_t* deg_cov,
+                      int32_t* col_cov, int64_t* row_ncov, int32_t* deg_ncov, int32_t* col_ncov, int32_t* err,
+                      cudaStream_t st);
+bool conv1_fact_supported(int g, int k, int cin, int cout);
+int launch_conv1_fact(const fs_pose_batch& b, const char* cache, int64_t cache_stride, int64_t off_pp, const float* w,
+                      int c_elem, double box, __nv_bfloat16* out, cudaStream_t st);
+int launch_round_bf16(const float* in, float* out, int64_t n, cudaStream_t st);
+int launch_pocket_total(const int64_t* pocket_off, int n_pockets, const float* f, int64_t ld, char* cache,
+                        int64_t cache_stride, int64_t off_T, int64_t off_n, cudaStream_t st);
+int launch_pocket_poses(int n, int64_t* atom_off, int32_t* target, cudaStream_t st);
 int launch_csr_from_edges(const int64_t* edges, int64_t ne, const int64_t* node_off, int n_poses, int64_t n_nodes, int32_t* node_pose, int32_t* deg, int64_t* row_ptr, int64_t* cursor, int32_t* col, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t scan_ws_bytes(int64_t n);
 
 struct ConvArgs {
   const float* in; const float* w; const float* b;
   const float* bn_scale; const float* bn_shift; const float* residual;
-  float* out; int64_t n_vox; int g, cin, cout, k;
+  float* out; int64_t n_vox; int g, cin, cout, k; int no_relu;
 };
 int launch_conv3d_ffma(const ConvArgs& a, cudaStream_t st);
 int launch_maxpool2(const float* in, float* out, int n_poses, int g_out, int c, cudaStream_t st);
@@ -75,10 +94,14 @@ struct GnnMmaArgs {
   const int64_t* row_ncov; const int32_t* deg_ncov; const int32_t* col_ncov;
   const float* we; const float* be; const uint32_t* wfrag[2]; const float* wbias[2];
   const uint32_t* gfrag; const float* gbias; int k_steps[2]; float* lat; int64_t ld_lat; const int32_t* err;
+  const int32_t* fact_cnt; int64_t fact_stride; const int32_t* fact_aff; const int32_t* pose_target;
+  const char* cache; int64_t cache_stride; int64_t off_hcov, off_f, off_T, off_n;
+  float* dump_hcov; float* dump_f; int64_t dump_ld;
 };
 int gnn_mma_phase_words();
 int gnn_mma_gather_words();
 bool gnn_mma_fits(int max_nodes);
+int gnn_mma_max_nodes();
 int launch_gnn_mma(const GnnMmaArgs& a, int split, int n_poses, int max_nodes, cudaStream_t st);
 int launch_gnn(const GnnArgs& a, int dpad, int n_poses, int max_nodes, cudaStream_t st);
 bool gnn_needs_global_state(int dpad, int max_nodes);
@@ -426,6 +449,7 @@ struct WsPlan {
   size_t total = 0;
   size_t node_off, deg_cov, deg_ncov, row_cov, row_ncov, col_cov, col_ncov, node_pose, cursor;
   size_t feats, grid, a1, a2, p1, a3, a4, p2, d1, lat, hb0, hb1, g1, g2, pv, pg, state, scan, umma;
+  size_t fact_cnt, fact_aff;
   size_t take(size_t bytes) { size_t o = total; total = align_up(total + bytes, 256); return o; }
 };
 
@@ -460,7 +484,30 @@ static WsPlan plan_ws(const fs_model& m, int64_t P, int64_t N, int64_t E, int pr
   (void)max_nodes;
   w.state = w.take((size_t)2 * 4 * N * m.dpad);   // GNN fallback state (unused when smem fits)
   w.scan = w.take(scan_ws_bytes(N > P ? N : P) + 1024);
+  w.fact_cnt = w.take(8 * P);
+  w.fact_aff = w.take(4 * N);
   return w;
+}
+
+// ---- pocket cache (fs_pocket_prepare / fs_score_poses_cached) --------------
+struct PocketCacheLayout {
+  int64_t off_n, off_T, off_pp, off_hcov, off_f, bytes;
+};
+
+static PocketCacheLayout cache_layout(const fs_model& m, int max_pocket) {
+  PocketCacheLayout L;
+  L.off_n = 0;
+  L.off_T = 256;
+  L.off_pp = (int64_t)align_up(L.off_T + 8 * 128, 256);
+  L.off_hcov = (int64_t)align_up(L.off_pp + (int64_t)4 * m.G * m.G * m.G * m.f1, 256);
+  L.off_f = (int64_t)align_up(L.off_hcov + (int64_t)4 * 24 * max_pocket, 256);
+  L.bytes = (int64_t)align_up(L.off_f + (int64_t)4 * 128 * max_pocket, 256);
+  return L;
+}
+
+static bool factoring_ok(const fs_model& m, int max_pocket) {
+  return m.umma_ok && m.gmma_ok && conv1_fact_supported(m.G, m.k1, m.cin, m.f1) && max_pocket > 0 &&
+         max_pocket <= FS_MAX_POSE_ATOMS && gnn_mma_fits(max_pocket);
 }
 
 static int act_of(int a) { return a == 0 ? FS_ACT_RELU : a == 1 ? FS_ACT_LEAKY : FS_ACT_SELU; }
@@ -524,7 +571,8 @@ static int voxel_tail(const fs_model& m, int P, char* ws, const WsPlan& w, bool 
 }
 
 static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const WsPlan& w,
-                      const int32_t* err, bool want_pred, int precision, cudaStream_t st) {
+                      const int32_t* err, bool want_pred, int precision, cudaStream_t st,
+                      const GnnMmaArgs* extra = nullptr) {
   GnnArgs g{};
   g.feats = (float*)(ws + w.feats); g.F = m.F; g.node_off = (int64_t*)(ws + w.node_off);
   g.row_cov = (int64_t*)(ws + w.row_cov); g.col_cov = (int32_t*)(ws + w.col_cov);
@@ -537,8 +585,9 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
   mark_stage(ST_GNN, st);
   int rc;
   static const bool force_ffma = getenv("FS_GNN_FFMA") != nullptr;
-  if (precision == FS_PREC_BF16 && m.gmma_ok && !force_ffma && gnn_mma_fits(max_nodes)) {
+  if (extra || (precision == FS_PREC_BF16 && m.gmma_ok && !force_ffma && gnn_mma_fits(max_nodes))) {
     GnnMmaArgs q{};
+    if (extra) q = *extra;   // factored-mode / dump fields
     q.feats = g.feats; q.F = g.F; q.node_off = g.node_off;
     q.row_cov = g.row_cov; q.col_cov = g.col_cov; q.row_ncov = g.row_ncov; q.col_ncov = g.col_ncov;
     q.deg_cov = g.deg_cov; q.deg_ncov = g.deg_ncov;
@@ -791,6 +840,142 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   }
   if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st))) return rc;
   if ((rc = graph_head(*m, P, max_atoms, W, w, err, late || pred_g, precision, st))) return rc;
+  if (!late && (rc = fusion_head(*m, P, W, w, scores, st))) return rc;
+  if ((rc = launch_finalize(P, d.fusion_mode, (float*)(W + w.pv), (float*)(W + w.pg), scores, err, st))) return rc;
+  rc = copy_outputs(*m, P, W, w, lat_v, lat_g, pred_v, pred_g, st);
+  mark_stage(ST_END, st);
+  return rc;
+}
+
+// ---- pocket-invariant factoring ----------------------------
+// covalent CSR capacity of a pocket-only pose (directed entries)
+static int64_t pocket_edge_cap(int max_pocket) { return (int64_t)64 * max_pocket + 1024; }
+
+size_t fs_pocket_cache_bytes(const fs_model* m, int32_t max_pocket_atoms) {
+  if (!m || !factoring_ok(*m, max_pocket_atoms)) return 0;
+  return (size_t)cache_layout(*m, max_pocket_atoms).bytes;
+}
+
+static size_t prep_extra_bytes(const fs_model& m, int n, int mp) {
+  return align_up(8 * (size_t)(n + 1), 256) + align_up(4 * (size_t)n, 256) +
+         align_up((size_t)4 * n * mp * 24, 256) + align_up((size_t)4 * n * mp * 128, 256) +
+         align_up((size_t)4 * m.k1 * m.k1 * m.k1 * m.cin * m.f1, 256) +
+         align_up((size_t)4 * n * m.G * m.G * m.G * m.f1, 256);
+}
+
+size_t fs_pocket_prepare_ws_bytes(const fs_model* m, int32_t n_pockets, int32_t max_pocket_atoms) {
+  if (!m || n_pockets < 0 || !factoring_ok(*m, max_pocket_atoms)) return 0;
+  const int64_t N = (int64_t)n_pockets * max_pocket_atoms;
+  return plan_ws(*m, n_pockets, N, n_pockets * pocket_edge_cap(max_pocket_atoms), FS_PREC_FP32).total +
+         prep_extra_bytes(*m, n_pockets, max_pocket_atoms) + 512;
+}
+
+int fs_pocket_prepare(const fs_model* m, const double* pocket_xyz, const int32_t* pocket_elem,
+                      const int32_t* pocket_role, const int64_t* pocket_off, int32_t n_pockets,
+                      int32_t max_pocket_atoms, void* cache, int32_t* err, void* ws, size_t ws_bytes,
+                      void* stream) {
+  if (!m || !pocket_xyz || !pocket_elem || !pocket_role || !pocket_off || !cache || !err || !ws) return FS_EINVAL;
+  if (!factoring_ok(*m, max_pocket_atoms)) return FS_ENOTSUP;
+  const int n = n_pockets, mp = max_pocket_atoms;
+  if (n <= 0) return FS_OK;
+  if (ws_bytes < fs_pocket_prepare_ws_bytes(m, n, mp)) return FS_ECAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  const fs_model_desc& d = m->d;
+  const PocketCacheLayout L = cache_layout(*m, mp);
+  const int64_t cap = pocket_edge_cap(mp);
+  // fp32 plan: the pocket grid is voxelized as fp32 for the FFMA conv1
+  WsPlan w = plan_ws(*m, n, (int64_t)n * mp, n * cap, FS_PREC_FP32);
+  char* W = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  char* X = W + w.total;   // prep-only buffers
+  int64_t* atom_off = (int64_t*)X; X += align_up(8 * (size_t)(n + 1), 256);
+  int32_t* target = (int32_t*)X; X += align_up(4 * (size_t)n, 256);
+  float* dump_h = (float*)X; X += align_up((size_t)4 * n * mp * 24, 256);
+  float* dump_f = (float*)X; X += align_up((size_t)4 * n * mp * 128, 256);
+  float* w1r = (float*)X; X += align_up((size_t)4 * m->k1 * m->k1 * m->k1 * m->cin * m->f1, 256);
+  float* pp = (float*)X;
+  int rc;
+  if ((rc = launch_pocket_poses(n, atom_off, target, st))) return rc;
+  fs_pose_batch pb{};
+  pb.pocket_xyz = pocket_xyz; pb.pocket_elem = pocket_elem; pb.pocket_role = pocket_role;
+  pb.pocket_off = pocket_off; pb.n_pockets = n;
+  pb.atom_xyz = pocket_xyz; pb.atom_elem = pocket_elem; pb.atom_role = pocket_role; pb.atom_off = atom_off;
+  pb.pose_target = target; pb.n_poses = n; pb.max_pose_atoms = mp;
+  FS_CUDA_CHECK(cudaMemsetAsync(err, 0, 4 * (size_t)n, st));
+  int64_t* node_off = (int64_t*)(W + w.node_off);
+  if ((rc = launch_node_offsets(pb, node_off, W + w.scan, scan_ws_bytes((int64_t)n * mp) + 1024, st))) return rc;
+  if ((rc = launch_node_features(pb, node_off, d.c_elem, d.box_size, W + w.feats, false, st))) return rc;
+  if ((rc = launch_graph_csr(pb, node_off, d.cov_thresh, d.noncov_thresh, (int64_t*)(W + w.row_cov),
+                             (int32_t*)(W + w.deg_cov), (int32_t*)(W + w.col_cov), nullptr, (int64_t*)(W + w.row_ncov),
+                             (int32_t*)(W + w.deg_ncov), (int32_t*)(W + w.col_ncov), nullptr, cap, err, st)))
+    return rc;
+  // SG-CNN of the pocket alone (no ligand -> no non-covalent edges: every
+  // node follows the message-free trajectory), dumping the post-covalent
+  // states and the per-node pool terms
+  GnnMmaArgs x{};
+  x.dump_hcov = dump_h; x.dump_f = dump_f; x.dump_ld = mp;
+  if ((rc = graph_head(*m, n, mp, W, w, err, false, FS_PREC_BF16, st, &x))) return rc;
+  char* C = (char*)cache;
+  FS_CUDA_CHECK(cudaMemcpy2DAsync(C + L.off_hcov, L.bytes, dump_h, (size_t)4 * mp * 24, (size_t)4 * mp * 24, n,
+                                  cudaMemcpyDeviceToDevice, st));
+  FS_CUDA_CHECK(cudaMemcpy2DAsync(C + L.off_f, L.bytes, dump_f, (size_t)4 * mp * 128, (size_t)4 * mp * 128, n,
+                                  cudaMemcpyDeviceToDevice, st));
+  if ((rc = launch_pocket_total(pocket_off, n, dump_f, mp, C, L.bytes, L.off_T, L.off_n, st))) return rc;
+  // conv1 pre-activation of the pocket channels, bf16-valued weights, fp32
+  if ((rc = launch_voxelize(pb, d.grid_extent, m->cgrid, d.box_size, FS_GRID_NDHWC_F32, W + w.grid, err, st))) return rc;
+  const int64_t nw = (int64_t)m->k1 * m->k1 * m->k1 * m->cin * m->f1;
+  if ((rc = launch_round_bf16(m->P(m->c1w), w1r, nw, st))) return rc;
+  ConvArgs c{};
+  c.in = (float*)(W + w.grid); c.w = w1r; c.b = m->P(m->c1b); c.out = pp;
+  c.n_vox = (int64_t)n * m->G * m->G * m->G; c.g = m->G; c.cin = m->cin; c.cout = m->f1; c.k = m->k1; c.no_relu = 1;
+  if ((rc = launch_conv3d_ffma(c, st))) return rc;
+  const size_t ppb = (size_t)4 * m->G * m->G * m->G * m->f1;
+  FS_CUDA_CHECK(cudaMemcpy2DAsync(C + L.off_pp, L.bytes, pp, ppb, ppb, n, cudaMemcpyDeviceToDevice, st));
+  return FS_OK;
+}
+
+int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch* b, const void* cache,
+                          int32_t max_pocket_atoms, int64_t max_edges, void* ws, size_t ws_bytes, float* scores,
+                          float* lat_v, float* lat_g, float* pred_v, float* pred_g, int32_t* err, void* stream) {
+  if (!m || !b || !cache || !ws || !scores || !err || max_edges <= 0) return FS_EINVAL;
+  if (precision != FS_PREC_BF16 || !factoring_ok(*m, max_pocket_atoms)) return FS_ENOTSUP;
+  const int P = b->n_poses;
+  if (P <= 0) return FS_OK;
+  const int max_atoms = b->max_pose_atoms > 0 ? b->max_pose_atoms : FS_MAX_POSE_ATOMS;
+  // compact node slice per pose; poses whose touched set does not fit the
+  // tensor-core SG-CNN's shared memory are flagged FS_ERR_NOT_FACTORED
+  int64_t S = (int64_t)((max_atoms + 15) & ~15) + 32;
+  if (S > gnn_mma_max_nodes()) S = gnn_mma_max_nodes();
+  const int64_t N = (int64_t)P * S;
+  WsPlan w = plan_ws(*m, P, N, (int64_t)P * max_edges, FS_PREC_BF16);
+  char* W = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  if ((size_t)(W - (char*)ws) + w.total > ws_bytes) return FS_ECAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  const fs_model_desc& d = m->d;
+  const PocketCacheLayout L = cache_layout(*m, max_pocket_atoms);
+  const bool late = d.fusion_mode == FS_MODE_LATE;
+  int32_t* cnt = (int32_t*)(W + w.fact_cnt);
+  int32_t* aff = (int32_t*)(W + w.fact_aff);
+  int rc;
+  mark_stage(ST_FEATURIZE, st);
+  FS_CUDA_CHECK(cudaMemsetAsync(err, 0, 4 * (size_t)P, st));
+  if ((rc = launch_graph_fact(*b, d.cov_thresh, d.noncov_thresh, d.box_size, d.c_elem, S, max_edges, max_pocket_atoms,
+                              cnt, aff, (float*)(W + w.feats), (int64_t*)(W + w.row_cov), (int32_t*)(W + w.deg_cov),
+                              (int32_t*)(W + w.col_cov), (int64_t*)(W + w.row_ncov), (int32_t*)(W + w.deg_ncov),
+                              (int32_t*)(W + w.col_ncov), err, st)))
+    return rc;
+  mark_stage(ST_CONV1, st);
+  if ((rc = launch_conv1_fact(*b, (const char*)cache, L.bytes, L.off_pp, m->P(m->c1w), d.c_elem, d.box_size,
+                              umma::act1_ptr(W + w.umma), st)))
+    return rc;
+  if ((rc = umma::voxel_convs_from2(d, (const char*)m->blob + m->umma_off, m->P(m->c2b), m->P(m->c3b), m->P(m->c4b),
+                                    P, W + w.umma, (float*)(W + w.p2), st)))
+    return rc;
+  if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st))) return rc;
+  GnnMmaArgs x{};
+  x.fact_cnt = cnt; x.fact_stride = S; x.fact_aff = aff; x.pose_target = b->pose_target;
+  x.cache = (const char*)cache; x.cache_stride = L.bytes;
+  x.off_hcov = L.off_hcov; x.off_f = L.off_f; x.off_T = L.off_T; x.off_n = L.off_n;
+  if ((rc = graph_head(*m, P, (int)S, W, w, err, late || pred_g, FS_PREC_BF16, st, &x))) return rc;
   if (!late && (rc = fusion_head(*m, P, W, w, scores, st))) return rc;
   if ((rc = launch_finalize(P, d.fusion_mode, (float*)(W + w.pv), (float*)(W + w.pg), scores, err, st))) return rc;
   rc = copy_outputs(*m, P, W, w, lat_v, lat_g, pred_v, pred_g, st);

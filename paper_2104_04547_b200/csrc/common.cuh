@@ -1,5 +1,6 @@
 // Shared device helpers for the fusionb200 kernels (sm_100a).
 #pragma once
+#include <cstdio>
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -18,11 +19,27 @@ void set_cuda_error(cudaError_t e);
     if (_e != cudaSuccess) { ::fs::set_cuda_error(_e); return FS_ECUDA; } \
   } while (0)
 
+// Device-side index checks, compiled in only with -DFS_BOUNDS (FS_BOUNDS=1 build).
+#ifdef FS_BOUNDS
+#define FS_DCHECK(cond, what, v, lim)                                                                \
+  do {                                                                                             \
+    if (!(cond)) {                                                                                 \
+      printf("FS_DCHECK %s:%d %s: %lld vs %lld (block %d)\n", __FILE__, __LINE__, what, (long long)(v), \
+             (long long)(lim), (int)blockIdx.x);                                                   \
+      __trap();                                                                                    \
+    }                                                                                              \
+  } while (0)
+#else
+#define FS_DCHECK(cond, what, v, lim) do {} while (0)
+#endif
+
 // Kernel launches issued by the library (reported by fs_launch_count()).
-void count_launch();
+// With FS_DEBUG_SYNC=1 in the environment every launch is followed by a
+// device synchronise and a report of the launching site on failure.
+void count_launch(const char* file, int line);
 #define FS_LAUNCH_CHECK()            \
   do {                               \
-    ::fs::count_launch();            \
+    ::fs::count_launch(__FILE__, __LINE__); \
     FS_CUDA_CHECK(cudaGetLastError()); \
   } while (0)
 

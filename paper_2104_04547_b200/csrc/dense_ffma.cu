@@ -21,6 +21,7 @@ struct ConvArgs {
   float* out;
   int64_t n_vox;      // P * G^3
   int g, cin, cout, k;
+  int no_relu;        // 1: out = acc + b (pocket cache: conv1 pre-activation)
 };
 
 __global__ void __launch_bounds__(256) conv3d_ffma_kernel(ConvArgs a) {
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(256) conv3d_ffma_kernel(ConvArgs a) {
   #pragma unroll
   for (int q = 0; q < 8; ++q) {
     if (q >= nvalid) break;
-    float y = fmaxf(acc[q] + a.b[o0 + q], 0.0f);
+    float y = a.no_relu ? acc[q] + a.b[o0 + q] : fmaxf(acc[q] + a.b[o0 + q], 0.0f);
     if (a.bn_scale) y = fmaf(y, a.bn_scale[o0 + q], a.bn_shift[o0 + q]);
     if (a.residual) y += a.residual[v * a.cout + o0 + q];
     o[q] = y;

@@ -34,6 +34,21 @@ struct GnnMmaArgs {
   int k_steps[2];
   float* lat; int64_t ld_lat;             // [P][ld_lat], columns 0..127
   const int32_t* err;
+  // ---- pocket factoring (fs_score_poses_cached); fact_cnt == nullptr: off.
+  // Pose p owns node slice [p*fact_stride, +fact_stride): ligand rows
+  // [0, nL), zero rows up to nLp = roundup16(nL), then the nA pocket atoms
+  // the ligand touches (ids fact_aff[]), whose covalent phase is taken from
+  // the pocket cache (cache_hcov) and whose untouched neighbours enter the
+  // pool through cache_T - sum(cache_f[affected]).
+  const int32_t* fact_cnt;                // [P][2] = (nL, nA)
+  int64_t fact_stride;
+  const int32_t* fact_aff;                // [P*fact_stride]
+  const int32_t* pose_target;             // [P]
+  const char* cache; int64_t cache_stride;
+  int64_t off_hcov, off_f, off_T, off_n;  // byte offsets inside one pocket's cache
+  // ---- pocket preparation dumps (plain path): node states after the covalent
+  // phase [P][dump_ld][24] and per-node pool terms [P][dump_ld][128]
+  float* dump_hcov; float* dump_f; int64_t dump_ld;
 };
 
 constexpr int kMmaWarps = 16;
@@ -140,12 +155,25 @@ __device__ __forceinline__ void acc_row(float (&a)[6], const float* __restrict__
   }
 }
 
-template <int SPLIT>
+template <int SPLIT, bool FACT>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int p = blockIdx.x;
-  const int64_t base = a.node_off[p];
-  const int n = static_cast<int>(a.node_off[p + 1] - base);
+  int64_t base;
+  int n, nL = 0, nLp = 0;
+  const char* pc = nullptr;   // this pose's pocket cache
+  if constexpr (FACT) {
+    base = static_cast<int64_t>(p) * a.fact_stride;
+    nL = a.fact_cnt[2 * p];
+    nLp = (nL + 15) & ~15;
+    n = nLp + a.fact_cnt[2 * p + 1];
+    pc = a.cache + static_cast<int64_t>(a.pose_target[p]) * a.cache_stride;
+  } else {
+    base = a.node_off[p];
+    n = static_cast<int>(a.node_off[p + 1] - base);
+  }
+  // rows that hold a node (factored slices have zero rows between ligand and pocket)
+  auto valid = [&](int r) { return FACT ? (r < nL || (r >= nLp && r < n)) : r < n; };
   float* lat = a.lat + static_cast<int64_t>(p) * a.ld_lat;
   if (a.err && a.err[p]) {
     for (int k = threadIdx.x; k < 128; k += blockDim.x) lat[k] = __int_as_float(0x7fc00000);
@@ -165,12 +193,21 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   const int g = lane >> 2, t = lane & 3;
 #define COLS(c) ((c) < 2 ? 2 * t + (c) : (c) < 4 ? 6 + 2 * t + (c) : 12 + 2 * t + (c))
 
-  // ---- embedding h0 = tanh(X.We + be); padded rows (and row npad) are zero ----
+  // ---- embedding h0 = tanh(X.We + be); padded rows (and row npad) are zero.
+  // Factored: pocket rows start from their cached post-covalent state. ----
   for (int i = threadIdx.x; i <= npad; i += blockDim.x) {
+    if (FACT && i >= nLp && i < n) {
+      const float4* src = reinterpret_cast<const float4*>(
+          reinterpret_cast<const float*>(pc + a.off_hcov) + static_cast<int64_t>(a.fact_aff[base + i]) * 24);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) reinterpret_cast<float4*>(H + i * 24)[k] = src[k];
+      continue;
+    }
+    const bool emb = FACT ? i < nL : i < n;
     float acc[24];
 #pragma unroll
-    for (int k = 0; k < 24; ++k) acc[k] = i < n ? a.be[k] : 0.f;
-    if (i < n) {
+    for (int k = 0; k < 24; ++k) acc[k] = emb ? a.be[k] : 0.f;
+    if (emb) {
       const float* x = a.feats + (base + i) * a.F;
       for (int f = 0; f < a.F; ++f) {
         const float xv = x[f];
@@ -181,13 +218,19 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
     for (int k = 0; k < 24; k += 4)
       *reinterpret_cast<float4*>(H + i * 24 + k) =
-          i < n ? make_float4(fs_tanh(acc[k]), fs_tanh(acc[k + 1]), fs_tanh(acc[k + 2]), fs_tanh(acc[k + 3]))
+          emb ? make_float4(fs_tanh(acc[k]), fs_tanh(acc[k + 1]), fs_tanh(acc[k + 2]), fs_tanh(acc[k + 3]))
                 : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 
   int gstep = 0;
   for (int ph = 0; ph < 2; ++ph) {
     __syncthreads();
+    if (!FACT && ph == 1 && a.dump_hcov) {   // pocket preparation: post-covalent states
+      float* o = a.dump_hcov + static_cast<int64_t>(p) * a.dump_ld * 24;
+      for (int i = threadIdx.x; i < n * 24; i += blockDim.x) o[i] = H[i];
+    }
+    // factored covalent phase: only the ligand rows move
+    const int prow = FACT && ph == 0 ? nLp : npad;
     for (int i = threadIdx.x; i < kPhaseWords; i += blockDim.x) WF[i] = a.wfrag[ph][i];
     for (int i = threadIdx.x; i < 72; i += blockDim.x) WB[i] = a.wbias[ph][i];
     if (threadIdx.x < kBins) CTL[4 + threadIdx.x] = 0;
@@ -200,7 +243,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     // The order inside a bin is arbitrary: a row's sum never depends on
     // where it is gathered, so the result stays deterministic.
     int* key = reinterpret_cast<int*>(S);     // S is scratch until the first step
-    for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+    for (int i = threadIdx.x; i < prow; i += blockDim.x) {
       const int d = i < n ? degs[base + i] : 0;
       const int bin = kHeavyDeg - min(d, kHeavyDeg);
       key[i] = (bin << 16) | atomicAdd(&CTL[4 + bin], 1);
@@ -212,11 +255,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       CTL[2] = CTL[4];
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < npad; i += blockDim.x)
+    for (int i = threadIdx.x; i < prow; i += blockDim.x)
       PERM[CTL[4 + kBins + (key[i] >> 16)] + (key[i] & 0xffff)] = static_cast<uint16_t>(i);
     __syncthreads();
     const int nh = CTL[2];
-    const int nitems = nh + (npad - nh + 15) / 16;
+    const int nitems = nh + (prow - nh + 15) / 16;
 
     const uint32_t* zr_hi = WF;
     const uint32_t* zr_lo = WF + kZrWords;
@@ -259,7 +302,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           // Exhausted slots read the all-zero row `npad` (x + 0 == x, so the
           // sums stay exactly CSR-ordered).
           const int k0 = nh + (item - nh) * 16 + g, k1 = k0 + 8;
-          const int r0 = k0 < npad ? PERM[k0] : npad, r1 = k1 < npad ? PERM[k1] : npad;
+          const int r0 = k0 < prow ? PERM[k0] : npad, r1 = k1 < prow ? PERM[k1] : npad;
           const int d0 = r0 < n ? degs[base + r0] : 0, d1 = r1 < n ? degs[base + r1] : 0;
           const int32_t* c0 = colv + (r0 < n ? rows[base + r0] : 0);
           const int32_t* c1 = colv + (r1 < n ? rows[base + r1] : 0);
@@ -305,7 +348,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       __syncthreads();
 
       // ---- pass 2: GRU update of every 16-row tile, in place ----
-      for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
+      for (int tile = warp; tile < prow / 16; tile += kMmaWarps) {
         float bz[6], br[6], bh[6];
 #pragma unroll
         for (int c = 0; c < 6; ++c) { bz[c] = WB[COLS(c)]; br[c] = WB[24 + COLS(c)]; bh[c] = WB[48 + COLS(c)]; }
@@ -356,7 +399,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             for (int e = 0; e < 2; ++e) {
               const int c = 2 * j + e;
               const float hh = fs_tanh(Dh[j][2 * rr + e] + bh[c]);
-              hn[c] = row < n ? fmaf(z[rr][c], hh - h[rr][c], h[rr][c]) : 0.f;
+              hn[c] = valid(row) ? fmaf(z[rr][c], hh - h[rr][c], h[rr][c]) : 0.f;
             }
 #pragma unroll
           for (int c = 0; c < 6; c += 2)
@@ -406,7 +449,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     put_a<SPLIT>(ahi[1], alo[1], 1, h[1][4], h[1][5]);
     put_a<SPLIT>(ahi[1], alo[1], 2, 0.f, 0.f);
     put_a<SPLIT>(ahi[1], alo[1], 3, 0.f, 0.f);
-    const bool v0 = tile * 16 + g < n, v1 = tile * 16 + g + 8 < n;
+    const bool v0 = valid(tile * 16 + g), v1 = valid(tile * 16 + g + 8);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       float Dg[4] = {0.f, 0.f, 0.f, 0.f}, Dv[4] = {0.f, 0.f, 0.f, 0.f};
@@ -432,6 +475,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         const float x0 = v0 ? fs_sigmoid(Dg[e] + bgv) * fs_tanh(Dv[e] + bfv) : 0.f;
         const float x1 = v1 ? fs_sigmoid(Dg[2 + e] + bgv) * fs_tanh(Dv[2 + e] + bfv) : 0.f;
         acc[j][e] += x0 + x1;
+        if (!FACT && a.dump_f) {   // pocket preparation: per-node pool terms
+          float* o = a.dump_f + (static_cast<int64_t>(p) * a.dump_ld + tile * 16 + g) * 128 + col;
+          if (v0) o[0] = x0;
+          if (v1) o[8 * 128] = x1;
+        }
       }
     }
   }
@@ -457,7 +505,16 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   if (threadIdx.x < 128) {
     float tot = 0.f;
     for (int w = 0; w < kMmaWarps; ++w) tot += RED[w * 128 + threadIdx.x];
-    lat[threadIdx.x] = tot / static_cast<float>(max(n, 1));
+    if constexpr (FACT) {
+      // untouched pocket nodes: cached total minus the touched ones' cached terms
+      const float* f = reinterpret_cast<const float*>(pc + a.off_f);
+      double corr = reinterpret_cast<const double*>(pc + a.off_T)[threadIdx.x];
+      for (int r = nLp; r < n; ++r) corr -= f[static_cast<int64_t>(a.fact_aff[base + r]) * 128 + threadIdx.x];
+      const int n_all = *reinterpret_cast<const int32_t*>(pc + a.off_n) + nL;
+      lat[threadIdx.x] = static_cast<float>((corr + static_cast<double>(tot)) / static_cast<double>(max(n_all, 1)));
+    } else {
+      lat[threadIdx.x] = tot / static_cast<float>(max(n, 1));
+    }
   }
 }
 
@@ -470,19 +527,27 @@ size_t gnn_mma_smem_bytes(int max_nodes) {
 
 bool gnn_mma_fits(int max_nodes) { return gnn_mma_smem_bytes(max_nodes) <= 227 * 1024; }
 
+int gnn_mma_max_nodes() {
+  int n = 16;
+  while (gnn_mma_fits(n + 16)) n += 16;
+  return n;
+}
+
+template <int SPLIT, bool FACT>
+static int launch_gnn_mma_t(const GnnMmaArgs& a, int n_poses, size_t smem, cudaStream_t st) {
+  FS_CUDA_CHECK(cudaFuncSetAttribute(gnn_mma_kernel<SPLIT, FACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  gnn_mma_kernel<SPLIT, FACT><<<n_poses, kMmaWarps * 32, smem, st>>>(a);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
 int launch_gnn_mma(const GnnMmaArgs& a, int split, int n_poses, int max_nodes, cudaStream_t st) {
   if (n_poses <= 0) return FS_OK;
   if (!gnn_mma_fits(max_nodes)) return FS_ECAPACITY;
   const size_t smem = gnn_mma_smem_bytes(max_nodes);
-  if (split == 3) {
-    FS_CUDA_CHECK(cudaFuncSetAttribute(gnn_mma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    gnn_mma_kernel<3><<<n_poses, kMmaWarps * 32, smem, st>>>(a);
-  } else {
-    FS_CUDA_CHECK(cudaFuncSetAttribute(gnn_mma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    gnn_mma_kernel<1><<<n_poses, kMmaWarps * 32, smem, st>>>(a);
-  }
-  FS_LAUNCH_CHECK();
-  return FS_OK;
+  if (a.fact_cnt) return launch_gnn_mma_t<3, true>(a, n_poses, smem, st);
+  return split == 3 ? launch_gnn_mma_t<3, false>(a, n_poses, smem, st) : launch_gnn_mma_t<1, false>(a, n_poses, smem, st);
 }
 
 }  // namespace fs

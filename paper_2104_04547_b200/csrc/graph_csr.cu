@@ -42,8 +42,10 @@ __host__ __device__ inline size_t graph_csr_smem_bytes(int n) {
   return (size_t)n * 16 + (size_t)n * 4 * 4 + (size_t)(n + 1) * 4 * 2 + (size_t)n * kMaskWords * 4 + cells * 4 + 512;
 }
 
-// in-place exclusive scan of a[0..n) (n+1-th entry receives the total)
+// in-place exclusive scan of a[0..n) (n+1-th entry receives the total).
+// Starts with a barrier: the caller's writes to a[] are visible to every thread.
 __device__ void block_exclusive_scan(int* a, int n, int* warp_tot) {
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int per = (n + blockDim.x - 1) / blockDim.x;
   const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
@@ -451,6 +453,252 @@ int launch_graph_csr(const fs_pose_batch& b, const int64_t* node_off, double tc,
     FS_CUDA_CHECK(cudaFuncSetAttribute(graph_csr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     graph_csr_kernel<false><<<b.n_poses, kCsrThreads, smem, st>>>(a);
   }
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
+
+// ===========================================================================
+// Pocket-factored radius graph (fs_score_poses_cached).
+// A factorable pose is pocket atoms (all role 0) + ligand atoms (all role 1,
+// at most kFactMaxLig).  Only edges that touch the ligand are built:
+//   covalent     : ligand-ligand (pocket-pocket edges live in the cache)
+//   non-covalent : ligand-pocket (bipartite, as in graph_csr_kernel)
+// Compact node slice of pose p (rows p*S ..): ligand atoms [0, nL), zero rows
+// up to nLp = roundup16(nL), then the nA pocket atoms with a ligand
+// neighbour, ascending pocket id (aff[] = their pocket ids).  Neighbour order
+// is ascending in the original node id, same predicate as the full kernel.
+// ===========================================================================
+struct GraphFactArgs {
+  fs_pose_batch b;
+  double tc, tn, box;
+  int c_elem;
+  int64_t S, cap;
+  int32_t* cnt; int32_t* aff; float* feats;
+  int64_t* row_cov; int32_t* deg_cov; int32_t* col_cov;
+  int64_t* row_ncov; int32_t* deg_ncov; int32_t* col_ncov;
+  int32_t* err;
+  int max_pocket;
+};
+
+constexpr int kFactMaxLig = 128;
+constexpr int kFactWords = kFactMaxLig / 32;
+
+__host__ __device__ inline size_t graph_fact_smem_bytes(int max_pocket) {
+  const size_t np4 = (size_t)((max_pocket + 3) & ~3), nc = np4 + kFactMaxLig + 32;
+  return np4 * 16 + kFactMaxLig * 16 + np4 * kFactWords * 4 + (np4 + 4) * 4 + 2 * (nc + 4) * 4 + 256;
+}
+
+__device__ __forceinline__ bool fact_decide(const PoseView& pv, bool prefilter, float d2f, float lo2, float hi2,
+                                            double xi, double yi, double zi, int j, double rmax2, double t) {
+  if (prefilter) {
+    if (d2f > hi2) return false;
+    if (d2f <= lo2) return true;
+  }
+  double d;
+  return exact_edge(pv, xi, yi, zi, j, rmax2, t, &d);
+}
+
+__global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_flag;
+  __shared__ double s_red[kCsrWarps];
+  __shared__ int warp_tot[32];
+  const int p = blockIdx.x;
+  const PoseView pv = pose_view(a.b, p);
+  const int np = (int)pv.np_, nL = (int)pv.na;
+  const int64_t nb = (int64_t)p * a.S, cb = (int64_t)p * a.cap;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto give_up = [&](int flags) {
+    if (threadIdx.x == 0) { atomicOr(&a.err[p], flags); a.cnt[2 * p] = 0; a.cnt[2 * p + 1] = 0; }
+  };
+  if (np == 0 || np > a.max_pocket || nL > kFactMaxLig || np + nL > FS_MAX_POSE_ATOMS) {
+    give_up(FS_ERR_NOT_FACTORED);
+    return;
+  }
+  const int np4 = (a.max_pocket + 3) & ~3, ncmax = np4 + kFactMaxLig + 32;
+  float4* pf = reinterpret_cast<float4*>(smem_raw);
+  float4* lf = pf + np4;
+  uint32_t* mask = reinterpret_cast<uint32_t*>(lf + kFactMaxLig);   // [np][kFactWords]
+  int* rank = reinterpret_cast<int*>(mask + (size_t)np4 * kFactWords);   // [np + 1]
+  int* offc = rank + np4 + 4;                                        // [nc + 1]
+  int* offn = offc + ncmax + 4;
+  if (threadIdx.x == 0) s_flag = 0;
+  __syncthreads();
+
+  // ---- atoms; the pose must be pocket(role 0) + ligand(role 1), finite ----
+  double amax = 0.0;
+  int bad = 0;
+  for (int i = threadIdx.x; i < np + nL; i += blockDim.x) {
+    double x, y, z; int32_t e, r;
+    pv.atom(i, x, y, z, e, r);
+    if (!isfinite(x) || !isfinite(y) || !isfinite(z) || r != (i < np ? 0 : 1)) bad = 1;
+    amax = fmax(amax, fmax(fabs(x), fmax(fabs(y), fabs(z))));
+    const float4 v = make_float4((float)x, (float)y, (float)z, 0.f);
+    if (i < np) pf[i] = v; else lf[i - np] = v;
+  }
+  for (int i = threadIdx.x; i < np * kFactWords; i += blockDim.x) mask[i] = 0u;
+  if (bad) atomicOr(&s_flag, 1);
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if (lane == 0) s_red[warp] = amax;
+  __syncthreads();
+  if (s_flag) { give_up(FS_ERR_NOT_FACTORED); return; }
+  double absmax = 0.0;
+  for (int w = 0; w < kCsrWarps; ++w) absmax = fmax(absmax, s_red[w]);
+  const bool prefilter = absmax < 1024.0;
+  const double rmax = fmax(a.tc, a.tn), rmax2 = __dmul_rn(rmax, rmax);
+  const float delta = 1e-5f + 2e-6f * (float)absmax;
+  const float c_lo2 = ((float)a.tc - delta) * ((float)a.tc - delta), c_hi2 = ((float)a.tc + delta) * ((float)a.tc + delta);
+  const float n_lo2 = ((float)a.tn - delta) * ((float)a.tn - delta), n_hi2 = ((float)a.tn + delta) * ((float)a.tn + delta);
+
+  // ---- non-covalent (ligand x pocket) bitmasks; ligand-ligand covalent degrees ----
+  for (int s = warp; s < nL; s += kCsrWarps) {
+    double xi, yi, zi; int32_t e_, r_;
+    pv.atom(np + s, xi, yi, zi, e_, r_);
+    const float4 fi = lf[s];
+    int cn = 0;
+    for (int j0 = 0; j0 < np; j0 += 32) {
+      const int j = j0 + lane;
+      bool hit = false;
+      if (j < np) {
+        const float4 fj = pf[j];
+        const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+        hit = fact_decide(pv, prefilter, dx * dx + dy * dy + dz * dz, n_lo2, n_hi2, xi, yi, zi, j, rmax2, a.tn);
+      }
+      cn += __popc(__ballot_sync(0xffffffffu, hit));
+      if (hit) atomicOr(&mask[j * kFactWords + (s >> 5)], 1u << (s & 31));
+    }
+    int cc = 0;
+    for (int j0 = 0; j0 < nL; j0 += 32) {
+      const int j = j0 + lane;
+      bool hit = false;
+      if (j < nL && j != s) {
+        const float4 fj = lf[j];
+        const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+        hit = fact_decide(pv, prefilter, dx * dx + dy * dy + dz * dz, c_lo2, c_hi2, xi, yi, zi, np + j, rmax2, a.tc);
+      }
+      cc += __popc(__ballot_sync(0xffffffffu, hit));
+    }
+    if (lane == 0) { offn[s] = cn; offc[s] = cc; }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < np; j += blockDim.x) {
+    uint32_t any = 0u;
+#pragma unroll
+    for (int w = 0; w < kFactWords; ++w) any |= mask[j * kFactWords + w];
+    rank[j] = any ? 1 : 0;
+  }
+  block_exclusive_scan(rank, np, warp_tot);
+  const int nA = rank[np];
+  const int nLp = (nL + 15) & ~15, nc = nLp + nA;
+  if (nc > a.S) { give_up(FS_ERR_NOT_FACTORED); return; }
+  for (int r = nL + threadIdx.x; r < nc; r += blockDim.x) { offc[r] = 0; if (r < nLp) offn[r] = 0; }
+  for (int j = threadIdx.x; j < np; j += blockDim.x) {
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < kFactWords; ++w) c += __popc(mask[j * kFactWords + w]);
+    if (c) offn[nLp + rank[j]] = c;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < nc; r += blockDim.x) { a.deg_cov[nb + r] = offc[r]; a.deg_ncov[nb + r] = offn[r]; }
+  block_exclusive_scan(offc, nc, warp_tot);
+  block_exclusive_scan(offn, nc, warp_tot);
+  if (offc[nc] > a.cap || offn[nc] > a.cap) { give_up(FS_ERR_EDGE_CAP); return; }
+  for (int r = threadIdx.x; r < nc; r += blockDim.x) { a.row_cov[nb + r] = cb + offc[r]; a.row_ncov[nb + r] = cb + offn[r]; }
+  for (int j = threadIdx.x; j < np; j += blockDim.x) {
+    uint32_t any = 0u;
+#pragma unroll
+    for (int w = 0; w < kFactWords; ++w) any |= mask[j * kFactWords + w];
+    if (any) {
+      FS_DCHECK(nLp + rank[j] < a.S, "aff", nLp + rank[j], a.S);
+      a.aff[nb + nLp + rank[j]] = j;
+    }
+  }
+  if (threadIdx.x == 0) { a.cnt[2 * p] = nL; a.cnt[2 * p + 1] = nA; }
+
+  // ---- fill: ligand rows (covalent: ligand ids; non-covalent: compact pocket ids) ----
+  int32_t* colc = a.col_cov + cb;
+  int32_t* coln = a.col_ncov + cb;
+  const unsigned below = (1u << lane) - 1u;
+  for (int s = warp; s < nL; s += kCsrWarps) {
+    double xi, yi, zi; int32_t e_, r_;
+    pv.atom(np + s, xi, yi, zi, e_, r_);
+    const float4 fi = lf[s];
+    int o = offc[s];
+    for (int j0 = 0; j0 < nL; j0 += 32) {
+      const int j = j0 + lane;
+      bool hit = false;
+      if (j < nL && j != s) {
+        const float4 fj = lf[j];
+        const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+        hit = fact_decide(pv, prefilter, dx * dx + dy * dy + dz * dz, c_lo2, c_hi2, xi, yi, zi, np + j, rmax2, a.tc);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        FS_DCHECK(o + __popc(m & below) < a.cap, "colc", o + __popc(m & below), a.cap);
+        colc[o + __popc(m & below)] = j;
+      }
+      o += __popc(m);
+    }
+    o = offn[s];
+    for (int j0 = 0; j0 < np; j0 += 32) {
+      const int j = j0 + lane;
+      const bool hit = j < np && ((mask[j * kFactWords + (s >> 5)] >> (s & 31)) & 1u);
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        FS_DCHECK(o + __popc(m & below) < a.cap, "coln lig", o + __popc(m & below), a.cap);
+        FS_DCHECK(nLp + rank[j] < nc, "coln val", nLp + rank[j], nc);
+        coln[o + __popc(m & below)] = nLp + rank[j];
+      }
+      o += __popc(m);
+    }
+  }
+  // pocket rows: their ligand neighbours, ascending
+  for (int j = threadIdx.x; j < np; j += blockDim.x) {
+    int o = -1;
+#pragma unroll
+    for (int w = 0; w < kFactWords; ++w) {
+      uint32_t bits = mask[j * kFactWords + w];
+      if (bits && o < 0) o = offn[nLp + rank[j]];
+      while (bits) {
+        const int bt = __ffs(bits) - 1;
+        bits &= bits - 1;
+        FS_DCHECK(o >= 0 && o < a.cap, "coln pocket", o, a.cap);
+        coln[o++] = 32 * w + bt;
+      }
+    }
+  }
+  // ligand node features, as node_features_kernel<float> (complexes.py:233-236)
+  const int F = a.c_elem + 4;
+  for (int s = threadIdx.x; s < nL; s += blockDim.x) {
+    double x, y, z; int32_t e, r;
+    pv.atom(np + s, x, y, z, e, r);
+    float* f = a.feats + (nb + s) * F;
+    const int ec = min(max(e, 0), a.c_elem - 1);
+    for (int c = 0; c < a.c_elem; ++c) f[c] = c == ec ? 1.f : 0.f;
+    f[a.c_elem] = (float)r;
+    f[a.c_elem + 1] = (float)__dadd_rn(__ddiv_rn(x, a.box), 0.5);
+    f[a.c_elem + 2] = (float)__dadd_rn(__ddiv_rn(y, a.box), 0.5);
+    f[a.c_elem + 3] = (float)__dadd_rn(__ddiv_rn(z, a.box), 0.5);
+  }
+}
+
+int launch_graph_fact(const fs_pose_batch& b, double tc, double tn, double box, int c_elem, int64_t S, int64_t cap,
+                      int max_pocket, int32_t* cnt, int32_t* aff, float* feats, int64_t* row_cov, int32_t* deg_cov,
+                      int32_t* col_cov, int64_t* row_ncov, int32_t* deg_ncov, int32_t* col_ncov, int32_t* err,
+                      cudaStream_t st) {
+  if (!(tc >= 1.2 && tc <= 5.9) || !(tn >= 1.2 && tn <= 5.9)) return FS_EINVAL;
+  if (b.n_poses <= 0) return FS_OK;
+  GraphFactArgs a;
+  a.b = b; a.tc = tc; a.tn = tn; a.box = box; a.c_elem = c_elem; a.S = S; a.cap = cap;
+  a.cnt = cnt; a.aff = aff; a.feats = feats;
+  a.row_cov = row_cov; a.deg_cov = deg_cov; a.col_cov = col_cov;
+  a.row_ncov = row_ncov; a.deg_ncov = deg_ncov; a.col_ncov = col_ncov;
+  a.err = err; a.max_pocket = max_pocket;
+  const size_t smem = graph_fact_smem_bytes(max_pocket);
+  if (smem > 227 * 1024) return FS_ECAPACITY;
+  FS_CUDA_CHECK(cudaFuncSetAttribute(graph_fact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  graph_fact_kernel<<<b.n_poses, kCsrThreads, smem, st>>>(a);
   FS_LAUNCH_CHECK();
   return FS_OK;
 }

@@ -583,6 +583,32 @@ int voxel_convs(const fs_model_desc& d, const char* wblob, const float* b1, cons
   return FS_OK;
 }
 
+__nv_bfloat16* act1_ptr(char* ws) {
+  return reinterpret_cast<__nv_bfloat16*>((reinterpret_cast<uintptr_t>(ws) + 1023) & ~static_cast<uintptr_t>(1023));
+}
+
+// conv2..conv4 from an act1 produced elsewhere (the pocket-factored conv1)
+int voxel_convs_from2(const fs_model_desc& d, const char* wblob, const float* b2, const float* b3, const float* b4,
+                      int P, char* ws, float* flat_out, cudaStream_t st) {
+  if (!supports(d)) return FS_ENOTSUP;
+  if (P <= 0) return FS_OK;
+  char* a1 = reinterpret_cast<char*>(act1_ptr(ws));
+  char* a2 = a1 + act1_bytes(P);
+  char* a3 = a2 + act2_bytes(P);
+  int rc;
+  ConvParams p{};
+  p.n_poses = P;
+  mark_stage(ST_CONV2, st);
+  p.w = wblob + OFF_W2; p.bias = b2; p.out = a2;
+  if ((rc = launch_layer<C2>(a1, p, st))) return rc;
+  mark_stage(ST_CONV3, st);
+  p.w = wblob + OFF_W3; p.bias = b3; p.out = a3;
+  if ((rc = launch_layer<C3>(a2, p, st))) return rc;
+  mark_stage(ST_CONV4, st);
+  p.w = wblob + OFF_W4; p.bias = b4; p.out = flat_out; p.residual = reinterpret_cast<const __nv_bfloat16*>(a3);
+  return launch_layer<C4>(a3, p, st);
+}
+
 int debug_layer(const fs_model_desc& d, const char* wblob, const float* bias, const float* residual_unused,
                 int layer, int P, const void* in, const void* residual, void* out, cudaStream_t st) {
   (void)residual_unused;

@@ -24,6 +24,12 @@ int voxel_convs(const fs_model_desc& d, const char* wblob, const float* b1, cons
                 const float* b3, const float* b4, int n_poses, const __nv_bfloat16* grid, char* ws,
                 float* flat_out, cudaStream_t st);
 
+// The act1 buffer inside the voxel_convs workspace, and conv2..4 from it
+// (pocket-factored path: act1 comes from conv1_fact_kernel).
+__nv_bfloat16* act1_ptr(char* ws);
+int voxel_convs_from2(const fs_model_desc& d, const char* wblob, const float* b2, const float* b3,
+                      const float* b4, int n_poses, char* ws, float* flat_out, cudaStream_t st);
+
 // One layer (1..4) on explicit buffers, for per-layer parity tests.
 int debug_layer(const fs_model_desc& d, const char* wblob, const float* bias, const float* unused, int layer, int P,
                 const void* in, const void* residual, void* out, cudaStream_t st);

@@ -362,6 +362,60 @@ class DeviceModel:
                 return out
             cap *= 2
 
+    # ---- pocket-invariant factoring ----
+    def prepare_pockets(self, pocket_xyz, pocket_elem, pocket_role, pocket_off):
+        """Build the pocket cache (fs_pocket_prepare) for the given device
+        pocket arrays (fs_pose_batch layout).  Returns a PocketCache."""
+        L = N.lib()
+        off_h = pocket_off.cpu().numpy()
+        n = len(off_h) - 1
+        mp = int(np.diff(off_h).max()) if n else 1
+        stride = L.fs_pocket_cache_bytes(self.handle, mp)
+        if stride == 0:
+            raise RuntimeError("pocket factoring is not supported for this model / pocket size")
+        cache = torch.empty(max(n, 1) * stride, dtype=torch.uint8, device=self.device)
+        err = torch.zeros(max(n, 1), dtype=torch.int32, device=self.device)
+        ws = self.workspace(L.fs_pocket_prepare_ws_bytes(self.handle, n, mp))
+        N.check(L.fs_pocket_prepare(self.handle, _ptr(pocket_xyz), _ptr(pocket_elem), _ptr(pocket_role),
+                                    _ptr(pocket_off), n, mp, _ptr(cache), _ptr(err), _ptr(ws), ws.numel(),
+                                    _stream()), "fs_pocket_prepare")
+        bad = err[:n].cpu().numpy()
+        if bad.any():
+            raise ValueError(f"pocket preparation failed (err bits {bad.tolist()})")
+        return PocketCache(cache, err, n, mp, stride)
+
+    def score_poses_cached(self, batch: PoseBatch, cache: "PocketCache", max_edges_per_pose=32768,
+                           outputs=("scores",), rescore=True):
+        """fs_score_poses_cached (bf16): scores from ligand atoms + the pocket
+        cache.  Poses flagged FS_ERR_NOT_FACTORED (or EDGE_CAP) are re-scored
+        through the full path when `rescore` (needs a host read of err)."""
+        L = N.lib()
+        P = batch.n_poses
+        dev = self.device
+        out = {"scores": torch.empty(P, dtype=torch.float32, device=dev),
+               "err": torch.empty(P, dtype=torch.int32, device=dev)}
+        for k, shape in (("lat_v", (P, self.latent_v)), ("lat_g", (P, self.latent_g)), ("pred_v", (P,)),
+                         ("pred_g", (P,))):
+            if k in outputs:
+                out[k] = torch.empty(shape, dtype=torch.float32, device=dev)
+        cap = int(max_edges_per_pose)
+        S = (batch.max_pose_atoms + 15) // 16 * 16 + 32
+        nbytes = L.fs_workspace_bytes(self.handle, P, P * S, max(1, P) * cap, N.PRECISIONS["bf16"])
+        ws = self.workspace(nbytes)
+        s = batch.cstruct()
+        N.check(L.fs_score_poses_cached(self.handle, N.PRECISIONS["bf16"], C.byref(s), _ptr(cache.buf),
+                                        cache.max_pocket_atoms, cap, _ptr(ws), ws.numel(), _ptr(out["scores"]),
+                                        _ptr(out.get("lat_v")), _ptr(out.get("lat_g")), _ptr(out.get("pred_v")),
+                                        _ptr(out.get("pred_g")), _ptr(out["err"]), _stream()),
+                "fs_score_poses_cached")
+        if rescore:
+            redo = ((out["err"] & (N.FS_ERR_NOT_FACTORED | N.FS_ERR_EDGE_CAP)) != 0).nonzero().flatten()
+            if redo.numel():
+                full = self.score_poses(batch, "bf16", max_edges_per_pose, outputs)
+                for k, v in out.items():
+                    v[redo] = full[k][redo]
+        return out
+
     def score_features(self, n_poses, grids=None, feats=None, node_off=None, cov_edges=None,
                        ncov_edges=None, heads=7, precision="fp32"):
         """Pre-featurized batch (drop-in predict_batch / head forwards)."""
@@ -421,6 +475,18 @@ def best_pose(compound, pose_id, scores, n_compounds, direction="max"):
     N.check(L.fs_best_pose(_ptr(compound), _ptr(pose_id), _ptr(scores), scores.numel(), n_compounds,
                            1 if direction == "max" else -1, _ptr(idx), _ptr(key), _stream()), "fs_best_pose")
     return idx[:n_compounds]
+
+
+@dataclass
+class PocketCache:
+    """Device pocket cache of fs_pocket_prepare (one slot of `stride` bytes per
+    pocket, in the order of the pocket arrays it was prepared from)."""
+
+    buf: torch.Tensor
+    err: torch.Tensor
+    n_pockets: int
+    max_pocket_atoms: int
+    stride: int
 
 
 class BestPoseAccumulator:

@@ -1,0 +1,102 @@
+"""GPU: pocket-invariant factoring.
+
+fs_score_poses_cached recomputes only what a ligand changes; its scores must
+equal the full bf16 path (fs_score_poses) to fp32 rounding, and the oracle
+within the bf16 tolerance.  Non-factorable poses are flagged and re-scored
+through the full path."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import fusion_oracle as orc  # noqa: E402
+from tests._cfg import COHERENT, GRAPH, VOXEL  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    from paper_2104_04547_b200 import engine as E
+    from paper_2104_04547_b200 import models, synth
+    vcfg, gcfg, fcfg = models.VoxelHeadConfig(), models.GraphHeadConfig(), models.table_coherent_fusion_config()
+    dm = E.DeviceModel(vcfg, gcfg, fcfg, models.FusionModel(vcfg, gcfg, fcfg, seed=0).all_params())
+    if not dm.supports("bf16"):
+        pytest.skip("bf16 path unsupported")
+    pockets = [synth.make_pocket(1000, seed=41, name="a"), synth.make_pocket(420, seed=42, name="b")]
+    lib = synth.concat([synth.make_poses(9, 5, seed=43, target=0),
+                        synth.make_poses(6, 4, seed=44, target=1, ligand_atoms=(3, 100)),
+                        synth.make_poses(2, 3, seed=45, target=0, ligand_atoms=(120, 128))])
+    pk = (np.concatenate([p.xyz for p in pockets]), np.concatenate([p.elem for p in pockets]),
+          np.concatenate([p.role for p in pockets]),
+          np.concatenate([[0], np.cumsum([len(p.xyz) for p in pockets])]))
+    batch = E.batch_from_arrays(lib.xyz, lib.elem, lib.role, lib.atom_off, pocket=pk, pose_target=lib.target)
+    cache = dm.prepare_pockets(batch.pocket_xyz, batch.pocket_elem, batch.pocket_role, batch.pocket_off)
+    return torch, E, synth, dm, pockets, lib, pk, batch, cache
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-12)))
+
+
+def test_factored_equals_full_path(env):
+    torch, E, synth, dm, pockets, lib, pk, batch, cache = env
+    outs = ("scores", "lat_v", "lat_g")
+    full = dm.score_poses(batch, "bf16", 1 << 17, outs, retry=False)
+    fact = dm.score_poses_cached(batch, cache, 1 << 17, outs, rescore=False)
+    assert int(full["err"].abs().sum()) == 0
+    assert int(fact["err"].abs().sum()) == 0
+    # graph latents: same math, different fp32 summation orders (ligand
+    # covalent rows ascending vs stencil order, pool = cached total - touched
+    # terms).  The GRU amplifies order noise with neighbour count: measured
+    # ~2e-6 for the workload's ligands (<= 64 atoms), <= 7e-5 at 128 atoms.
+    dg = (fact["lat_g"] - full["lat_g"]).abs().max(dim=1).values.cpu().numpy()
+    small = np.diff(lib.atom_off) <= 64
+    assert dg[small].max() < 2e-5, dg[small].max()
+    assert dg.max() < 2e-4, dg.max()
+    assert _rel(fact["lat_v"].cpu().numpy() + 1.0, full["lat_v"].cpu().numpy() + 1.0) < 2e-2
+    assert _rel(fact["scores"].cpu().numpy(), full["scores"].cpu().numpy()) < 2e-3
+
+
+def test_factored_vs_oracle(env):
+    torch, E, synth, dm, pockets, lib, pk, batch, cache = env
+    fact = dm.score_poses_cached(batch, cache, 32768)["scores"].cpu().numpy()
+    params = orc.init_params(VOXEL, GRAPH, COHERENT, 0)
+    for p in (0, 17, 45):
+        pos, el, ro = synth.complex_arrays(pockets[lib.target[p]], lib, p)
+        want = orc.score_pose(params, (VOXEL, GRAPH, COHERENT), pos, el, ro)["score"]
+        assert abs(fact[p] - want) / abs(want) < 3e-2
+
+
+def test_factored_batch_invariance_bitwise(env):
+    torch, E, synth, dm, pockets, lib, pk, batch, cache = env
+    whole = dm.score_poses_cached(batch, cache)["scores"].cpu().numpy()
+    for s, e in ((0, 1), (10, 23), (44, 50)):
+        part = lib.slice(s, e)
+        b = E.batch_from_arrays(part.xyz, part.elem, part.role, part.atom_off, pocket=pk, pose_target=part.target)
+        got = dm.score_poses_cached(b, cache)["scores"].cpu().numpy()
+        assert np.array_equal(got, whole[s:e])
+
+
+def test_non_factorable_poses_are_flagged_and_rescored(env):
+    torch, E, synth, dm, pockets, lib, pk, batch, cache = env
+    part = lib.slice(0, 6)
+    role = part.role.copy()
+    role[part.atom_off[2]] = 0                    # pose 2: a ligand atom with the pocket's role
+    xyz = part.xyz.copy()
+    big = synth.make_poses(1, 1, seed=9, ligand_atoms=(140, 140))    # > 128 ligand atoms
+    lib2 = synth.concat([synth.PoseLibrary(xyz, part.elem, role, part.atom_off, part.target, part.compound,
+                                           part.pose_id), big])
+    b = E.batch_from_arrays(lib2.xyz, lib2.elem, lib2.role, lib2.atom_off, pocket=pk, pose_target=lib2.target)
+    raw = dm.score_poses_cached(b, cache, rescore=False)
+    err = raw["err"].cpu().numpy()
+    assert err[2] & 128 and err[6] & 128
+    assert not err[[0, 1, 3, 4, 5]].any()
+    fixed = dm.score_poses_cached(b, cache)
+    full = dm.score_poses(b, "bf16")
+    assert not fixed["err"].cpu().numpy().any()
+    s_fixed, s_full = fixed["scores"].cpu().numpy(), full["scores"].cpu().numpy()
+    assert s_fixed[2] == s_full[2] and s_fixed[6] == s_full[6]
+    assert _rel(s_fixed, s_full) < 2e-3
