@@ -54,8 +54,10 @@ int launch_graph_fact(const fs_pose_batch& b, double tc, double tn, double box, 
                       int32_t* col_cov, int64_t* row_ncov, int32_t* deg_ncov, int32_t* col_ncov, int32_t* err,
                       cudaStream_t st);
 bool conv1_fact_supported(int g, int k, int cin, int cout);
-int launch_conv1_fact(const fs_pose_batch& b, const char* cache, int64_t cache_stride, int64_t off_pp, const float* w,
-                      int c_elem, double box, __nv_bfloat16* out, cudaStream_t st);
+int launch_conv1_fact(const fs_pose_batch& b, const char* cache, int64_t cache_stride, int64_t off_pp,
+                      int64_t off_ppact, int64_t off_wl, int c_elem, double box, __nv_bfloat16* out, cudaStream_t st);
+int launch_pocket_conv1_fields(const float* pp, int n_pockets, char* cache, int64_t cache_stride, int64_t off_ppact,
+                               int64_t off_wl, const float* w1, int c_elem, cudaStream_t st);
 int launch_round_bf16(const float* in, float* out, int64_t n, cudaStream_t st);
 int launch_pocket_total(const int64_t* pocket_off, int n_pockets, const float* f, int64_t ld, char* cache,
                         int64_t cache_stride, int64_t off_T, int64_t off_n, cudaStream_t st);
@@ -491,7 +493,7 @@ static WsPlan plan_ws(const fs_model& m, int64_t P, int64_t N, int64_t E, int pr
 
 // ---- pocket cache (fs_pocket_prepare / fs_score_poses_cached) --------------
 struct PocketCacheLayout {
-  int64_t off_n, off_T, off_pp, off_hcov, off_f, bytes;
+  int64_t off_n, off_T, off_pp, off_ppact, off_wl, off_hcov, off_f, bytes;
 };
 
 static PocketCacheLayout cache_layout(const fs_model& m, int max_pocket) {
@@ -499,7 +501,9 @@ static PocketCacheLayout cache_layout(const fs_model& m, int max_pocket) {
   L.off_n = 0;
   L.off_T = 256;
   L.off_pp = (int64_t)align_up(L.off_T + 8 * 128, 256);
-  L.off_hcov = (int64_t)align_up(L.off_pp + (int64_t)4 * m.G * m.G * m.G * m.f1, 256);
+  L.off_ppact = (int64_t)align_up(L.off_pp + (int64_t)4 * m.G * m.G * m.G * m.f1, 256);
+  L.off_wl = (int64_t)align_up(L.off_ppact + (int64_t)2 * m.G * m.G * m.G * m.f1, 256);
+  L.off_hcov = (int64_t)align_up(L.off_wl + (int64_t)4 * m.k1 * m.k1 * m.k1 * m.d.c_elem * m.f1, 256);
   L.off_f = (int64_t)align_up(L.off_hcov + (int64_t)4 * 24 * max_pocket, 256);
   L.bytes = (int64_t)align_up(L.off_f + (int64_t)4 * 128 * max_pocket, 256);
   return L;
@@ -930,7 +934,7 @@ int fs_pocket_prepare(const fs_model* m, const double* pocket_xyz, const int32_t
   if ((rc = launch_conv3d_ffma(c, st))) return rc;
   const size_t ppb = (size_t)4 * m->G * m->G * m->G * m->f1;
   FS_CUDA_CHECK(cudaMemcpy2DAsync(C + L.off_pp, L.bytes, pp, ppb, ppb, n, cudaMemcpyDeviceToDevice, st));
-  return FS_OK;
+  return launch_pocket_conv1_fields(pp, n, C, L.bytes, L.off_ppact, L.off_wl, m->P(m->c1w), d.c_elem, st);
 }
 
 int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch* b, const void* cache,
@@ -964,8 +968,8 @@ int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch*
                               (int32_t*)(W + w.col_ncov), err, st)))
     return rc;
   mark_stage(ST_CONV1, st);
-  if ((rc = launch_conv1_fact(*b, (const char*)cache, L.bytes, L.off_pp, m->P(m->c1w), d.c_elem, d.box_size,
-                              umma::act1_ptr(W + w.umma), st)))
+  if ((rc = launch_conv1_fact(*b, (const char*)cache, L.bytes, L.off_pp, L.off_ppact, L.off_wl, d.c_elem,
+                              d.box_size, umma::act1_ptr(W + w.umma), st)))
     return rc;
   if ((rc = umma::voxel_convs_from2(d, (const char*)m->blob + m->umma_off, m->P(m->c2b), m->P(m->c3b), m->P(m->c4b),
                                     P, W + w.umma, (float*)(W + w.p2), st)))

@@ -11,99 +11,118 @@
 // chunk-major [P][C/8][D][H][W][8]) feeds the tcgen05 conv2 unchanged.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace fs {
 
 struct Conv1FactArgs {
   fs_pose_batch b;
-  const char* cache; int64_t cache_stride; int64_t off_pp;   // pre-activation [G^3][COUT] fp32 per pocket
-  const float* w;               // conv1 weights [k^3][cin][cout] fp32 (rounded to bf16 here)
+  const char* cache; int64_t cache_stride;
+  int64_t off_pp;               // pre-activation [G^3][COUT] fp32 (pocket channels + bias)
+  int64_t off_ppact;            // relu(pre-activation) as bf16 in the act1 layout [COUT/8][G^3][8]
+  int64_t off_wl;               // ligand-channel weights [k^3][c_elem][COUT], bf16-valued fp32
   int c_elem; double box;
   __nv_bfloat16* out;           // [P][COUT/8][G^3][8]
 };
 
 constexpr int kC1G = 16, kC1K = 5, kC1R = 2, kC1Out = 32, kC1MaxLig = 128;
+constexpr int kC1G3 = kC1G * kC1G * kC1G;
+constexpr int kC1Threads = 256;
 
-// 256 threads = the 16x16 (h, w) columns; each walks d = 0..15.
-__global__ void __launch_bounds__(256) conv1_fact_kernel(Conv1FactArgs a) {
-  extern __shared__ __align__(16) float wl[];           // [k^3][c_elem][32] ligand-channel weights
+// Persistent CTAs, one pose at a time:
+//  1. ligand atoms -> voxels; mark every output voxel within the 5^3 window
+//     of a ligand atom (bitmask);
+//  2. voxels no ligand atom reaches: act1 = cached relu(pocket pre-activation)
+//     (a 16-byte copy per 8 channels, L2 -> HBM);
+//  3. reached voxels: pocket pre-activation + the ligand atoms' weights, in
+//     atom order (deterministic), ReLU, bf16.
+__global__ void __launch_bounds__(kC1Threads) conv1_fact_kernel(Conv1FactArgs a) {
+  extern __shared__ __align__(16) float wl[];           // [k^3][c_elem][32]
   __shared__ int4 atoms[kC1MaxLig];                      // (ix, iy, iz, ligand channel)
-  const int p = blockIdx.x;
-  const PoseView pv = pose_view(a.b, p);
-  const int nL = (int)pv.na;
-  if (nL > kC1MaxLig || pv.np_ == 0) return;             // not factorable (flagged by graph_fact_kernel)
-  const int cin = 2 * a.c_elem;
-  const int kk = kC1K * kC1K * kC1K;
-  for (int i = threadIdx.x; i < kk * a.c_elem * kC1Out; i += blockDim.x) {
-    const int o = i % kC1Out, c = (i / kC1Out) % a.c_elem, k = i / (kC1Out * a.c_elem);
-    wl[i] = __bfloat162float(__float2bfloat16_rn(a.w[(static_cast<int64_t>(k) * cin + a.c_elem + c) * kC1Out + o]));
-  }
+  __shared__ uint32_t touched[kC1G3 / 32];
+  __shared__ int s_cnt;
+  __shared__ uint16_t tlist[kC1G3];
+  const int nw = kC1K * kC1K * kC1K * a.c_elem * kC1Out;
+  const char* c0 = a.cache;   // the weights are identical in every pocket slot
+  for (int i = threadIdx.x; i < nw / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(wl)[i] = reinterpret_cast<const float4*>(c0 + a.off_wl)[i];
   const double half = a.box / 2.0, gd = kC1G;
-  for (int s = threadIdx.x; s < nL; s += blockDim.x) {
-    double x, y, z; int32_t e, r;
-    pv.atom(pv.np_ + s, x, y, z, e, r);
-    // voxel index exactly as the voxelizer (complexes.py:180-181)
-    auto ax = [&](double v) {
-      double t = __dmul_rn(__ddiv_rn(__dadd_rn(v, half), a.box), gd);
-      t = floor(t);
-      t = fmin(fmax(t, 0.0), gd - 1.0);
-      return (int)t;
-    };
-    atoms[s] = make_int4(ax(x), ax(y), ax(z), min(max(e, 0), a.c_elem - 1));
-  }
-  __syncthreads();
-  const int h = threadIdx.x >> 4, w = threadIdx.x & 15;
-  uint32_t near[kC1MaxLig / 32];
-#pragma unroll
-  for (int wd = 0; wd < kC1MaxLig / 32; ++wd) {
-    uint32_t m = 0u;
-    for (int s = 32 * wd; s < min(nL, 32 * wd + 32); ++s) {
-      const int4 at = atoms[s];
-      if (abs(at.y - h) <= kC1R && abs(at.z - w) <= kC1R) m |= 1u << (s & 31);
+  for (int p = blockIdx.x; p < a.b.n_poses; p += gridDim.x) {
+    const PoseView pv = pose_view(a.b, p);
+    const int nL = (int)pv.na;
+    if (nL > kC1MaxLig || pv.np_ == 0) continue;         // not factorable (flagged by graph_fact_kernel)
+    __syncthreads();                                     // previous pose done with atoms/touched/tlist
+    for (int i = threadIdx.x; i < kC1G3 / 32; i += blockDim.x) touched[i] = 0u;
+    if (threadIdx.x == 0) s_cnt = 0;
+    for (int s = threadIdx.x; s < nL; s += blockDim.x) {
+      double x, y, z; int32_t e, r;
+      pv.atom(pv.np_ + s, x, y, z, e, r);
+      // voxel index exactly as the voxelizer (complexes.py:180-181)
+      auto ax = [&](double v) {
+        double t = __dmul_rn(__ddiv_rn(__dadd_rn(v, half), a.box), gd);
+        t = floor(t);
+        t = fmin(fmax(t, 0.0), gd - 1.0);
+        return (int)t;
+      };
+      atoms[s] = make_int4(ax(x), ax(y), ax(z), min(max(e, 0), a.c_elem - 1));
     }
-    near[wd] = m;
-  }
-  const float* pp = reinterpret_cast<const float*>(a.cache + static_cast<int64_t>(a.b.pose_target[p]) * a.cache_stride +
-                                                   a.off_pp);
-  constexpr int64_t G3 = kC1G * kC1G * kC1G;
-  for (int d = 0; d < kC1G; ++d) {
-    const int vox = (d * kC1G + h) * kC1G + w;
-    float acc[kC1Out];
-    const float4* src = reinterpret_cast<const float4*>(pp + static_cast<int64_t>(vox) * kC1Out);
-#pragma unroll
-    for (int q = 0; q < kC1Out / 4; ++q) {
-      const float4 v = __ldg(src + q);
-      acc[4 * q] = v.x; acc[4 * q + 1] = v.y; acc[4 * q + 2] = v.z; acc[4 * q + 3] = v.w;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nL * 125; i += blockDim.x) {
+      const int4 at = atoms[i / 125];
+      const int k = i % 125;
+      const int d = at.x + k / 25 - kC1R, h = at.y + (k / 5) % 5 - kC1R, w = at.z + k % 5 - kC1R;
+      if (d < 0 || d >= kC1G || h < 0 || h >= kC1G || w < 0 || w >= kC1G) continue;
+      const int v = (d * kC1G + h) * kC1G + w;
+      atomicOr(&touched[v >> 5], 1u << (v & 31));
     }
-    // ligand atoms in deterministic (atom) order: out[o] += W[v - o + r] (cross-correlation, 'same')
+    __syncthreads();
+    const char* pc = a.cache + static_cast<int64_t>(a.b.pose_target[p]) * a.cache_stride;
+    const uint4* ppact = reinterpret_cast<const uint4*>(pc + a.off_ppact);
+    uint4* op = reinterpret_cast<uint4*>(a.out) + static_cast<int64_t>(p) * (kC1Out / 8) * kC1G3;
+    // untouched voxels: copy; touched ones: list them
+    for (int u = threadIdx.x; u < (kC1Out / 8) * kC1G3; u += blockDim.x) {
+      const int v = u & (kC1G3 - 1);
+      const bool t = (touched[v >> 5] >> (v & 31)) & 1u;
+      if (!t) op[u] = __ldg(ppact + u);
+      else if (u < kC1G3) tlist[atomicAdd(&s_cnt, 1)] = static_cast<uint16_t>(v);
+    }
+    __syncthreads();
+    const float* pp = reinterpret_cast<const float*>(pc + a.off_pp);
+    const int nt = s_cnt;
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+      const int v = tlist[i];
+      const int d = v >> 8, h = (v >> 4) & 15, w = v & 15;
+      float acc[kC1Out];
+      const float4* src = reinterpret_cast<const float4*>(pp + static_cast<int64_t>(v) * kC1Out);
 #pragma unroll
-    for (int wd = 0; wd < kC1MaxLig / 32; ++wd) {
-      uint32_t bits = near[wd];
-      while (bits) {
-        const int s = 32 * wd + __ffs(bits) - 1;
-        bits &= bits - 1;
+      for (int q = 0; q < kC1Out / 4; ++q) {
+        const float4 x = __ldg(src + q);
+        acc[4 * q] = x.x; acc[4 * q + 1] = x.y; acc[4 * q + 2] = x.z; acc[4 * q + 3] = x.w;
+      }
+      // out[o] += W[v_atom - o + r] (cross-correlation, 'same'), atom order
+      for (int s = 0; s < nL; ++s) {
         const int4 at = atoms[s];
-        const int kd = at.x - d + kC1R;
-        if (kd < 0 || kd >= kC1K) continue;
-        const int k = (kd * kC1K + (at.y - h + kC1R)) * kC1K + (at.z - w + kC1R);
+        const int kd = at.x - d + kC1R, kh = at.y - h + kC1R, kw = at.z - w + kC1R;
+        if ((unsigned)kd >= kC1K || (unsigned)kh >= kC1K || (unsigned)kw >= kC1K) continue;
+        const int k = (kd * kC1K + kh) * kC1K + kw;
         const float4* wk = reinterpret_cast<const float4*>(wl + (k * a.c_elem + at.w) * kC1Out);
 #pragma unroll
         for (int q = 0; q < kC1Out / 4; ++q) {
-          const float4 v = wk[q];
-          acc[4 * q] += v.x; acc[4 * q + 1] += v.y; acc[4 * q + 2] += v.z; acc[4 * q + 3] += v.w;
+          const float4 x = wk[q];
+          acc[4 * q] += x.x; acc[4 * q + 1] += x.y; acc[4 * q + 2] += x.z; acc[4 * q + 3] += x.w;
         }
       }
-    }
-    uint4* op = reinterpret_cast<uint4*>(a.out) + static_cast<int64_t>(p) * (kC1Out / 8) * G3 + vox;
 #pragma unroll
-    for (int q = 0; q < kC1Out / 8; ++q) {
-      uint4 pk;
-      __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+      for (int q = 0; q < kC1Out / 8; ++q) {
+        uint4 pk;
+        __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&pk);
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
-        b2[t] = __floats2bfloat162_rn(fmaxf(acc[8 * q + 2 * t], 0.f), fmaxf(acc[8 * q + 2 * t + 1], 0.f));
-      op[q * G3] = pk;
+        for (int t = 0; t < 4; ++t)
+          b2[t] = __floats2bfloat162_rn(fmaxf(acc[8 * q + 2 * t], 0.f), fmaxf(acc[8 * q + 2 * t + 1], 0.f));
+        op[q * kC1G3 + v] = pk;
+      }
     }
   }
 }
@@ -112,15 +131,50 @@ bool conv1_fact_supported(int g, int k, int cin, int cout) {
   return g == kC1G && k == kC1K && cout == kC1Out && cin % 2 == 0 && cin / 2 <= 8;
 }
 
-int launch_conv1_fact(const fs_pose_batch& b, const char* cache, int64_t cache_stride, int64_t off_pp, const float* w,
-                      int c_elem, double box, __nv_bfloat16* out, cudaStream_t st) {
+int launch_conv1_fact(const fs_pose_batch& b, const char* cache, int64_t cache_stride, int64_t off_pp,
+                      int64_t off_ppact, int64_t off_wl, int c_elem, double box, __nv_bfloat16* out, cudaStream_t st) {
   if (b.n_poses <= 0) return FS_OK;
   Conv1FactArgs a;
-  a.b = b; a.cache = cache; a.cache_stride = cache_stride; a.off_pp = off_pp; a.w = w;
-  a.c_elem = c_elem; a.box = box; a.out = out;
+  a.b = b; a.cache = cache; a.cache_stride = cache_stride; a.off_pp = off_pp; a.off_ppact = off_ppact;
+  a.off_wl = off_wl; a.c_elem = c_elem; a.box = box; a.out = out;
   const size_t smem = static_cast<size_t>(kC1K * kC1K * kC1K) * c_elem * kC1Out * 4;
   FS_CUDA_CHECK(cudaFuncSetAttribute(conv1_fact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  conv1_fact_kernel<<<b.n_poses, 256, smem, st>>>(a);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv1_fact_kernel, kC1Threads, smem);
+  const int grid = static_cast<int>(std::min<int64_t>(b.n_poses, static_cast<int64_t>(sms) * std::max(per_sm, 1)));
+  conv1_fact_kernel<<<grid, kC1Threads, smem, st>>>(a);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
+// cache fields derived from the pocket pre-activation: relu'd bf16 act1
+// layout, and (slot-independent) the ligand-channel weights as bf16 values
+__global__ void pocket_conv1_fields_kernel(const float* pp, int64_t pp_ld, char* cache, int64_t cache_stride,
+                                           int64_t off_ppact, int64_t off_wl, const float* w1, int c_elem) {
+  const int q = blockIdx.y;
+  const float* src = pp + static_cast<int64_t>(q) * pp_ld;
+  char* c = cache + static_cast<int64_t>(q) * cache_stride;
+  __nv_bfloat16* act = reinterpret_cast<__nv_bfloat16*>(c + off_ppact);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kC1G3 * kC1Out; i += gridDim.x * blockDim.x) {
+    const int v = i / kC1Out, o = i % kC1Out;
+    act[(static_cast<int64_t>(o / 8) * kC1G3 + v) * 8 + (o & 7)] = __float2bfloat16_rn(fmaxf(src[i], 0.f));
+  }
+  float* wlc = reinterpret_cast<float*>(c + off_wl);
+  const int cin = 2 * c_elem, nw = kC1K * kC1K * kC1K * c_elem * kC1Out;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) {
+    const int o = i % kC1Out, ch = (i / kC1Out) % c_elem, k = i / (kC1Out * c_elem);
+    wlc[i] = __bfloat162float(__float2bfloat16_rn(w1[(static_cast<int64_t>(k) * cin + c_elem + ch) * kC1Out + o]));
+  }
+}
+
+int launch_pocket_conv1_fields(const float* pp, int n_pockets, char* cache, int64_t cache_stride, int64_t off_ppact,
+                               int64_t off_wl, const float* w1, int c_elem, cudaStream_t st) {
+  if (n_pockets <= 0) return FS_OK;
+  dim3 grid(64, n_pockets);
+  pocket_conv1_fields_kernel<<<grid, 256, 0, st>>>(pp, static_cast<int64_t>(kC1G3) * kC1Out, cache, cache_stride,
+                                                   off_ppact, off_wl, w1, c_elem);
   FS_LAUNCH_CHECK();
   return FS_OK;
 }

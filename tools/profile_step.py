@@ -18,8 +18,13 @@ dm = E.DeviceModel(vcfg, gcfg, fcfg, m.all_params())
 pocket = synth.make_pocket(1000, seed=0)
 lib = synth.make_poses((2 * B) // 10 + 1, 10, seed=1).slice(0, 2 * B)
 dl = DeviceLibrary(lib, [pocket], torch.device("cuda"))
+fact = os.environ.get("FS_PROFILE_FACTORED") == "1"
+cache = dm.prepare_pockets(dl.pocket_xyz, dl.pocket_elem, dl.pocket_role, dl.pocket_off) if fact else None
 for i in range(2):
-    out = dm.score_poses(dl.batch(i * B, (i + 1) * B), prec, 32768, retry=False)
+    if fact:
+        out = dm.score_poses_cached(dl.batch(i * B, (i + 1) * B), cache, 32768, rescore=False)
+    else:
+        out = dm.score_poses(dl.batch(i * B, (i + 1) * B), prec, 32768, retry=False)
 torch.cuda.synchronize()
 assert int(out["err"].abs().sum()) == 0
 print("ok", float(out["scores"].float().mean()))
