@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     return;
   }
   const int ntiles = (n + 15) / 16, npad = ntiles * 16;
-  const int srows = max(npad + 1, 86);   // S doubles as the pool's reduction buffer (>= 2048 floats)
+  const int srows = max(npad + 1, 256);  // S doubles as the pool's reduction buffers (>= 6144 floats)
   // H: node states [npad + 1][24], row npad stays zero (padded gathers read it)
   // S: neighbour sums [srows][24], row npad is the sink of padded tile slots
   float* H = sm;
@@ -501,15 +501,27 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
       for (int e = 0; e < 2; ++e) RED[warp * 128 + 8 * j + 2 * t + e] = acc[j][e];
   }
+  double* RED2 = reinterpret_cast<double*>(RED + kMmaWarps * 128);   // [warps][128] (factored only)
+  if constexpr (FACT) {
+    // cached pool terms of the touched pocket nodes (to be replaced by their
+    // recomputed ones): warp w sums rows nLp+w, nLp+w+16, ...; lane owns 4 columns
+    const float* f = reinterpret_cast<const float*>(pc + a.off_f);
+    double cs[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r = nLp + warp; r < n; r += kMmaWarps) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(f + static_cast<int64_t>(a.fact_aff[base + r]) * 128) + lane);
+      cs[0] += v.x; cs[1] += v.y; cs[2] += v.z; cs[3] += v.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) RED2[warp * 128 + 4 * lane + k] = cs[k];
+  }
   __syncthreads();
   if (threadIdx.x < 128) {
     float tot = 0.f;
     for (int w = 0; w < kMmaWarps; ++w) tot += RED[w * 128 + threadIdx.x];
     if constexpr (FACT) {
       // untouched pocket nodes: cached total minus the touched ones' cached terms
-      const float* f = reinterpret_cast<const float*>(pc + a.off_f);
       double corr = reinterpret_cast<const double*>(pc + a.off_T)[threadIdx.x];
-      for (int r = nLp; r < n; ++r) corr -= f[static_cast<int64_t>(a.fact_aff[base + r]) * 128 + threadIdx.x];
+      for (int w = 0; w < kMmaWarps; ++w) corr -= RED2[w * 128 + threadIdx.x];
       const int n_all = *reinterpret_cast<const int32_t*>(pc + a.off_n) + nL;
       lat[threadIdx.x] = static_cast<float>((corr + static_cast<double>(tot)) / static_cast<double>(max(n_all, 1)));
     } else {
@@ -520,7 +532,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 
 size_t gnn_mma_smem_bytes(int max_nodes) {
   const int npad = (max_nodes + 15) / 16 * 16;
-  const int srows = npad + 1 > 86 ? npad + 1 : 86;
+  const int srows = npad + 1 > 256 ? npad + 1 : 256;
   return static_cast<size_t>(npad + 1 + srows) * 24 * 4 + kPhaseWords * 4 + 72 * 4 + kCtlWords * 4 +
          static_cast<size_t>(npad) * 2 + 64;
 }
