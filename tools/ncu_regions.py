@@ -39,18 +39,20 @@ def main(path, fname, specs):
             continue
         ie = hdr.index("Instructions Executed")
         st = hdr.index("Warp Stall Sampling (All Samples)")
+        reasons = [(i, h) for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
         try:
             addr = int(r[2], 16)
         except ValueError:
             continue
-        sass.append((addr, cur_file, line, float(r[ie] or 0), float(r[st] or 0)))
+        sass.append((addr, cur_file, line, float(r[ie] or 0), float(r[st] or 0),
+                     {h: float(r[i] or 0) for i, h in reasons}))
     sass.sort()
     tot_i = sum(s[3] for s in sass) or 1
     tot_s = sum(s[4] for s in sass) or 1
-    acc = {name: [0.0, 0.0] for name, _, _ in regions}
-    acc["other"] = [0.0, 0.0]
+    acc = {name: [0.0, 0.0, {}] for name, _, _ in regions}
+    acc["other"] = [0.0, 0.0, {}]
     last = None
-    for addr, f, ln, i, s in sass:
+    for addr, f, ln, i, s, rs in sass:
         if f == fname and ln >= MIN_LINE:
             last = ln
         reg = "other"
@@ -61,8 +63,12 @@ def main(path, fname, specs):
                     break
         acc[reg][0] += i
         acc[reg][1] += s
-    for k, (i, s) in acc.items():
-        print(f"{k:12s} instr {i / tot_i:6.1%}  stall {s / tot_s:6.1%}")
+        for h, v in rs.items():
+            acc[reg][2][h] = acc[reg][2].get(h, 0.0) + v
+    for k, (i, s, rs) in acc.items():
+        top = sorted(rs.items(), key=lambda x: -x[1])[:4]
+        tops = "  ".join(f"{h[6:]} {v / max(s, 1):.0%}" for h, v in top if v > 0)
+        print(f"{k:12s} instr {i / tot_i:6.1%}  stall {s / tot_s:6.1%}   {tops}")
 
 
 if __name__ == "__main__":
