@@ -380,6 +380,12 @@ def main():
             evs = stage_events[i]
             for j in range(len(N.STAGES) - 1):
                 fstage[j] += evs[j].elapsed_time(evs[j + 1])
+        if os.environ.get("FS_BENCH_VERBOSE"):
+            steps = [sum(stage_events[i][j].elapsed_time(stage_events[i][j + 1]) for j in range(len(N.STAGES) - 1))
+                     for i in range(K)]
+            gaps = [stage_events[i][-1].elapsed_time(stage_events[i + 1][0]) for i in range(K - 1)]
+            print("factored step ms", [round(x, 2) for x in steps], "gaps", [round(x, 2) for x in gaps],
+                  "total", f0.elapsed_time(f1), file=sys.stderr)
         tf = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tf, op=dist.ReduceOp.MAX)

@@ -47,11 +47,11 @@ int launch_rows(const int32_t* deg, int64_t n, int64_t* row_ptr, void* ws, size_
 int launch_edge_counts(const int64_t* node_off, int n_poses, const int64_t* row_ptr, const int32_t* col, int64_t* edge_off, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_edges(const int64_t* node_off, int n_poses, const int64_t* row_ptr, const int32_t* col, const double* dist, const int64_t* edge_off, int64_t* edges, double* dists, cudaStream_t st);
 int launch_graph_csr(const fs_pose_batch& b, const int64_t* node_off, double tc, double tn, int64_t* row_cov,
-                     int32_t* deg_cov, int32_t* col_cov, double* dist_cov, int64_t* row_ncov, int32_t* deg_ncov,
-                     int32_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st);
+                     int32_t* deg_cov, col_t* col_cov, double* dist_cov, int64_t* row_ncov, int32_t* deg_ncov,
+                     col_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st);
 int launch_graph_fact(const fs_pose_batch& b, double tc, double tn, double box, int c_elem, int64_t S, int64_t cap,
                       int max_pocket, int32_t* cnt, int32_t* aff, float* feats, int64_t* row_cov, int32_t* deg_cov,
-                      int32_t* col_cov, int64_t* row_ncov, int32_t* deg_ncov, int32_t* col_ncov, int32_t* err,
+                      col_t* col_cov, int64_t* row_ncov, int32_t* deg_ncov, col_t* col_ncov, int32_t* err,
                       cudaStream_t st);
 bool conv1_fact_supported(int g, int k, int cin, int cout);
 int launch_conv1_fact(const fs_pose_batch& b, const char* cache, int64_t cache_stride, int64_t off_pp,
@@ -62,7 +62,7 @@ int launch_round_bf16(const float* in, float* out, int64_t n, cudaStream_t st);
 int launch_pocket_total(const int64_t* pocket_off, int n_pockets, const float* f, int64_t ld, char* cache,
                         int64_t cache_stride, int64_t off_T, int64_t off_n, cudaStream_t st);
 int launch_pocket_poses(int n, int64_t* atom_off, int32_t* target, cudaStream_t st);
-int launch_csr_from_edges(const int64_t* edges, int64_t ne, const int64_t* node_off, int n_poses, int64_t n_nodes, int32_t* node_pose, int32_t* deg, int64_t* row_ptr, int64_t* cursor, int32_t* col, void* ws, size_t ws_bytes, cudaStream_t st);
+int launch_csr_from_edges(const int64_t* edges, int64_t ne, const int64_t* node_off, int n_poses, int64_t n_nodes, int32_t* node_pose, int32_t* deg, int64_t* row_ptr, int64_t* cursor, col_t* col, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t scan_ws_bytes(int64_t n);
 
 struct ConvArgs {
@@ -83,8 +83,8 @@ int launch_f64_to_f32(const double* in, float* out, int64_t n, int row, const in
 
 struct GnnArgs {
   const float* feats; int F; const int64_t* node_off;
-  const int64_t* row_cov; const int32_t* deg_cov; const int32_t* col_cov;
-  const int64_t* row_ncov; const int32_t* deg_ncov; const int32_t* col_ncov;
+  const int64_t* row_cov; const int32_t* deg_cov; const col_t* col_cov;
+  const int64_t* row_ncov; const int32_t* deg_ncov; const col_t* col_ncov;
   const float* we; const float* be; const float* phase[2];
   const float* gg; const float* bg; const float* gf; const float* bf;
   int k_steps[2]; int gn; float* state; float* lat; int64_t ld_lat; const int32_t* err; int smem_state;
@@ -92,8 +92,8 @@ struct GnnArgs {
 int gnn_padded_width(int d);
 struct GnnMmaArgs {
   const float* feats; int F; const int64_t* node_off;
-  const int64_t* row_cov; const int32_t* deg_cov; const int32_t* col_cov;
-  const int64_t* row_ncov; const int32_t* deg_ncov; const int32_t* col_ncov;
+  const int64_t* row_cov; const int32_t* deg_cov; const col_t* col_cov;
+  const int64_t* row_ncov; const int32_t* deg_ncov; const col_t* col_ncov;
   const float* we; const float* be; const uint32_t* wfrag[2]; const float* wbias[2];
   const uint32_t* gfrag; const float* gbias; int k_steps[2]; float* lat; int64_t ld_lat; const int32_t* err;
   const int32_t* fact_cnt; int64_t fact_stride; const int32_t* fact_aff; const int32_t* pose_target;
@@ -579,8 +579,8 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
                       const GnnMmaArgs* extra = nullptr) {
   GnnArgs g{};
   g.feats = (float*)(ws + w.feats); g.F = m.F; g.node_off = (int64_t*)(ws + w.node_off);
-  g.row_cov = (int64_t*)(ws + w.row_cov); g.col_cov = (int32_t*)(ws + w.col_cov);
-  g.row_ncov = (int64_t*)(ws + w.row_ncov); g.col_ncov = (int32_t*)(ws + w.col_ncov);
+  g.row_cov = (int64_t*)(ws + w.row_cov); g.col_cov = (col_t*)(ws + w.col_cov);
+  g.row_ncov = (int64_t*)(ws + w.row_ncov); g.col_ncov = (col_t*)(ws + w.col_ncov);
   g.deg_cov = (int32_t*)(ws + w.deg_cov); g.deg_ncov = (int32_t*)(ws + w.deg_ncov);
   g.we = m.P(m.we); g.be = m.P(m.be); g.phase[0] = m.P(m.ph[0]); g.phase[1] = m.P(m.ph[1]);
   g.gg = m.P(m.gg); g.bg = m.P(m.bg); g.gf = m.P(m.gf); g.bf = m.P(m.bf);
@@ -829,8 +829,8 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   // radius graph: one fused launch, pose-private CSR slices of max_edges
   // entries per edge type (rows = start offset + degree)
   if ((rc = launch_graph_csr(*b, node_off, d.cov_thresh, d.noncov_thresh, (int64_t*)(W + w.row_cov),
-                             (int32_t*)(W + w.deg_cov), (int32_t*)(W + w.col_cov), nullptr, (int64_t*)(W + w.row_ncov),
-                             (int32_t*)(W + w.deg_ncov), (int32_t*)(W + w.col_ncov), nullptr, max_edges, err, st)))
+                             (int32_t*)(W + w.deg_cov), (col_t*)(W + w.col_cov), nullptr, (int64_t*)(W + w.row_ncov),
+                             (int32_t*)(W + w.deg_ncov), (col_t*)(W + w.col_ncov), nullptr, max_edges, err, st)))
     return rc;
   if (precision == FS_PREC_BF16) {
     if ((rc = launch_voxelize(*b, d.grid_extent, m->cgrid, d.box_size, FS_GRID_NDHWC_BF16, W + w.grid, err, st))) return rc;
@@ -909,8 +909,8 @@ int fs_pocket_prepare(const fs_model* m, const double* pocket_xyz, const int32_t
   if ((rc = launch_node_offsets(pb, node_off, W + w.scan, scan_ws_bytes((int64_t)n * mp) + 1024, st))) return rc;
   if ((rc = launch_node_features(pb, node_off, d.c_elem, d.box_size, W + w.feats, false, st))) return rc;
   if ((rc = launch_graph_csr(pb, node_off, d.cov_thresh, d.noncov_thresh, (int64_t*)(W + w.row_cov),
-                             (int32_t*)(W + w.deg_cov), (int32_t*)(W + w.col_cov), nullptr, (int64_t*)(W + w.row_ncov),
-                             (int32_t*)(W + w.deg_ncov), (int32_t*)(W + w.col_ncov), nullptr, cap, err, st)))
+                             (int32_t*)(W + w.deg_cov), (col_t*)(W + w.col_cov), nullptr, (int64_t*)(W + w.row_ncov),
+                             (int32_t*)(W + w.deg_ncov), (col_t*)(W + w.col_ncov), nullptr, cap, err, st)))
     return rc;
   // SG-CNN of the pocket alone (no ligand -> no non-covalent edges: every
   // node follows the message-free trajectory), dumping the post-covalent
@@ -964,8 +964,8 @@ int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch*
   FS_CUDA_CHECK(cudaMemsetAsync(err, 0, 4 * (size_t)P, st));
   if ((rc = launch_graph_fact(*b, d.cov_thresh, d.noncov_thresh, d.box_size, d.c_elem, S, max_edges, max_pocket_atoms,
                               cnt, aff, (float*)(W + w.feats), (int64_t*)(W + w.row_cov), (int32_t*)(W + w.deg_cov),
-                              (int32_t*)(W + w.col_cov), (int64_t*)(W + w.row_ncov), (int32_t*)(W + w.deg_ncov),
-                              (int32_t*)(W + w.col_ncov), err, st)))
+                              (col_t*)(W + w.col_cov), (int64_t*)(W + w.row_ncov), (int32_t*)(W + w.deg_ncov),
+                              (col_t*)(W + w.col_ncov), err, st)))
     return rc;
   mark_stage(ST_CONV1, st);
   if ((rc = launch_conv1_fact(*b, (const char*)cache, L.bytes, L.off_pp, L.off_ppact, L.off_wl, d.c_elem,
@@ -1030,11 +1030,11 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const d
     int64_t* cursor = (int64_t*)(W + w.cursor);
     const size_t scan_b = scan_ws_bytes(n_nodes > P ? n_nodes : P) + 1024;
     if ((rc = launch_csr_from_edges(cov_edges, n_cov, noff, P, n_nodes, node_pose, (int32_t*)(W + w.deg_cov),
-                                    (int64_t*)(W + w.row_cov), cursor, (int32_t*)(W + w.col_cov), W + w.scan, scan_b,
+                                    (int64_t*)(W + w.row_cov), cursor, (col_t*)(W + w.col_cov), W + w.scan, scan_b,
                                     st)))
       return rc;
     if ((rc = launch_csr_from_edges(ncov_edges, n_ncov, noff, P, n_nodes, node_pose, (int32_t*)(W + w.deg_ncov),
-                                    (int64_t*)(W + w.row_ncov), cursor, (int32_t*)(W + w.col_ncov), W + w.scan,
+                                    (int64_t*)(W + w.row_ncov), cursor, (col_t*)(W + w.col_ncov), W + w.scan,
                                     scan_b, st)))
       return rc;
     if ((rc = launch_f64_to_f32(feats, (float*)(W + w.feats), n_nodes * m->F, m->F, node_pose, err, st))) return rc;

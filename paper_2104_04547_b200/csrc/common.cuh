@@ -19,6 +19,10 @@ void set_cuda_error(cudaError_t e);
     if (_e != cudaSuccess) { ::fs::set_cuda_error(_e); return FS_ECUDA; } \
   } while (0)
 
+// Pose-local neighbour ids of the scoring-path CSR (FS_MAX_POSE_ATOMS < 2^16):
+// 16-bit halves the id traffic of the SG-CNN gathers.
+typedef uint16_t col_t;
+
 // Device-side index checks, compiled in only with -DFS_BOUNDS (FS_BOUNDS=1 build).
 #ifdef FS_BOUNDS
 #define FS_DCHECK(cond, what, v, lim)                                                                \

@@ -457,18 +457,18 @@ __global__ void edge_degree_kernel(const int64_t* edges, int64_t ne, int32_t* de
 }
 
 __global__ void edge_fill_kernel(const int64_t* edges, int64_t ne, const int64_t* node_off,
-                                 const int32_t* node_pose, int64_t* cursor, int32_t* col) {
+                                 const int32_t* node_pose, int64_t* cursor, col_t* col) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= ne) return;
   int64_t i = edges[2 * e], j = edges[2 * e + 1];
   int64_t oi = node_off[node_pose[i]], oj = node_off[node_pose[j]];
   unsigned long long si = atomicAdd((unsigned long long*)&cursor[i], 1ull);
   unsigned long long sj = atomicAdd((unsigned long long*)&cursor[j], 1ull);
-  col[si] = (int32_t)(j - oj);
-  col[sj] = (int32_t)(i - oi);
+  col[si] = (col_t)(j - oj);
+  col[sj] = (col_t)(i - oi);
 }
 
-__global__ void sort_rows_kernel(const int64_t* row_ptr, int64_t n, int32_t* col) {
+__global__ void sort_rows_kernel(const int64_t* row_ptr, int64_t n, col_t* col) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int64_t rb = row_ptr[r], re = row_ptr[r + 1];
@@ -603,7 +603,7 @@ int launch_edges(const int64_t* node_off, int n_poses, const int64_t* row_ptr, c
 // cursor [n+1] int64 scratch.
 int launch_csr_from_edges(const int64_t* edges, int64_t ne, const int64_t* node_off, int n_poses,
                           int64_t n_nodes, int32_t* node_pose, int32_t* deg, int64_t* row_ptr,
-                          int64_t* cursor, int32_t* col, void* ws, size_t ws_bytes, cudaStream_t st) {
+                          int64_t* cursor, col_t* col, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (n_nodes <= 0) return FS_OK;
   node_pose_kernel<<<n_poses, 256, 0, st>>>(node_off, n_poses, node_pose);
   FS_LAUNCH_CHECK();

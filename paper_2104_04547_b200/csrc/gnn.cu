@@ -19,8 +19,8 @@ namespace fs {
 struct GnnArgs {
   const float* feats; int F;            // [N][F]
   const int64_t* node_off;
-  const int64_t* row_cov; const int32_t* deg_cov; const int32_t* col_cov;     // row start + degree
-  const int64_t* row_ncov; const int32_t* deg_ncov; const int32_t* col_ncov;
+  const int64_t* row_cov; const int32_t* deg_cov; const col_t* col_cov;     // row start + degree
+  const int64_t* row_ncov; const int32_t* deg_ncov; const col_t* col_ncov;
   const float* we; const float* be;     // [F][D], [D]
   const float* phase[2];                // per phase: Wc[D][3D] | bc[3D] | U[D][2D] | Uh[D][D]
   const float* gg; const float* bg;     // [D][GN], [GN]
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
     const float* Uh = U + D * 2 * D;
     const int64_t* rows = ph == 0 ? a.row_cov : a.row_ncov;
     const int32_t* degs = ph == 0 ? a.deg_cov : a.deg_ncov;
-    const int32_t* cols = ph == 0 ? a.col_cov : a.col_ncov;
+    const col_t* cols = ph == 0 ? a.col_cov : a.col_ncov;
     for (int step = 0; step < a.k_steps[ph]; ++step) {
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
         // keep ptxas from hoisting the (loop-invariant) shared-memory weight

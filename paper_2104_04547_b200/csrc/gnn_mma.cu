@@ -17,6 +17,8 @@
 // Determinism: every row's sum has a fixed order (CSR order, or for heavy
 // rows 8 CSR-strided partial sums in a fixed tree), fixed reduction trees,
 // fixed pool order -> a pose's latent is bitwise independent of its batch.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace fs {
@@ -24,8 +26,8 @@ namespace fs {
 struct GnnMmaArgs {
   const float* feats; int F;
   const int64_t* node_off;
-  const int64_t* row_cov; const int32_t* deg_cov; const int32_t* col_cov;     // row start + degree
-  const int64_t* row_ncov; const int32_t* deg_ncov; const int32_t* col_ncov;
+  const int64_t* row_cov; const int32_t* deg_cov; const col_t* col_cov;     // row start + degree
+  const int64_t* row_ncov; const int32_t* deg_ncov; const col_t* col_ncov;
   const float* we; const float* be;       // [F][24], [24]
   const uint32_t* wfrag[2];               // per phase, see gnn_mma_phase_words()
   const float* wbias[2];                  // per phase [72] = bz | br | bh
@@ -51,7 +53,7 @@ struct GnnMmaArgs {
   float* dump_hcov; float* dump_f; int64_t dump_ld;
 };
 
-constexpr int kMmaWarps = 16;
+constexpr int kMaxMmaWarps = 24;   // smem reduction buffers are sized for this many warps
 constexpr int kZrWords = 3 * 6 * 64;      // [kt][nt][lane][2] per hi/lo
 constexpr int kHhWords = 3 * 3 * 64;
 constexpr int kPhaseWords = 2 * (kZrWords + kHhWords);   // hi and lo
@@ -155,7 +157,7 @@ __device__ __forceinline__ void acc_row(float (&a)[6], const float* __restrict__
   }
 }
 
-template <int SPLIT, bool FACT>
+template <int SPLIT, bool FACT, int kMmaWarps>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a) {
   extern __shared__ __align__(16) float sm[];
   const int p = blockIdx.x;
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     return;
   }
   const int ntiles = (n + 15) / 16, npad = ntiles * 16;
-  const int srows = max(npad + 1, 256);  // S doubles as the pool's reduction buffers (>= 6144 floats)
+  const int srows = max(npad + 1, kMaxMmaWarps * 16);  // S doubles as the pool's reduction buffers (3 x warps x 128 floats)
   // H: node states [npad + 1][24], row npad stays zero (padded gathers read it)
   // S: neighbour sums [srows][24], row npad is the sink of padded tile slots
   float* H = sm;
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     if (threadIdx.x < 2) CTL[threadIdx.x] = 0;
     const int64_t* rows = ph == 0 ? a.row_cov : a.row_ncov;
     const int32_t* degs = ph == 0 ? a.deg_cov : a.deg_ncov;
-    const int32_t* colv = ph == 0 ? a.col_cov : a.col_ncov;
+    const col_t* colv = ph == 0 ? a.col_cov : a.col_ncov;
     __syncthreads();
     // gather order: counting sort by degree, descending (bin 0 = heavy rows).
     // The order inside a bin is arbitrary: a row's sum never depends on
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           // one heavy row: lane (q = lane/4, t) sums neighbours q, q+8, ...
           const int row = PERM[item];
           const int d = degs[base + row];
-          const int32_t* c = colv + rows[base + row];
+          const col_t* c = colv + rows[base + row];
           float s6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
           for (int q = g; q < d; q += 32) {
             int j[4];
@@ -304,8 +306,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           const int k0 = nh + (item - nh) * 16 + g, k1 = k0 + 8;
           const int r0 = k0 < prow ? PERM[k0] : npad, r1 = k1 < prow ? PERM[k1] : npad;
           const int d0 = r0 < n ? degs[base + r0] : 0, d1 = r1 < n ? degs[base + r1] : 0;
-          const int32_t* c0 = colv + (r0 < n ? rows[base + r0] : 0);
-          const int32_t* c1 = colv + (r1 < n ? rows[base + r1] : 0);
+          const col_t* c0 = colv + (r0 < n ? rows[base + r0] : 0);
+          const col_t* c1 = colv + (r1 < n ? rows[base + r1] : 0);
           const int dm = max(d0, d1);
           float a0[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, a1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
           int q = 0;
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 
 size_t gnn_mma_smem_bytes(int max_nodes) {
   const int npad = (max_nodes + 15) / 16 * 16;
-  const int srows = npad + 1 > 256 ? npad + 1 : 256;
+  const int srows = npad + 1 > kMaxMmaWarps * 16 ? npad + 1 : kMaxMmaWarps * 16;
   return static_cast<size_t>(npad + 1 + srows) * 24 * 4 + kPhaseWords * 4 + 72 * 4 + kCtlWords * 4 +
          static_cast<size_t>(npad) * 2 + 64;
 }
@@ -545,21 +547,30 @@ int gnn_mma_max_nodes() {
   return n;
 }
 
-template <int SPLIT, bool FACT>
+template <int SPLIT, bool FACT, int WARPS>
 static int launch_gnn_mma_t(const GnnMmaArgs& a, int n_poses, size_t smem, cudaStream_t st) {
-  FS_CUDA_CHECK(cudaFuncSetAttribute(gnn_mma_kernel<SPLIT, FACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  FS_CUDA_CHECK(cudaFuncSetAttribute(gnn_mma_kernel<SPLIT, FACT, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-  gnn_mma_kernel<SPLIT, FACT><<<n_poses, kMmaWarps * 32, smem, st>>>(a);
+  gnn_mma_kernel<SPLIT, FACT, WARPS><<<n_poses, WARPS * 32, smem, st>>>(a);
   FS_LAUNCH_CHECK();
   return FS_OK;
+}
+
+// warps per pose (FS_GNN_WARPS = 16 | 20; more warps = fewer registers each)
+static int gnn_warps() {
+  static const int w = getenv("FS_GNN_WARPS") ? atoi(getenv("FS_GNN_WARPS")) : 16;
+  return w == 20 ? 20 : 16;
 }
 
 int launch_gnn_mma(const GnnMmaArgs& a, int split, int n_poses, int max_nodes, cudaStream_t st) {
   if (n_poses <= 0) return FS_OK;
   if (!gnn_mma_fits(max_nodes)) return FS_ECAPACITY;
   const size_t smem = gnn_mma_smem_bytes(max_nodes);
-  if (a.fact_cnt) return launch_gnn_mma_t<3, true>(a, n_poses, smem, st);
-  return split == 3 ? launch_gnn_mma_t<3, false>(a, n_poses, smem, st) : launch_gnn_mma_t<1, false>(a, n_poses, smem, st);
+  const int w = gnn_warps();
+  if (a.fact_cnt)
+    return w == 20 ? launch_gnn_mma_t<3, true, 20>(a, n_poses, smem, st) : launch_gnn_mma_t<3, true, 16>(a, n_poses, smem, st);
+  if (split != 3) return launch_gnn_mma_t<1, false, 16>(a, n_poses, smem, st);
+  return w == 20 ? launch_gnn_mma_t<3, false, 20>(a, n_poses, smem, st) : launch_gnn_mma_t<3, false, 16>(a, n_poses, smem, st);
 }
 
 }  // namespace fs

@@ -24,8 +24,8 @@ struct GraphCsrArgs {
   fs_pose_batch b;
   const int64_t* node_off;
   double tc, tn;
-  int64_t* row_cov; int32_t* deg_cov; int32_t* col_cov; double* dist_cov;
-  int64_t* row_ncov; int32_t* deg_ncov; int32_t* col_ncov; double* dist_ncov;
+  int64_t* row_cov; int32_t* deg_cov; col_t* col_cov; double* dist_cov;
+  int64_t* row_ncov; int32_t* deg_ncov; col_t* col_ncov; double* dist_ncov;
   int64_t cap;          // entries per pose per edge type
   int32_t* err;
   int smem_atoms;
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   }
 
   // ---- fill non-covalent rows (ascending neighbour id) ----
-  int32_t* coln = a.col_ncov + cbase;
+  col_t* coln = a.col_ncov + cbase;
   double* distn = DIST ? a.dist_ncov + cbase : nullptr;
   if (use_mask) {
     for (int si = warp; si < nS; si += kCsrWarps) {          // S rows: L ids ascending
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   // a cell) -- a pose's sums never depend on its batch.  Featurizer path
   // (distances, edge lists compared bitwise with the reference): rows are
   // insertion-sorted to ascending neighbour id. ----
-  int32_t* colc = a.col_cov + cbase;
+  col_t* colc = a.col_cov + cbase;
   double* distc = DIST ? a.dist_cov + cbase : nullptr;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int rb = offc[i];
@@ -433,8 +433,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
 }
 
 int launch_graph_csr(const fs_pose_batch& b, const int64_t* node_off, double tc, double tn, int64_t* row_cov,
-                     int32_t* deg_cov, int32_t* col_cov, double* dist_cov, int64_t* row_ncov, int32_t* deg_ncov,
-                     int32_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st) {
+                     int32_t* deg_cov, col_t* col_cov, double* dist_cov, int64_t* row_ncov, int32_t* deg_ncov,
+                     col_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st) {
   if (!(tc >= 1.2 && tc <= 5.9) || !(tn >= 1.2 && tn <= 5.9)) return FS_EINVAL;   // complexes.py:228-231
   if (b.n_poses <= 0) return FS_OK;
   GraphCsrArgs a;
@@ -475,8 +475,8 @@ struct GraphFactArgs {
   int c_elem;
   int64_t S, cap;
   int32_t* cnt; int32_t* aff; float* feats;
-  int64_t* row_cov; int32_t* deg_cov; int32_t* col_cov;
-  int64_t* row_ncov; int32_t* deg_ncov; int32_t* col_ncov;
+  int64_t* row_cov; int32_t* deg_cov; col_t* col_cov;
+  int64_t* row_ncov; int32_t* deg_ncov; col_t* col_ncov;
   int32_t* err;
   int max_pocket;
 };
@@ -617,8 +617,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
   if (threadIdx.x == 0) { a.cnt[2 * p] = nL; a.cnt[2 * p + 1] = nA; }
 
   // ---- fill: ligand rows (covalent: ligand ids; non-covalent: compact pocket ids) ----
-  int32_t* colc = a.col_cov + cb;
-  int32_t* coln = a.col_ncov + cb;
+  col_t* colc = a.col_cov + cb;
+  col_t* coln = a.col_ncov + cb;
   const unsigned below = (1u << lane) - 1u;
   for (int s = warp; s < nL; s += kCsrWarps) {
     double xi, yi, zi; int32_t e_, r_;
@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
 
 int launch_graph_fact(const fs_pose_batch& b, double tc, double tn, double box, int c_elem, int64_t S, int64_t cap,
                       int max_pocket, int32_t* cnt, int32_t* aff, float* feats, int64_t* row_cov, int32_t* deg_cov,
-                      int32_t* col_cov, int64_t* row_ncov, int32_t* deg_ncov, int32_t* col_ncov, int32_t* err,
+                      col_t* col_cov, int64_t* row_ncov, int32_t* deg_ncov, col_t* col_ncov, int32_t* err,
                       cudaStream_t st) {
   if (!(tc >= 1.2 && tc <= 5.9) || !(tn >= 1.2 && tn <= 5.9)) return FS_EINVAL;
   if (b.n_poses <= 0) return FS_OK;
