@@ -35,11 +35,13 @@ constexpr int kCsrThreads = 256;
 constexpr int kCsrWarps = kCsrThreads / 32;
 constexpr int kCellsAxis = 9;           // cells grow past t_cov for boxes > 9*t_cov
 constexpr int kMaskWords = 2;         // bipartite bitmask path for |S| <= 64
+constexpr int kCovBits = 96;          // covalent candidates per row whose hit bits are kept (3 CTAs/SM)
 
 __host__ __device__ inline size_t graph_csr_smem_bytes(int n) {
   n = (n + 3) & ~3;   // keeps every sub-array 16-byte aligned
   const size_t cells = 2 * kCellsAxis * kCellsAxis * kCellsAxis + 2;
-  return (size_t)n * 16 + (size_t)n * 4 * 4 + (size_t)(n + 1) * 4 * 2 + (size_t)n * kMaskWords * 4 + cells * 4 + 512;
+  return (size_t)n * 16 + (size_t)n * 4 * 4 + (size_t)(n + 1) * 4 * 2 + (size_t)n * kMaskWords * 4 + cells * 4 +
+         (size_t)n * (kCovBits / 32 + 1) * 4 + 512;
 }
 
 // in-place exclusive scan of a[0..n) (n+1-th entry receives the total).
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   int* offn = offc + SA + 1;            // [n+1]
   uint32_t* mask = reinterpret_cast<uint32_t*>(offn + SA + 1);   // [|L|][kMaskWords]
   int* cell_start = reinterpret_cast<int*>(mask + (size_t)SA * kMaskWords);
+  uint32_t* covbits = reinterpret_cast<uint32_t*>(cell_start + 2 * kCellsAxis * kCellsAxis * kCellsAxis + 2);
   __syncthreads();
 
   // ---- atoms, validation, bounding box ----
@@ -155,7 +158,9 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   if (s_flags) { fail(s_flags); return; }
   if (n == 0) return;
   const bool prefilter = absmax < 1024.0;            // fp32 coordinate error <= 6.1e-5 A
-  const double cs = fmax(a.tc * 1.0001, ext_max / (kCellsAxis - 1));
+  // cells >= 1.001 t_cov: the fp32 cell index below (coordinate error
+  // <= 6.1e-5 A when |x| < 1024) cannot separate a covalent pair by two cells
+  const double cs = fmax(a.tc * 1.001, ext_max / (kCellsAxis - 1));
   const int nca = min(kCellsAxis, (int)floor(ext_max / cs) + 1);
   const int NC = nca * nca * nca;
   for (int i = threadIdx.x; i < 2 * NC + 1; i += blockDim.x) cell_start[i] = 0;
@@ -164,12 +169,25 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     int c = (int)floor(__ddiv_rn(__dsub_rn(x, s_min[ax]), cs));
     return min(max(c, 0), nca - 1);
   };
+  const float inv_cs = (float)(1.0 / cs);
+  const float fmin_x = (float)s_min[0], fmin_y = (float)s_min[1], fmin_z = (float)s_min[2];
+  auto cell_coord_f = [&](float x, float m) -> int {
+    const int c = (int)floorf((x - m) * inv_cs);
+    return min(max(c, 0), nca - 1);
+  };
 
   // ---- counting sort by (role, cell); role lists ascending by id ----
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double x, y, z; int32_t e, r;
-    pv.atom(i, x, y, z, e, r);
-    const int key = r * NC + (cell_coord(x, 0) * nca + cell_coord(y, 1)) * nca + cell_coord(z, 2);
+    const float4 f = pf[i];
+    const int r = (int)f.w;
+    int key;
+    if (prefilter) {
+      key = r * NC + (cell_coord_f(f.x, fmin_x) * nca + cell_coord_f(f.y, fmin_y)) * nca + cell_coord_f(f.z, fmin_z);
+    } else {
+      double x, y, z; int32_t e, rr;
+      pv.atom(i, x, y, z, e, rr);
+      key = r * NC + (cell_coord(x, 0) * nca + cell_coord(y, 1)) * nca + cell_coord(z, 2);
+    }
     keys[i] = key;
     atomicAdd(&cell_start[key], 1);
   }
@@ -292,7 +310,31 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     }
   }
 
-  // ---- covalent degrees: 27-cell stencil, one thread per row ----
+  // ---- covalent degrees: 27-cell stencil, one thread per row.  visit(j, c)
+  // sees every candidate j != i with its running candidate index c. ----
+  auto cov_cand = [&](int i, auto&& visit) {
+    const int ri = (int)pf[i].w;
+    const int key = keys[i] - ri * NC;
+    const int cz = key % nca, cy = (key / nca) % nca, cx = key / (nca * nca);
+    int c = 0;
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int ax = cx + dx;
+      if (ax < 0 || ax >= nca) continue;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int ay = cy + dy;
+        if (ay < 0 || ay >= nca) continue;
+        const int z0 = max(cz - 1, 0), z1 = min(cz + 1, nca - 1);
+        const int k0 = ri * NC + (ax * nca + ay) * nca + z0, k1 = ri * NC + (ax * nca + ay) * nca + z1;
+        const int qb = k0 == 0 ? 0 : cell_start[k0 - 1], qe = cell_start[k1];
+        for (int q = qb; q < qe; ++q) {
+          const int j = cell_list[q];
+          if (j == i) continue;
+          visit(j, c++);
+        }
+      }
+    }
+    return c;
+  };
   auto cov_scan = [&](int i, auto&& emit) {
     double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
     const float4 fi = pf[i];
@@ -319,10 +361,27 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       }
     }
   };
+  // count pass: the hit pattern over the first kCovBits candidates is kept
+  // (covbits) so the fill pass emits without re-testing distances
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    int c = 0;
-    cov_scan(i, [&](int) { ++c; });
-    offc[i] = c;
+    double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
+    const float4 fi = pf[i];
+    int cnt = 0;
+    uint32_t word = 0u;
+    uint32_t* bits = covbits + (size_t)i * (kCovBits / 32 + 1);
+    const int ncand = cov_cand(i, [&](int j, int c) {
+      const float4 fj = pf[j];
+      const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
+      const bool hit = decide(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, xi, yi, zi, j, a.tc);
+      cnt += hit;
+      if (c < kCovBits) {
+        word |= (uint32_t)hit << (c & 31);
+        if ((c & 31) == 31) { bits[c >> 5] = word; word = 0u; }
+      }
+    });
+    if (ncand < kCovBits && (ncand & 31)) bits[ncand >> 5] = word;
+    bits[kCovBits / 32] = (uint32_t)ncand;
+    offc[i] = cnt;
   }
   __syncthreads();
   // ---- degrees -> pose-local offsets, capacity check, row pointers ----
@@ -407,6 +466,15 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int rb = offc[i];
     int o = rb;
+    const uint32_t* bits = covbits + (size_t)i * (kCovBits / 32 + 1);
+    if (!DIST && bits[kCovBits / 32] <= (uint32_t)kCovBits) {
+      uint32_t word = 0u;
+      cov_cand(i, [&](int j, int c) {
+        if ((c & 31) == 0) word = bits[c >> 5];
+        if ((word >> (c & 31)) & 1u) colc[o++] = (col_t)j;
+      });
+      continue;
+    }
     cov_scan(i, [&](int j) {
       colc[o] = j;
       if (DIST) {
