@@ -194,6 +194,10 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    # keep stdout to the one JSON line: the image sets NCCL_DEBUG=VERSION, and
+    # NCCL prints its version banner to stdout at that level (and at WARN)
+    if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "NONE"
     import torch
     import torch.distributed as dist
     from paper_2104_04547_b200 import _native as N
