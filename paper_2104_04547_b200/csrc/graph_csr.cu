@@ -363,7 +363,10 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   };
   // count pass: the hit pattern over the first kCovBits candidates is kept
   // (covbits) so the fill pass emits without re-testing distances
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  // rows are taken in cell order: a warp's rows share their stencil cells
+  // (same trip counts, broadcast candidate reads)
+  for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+    const int i = cell_list[idx];
     double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
     const float4 fi = pf[i];
     int cnt = 0;
@@ -463,16 +466,50 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   // insertion-sorted to ascending neighbour id. ----
   col_t* colc = a.col_cov + cbase;
   double* distc = DIST ? a.dist_cov + cbase : nullptr;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+    const int i = cell_list[idx];
     const int rb = offc[i];
     int o = rb;
     const uint32_t* bits = covbits + (size_t)i * (kCovBits / 32 + 1);
     if (!DIST && bits[kCovBits / 32] <= (uint32_t)kCovBits) {
-      uint32_t word = 0u;
-      cov_cand(i, [&](int j, int c) {
-        if ((c & 31) == 0) word = bits[c >> 5];
-        if ((word >> (c & 31)) & 1u) colc[o++] = (col_t)j;
-      });
+      // replay the count pass's hits: candidate index c of a stencil column
+      // run maps to cell_list[qb + c - c0] (the row's own atom, skipped by
+      // the count pass, only sits in its own column, which is walked)
+      const int ri = (int)pf[i].w;
+      const int key = keys[i] - ri * NC;
+      const int cz = key % nca, cy = (key / nca) % nca, cx = key / (nca * nca);
+      int c0 = 0;
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int ax = cx + dx;
+        if (ax < 0 || ax >= nca) continue;
+        for (int dy = -1; dy <= 1; ++dy) {
+          const int ay = cy + dy;
+          if (ay < 0 || ay >= nca) continue;
+          const int z0 = max(cz - 1, 0), z1 = min(cz + 1, nca - 1);
+          const int k0 = ri * NC + (ax * nca + ay) * nca + z0, k1 = ri * NC + (ax * nca + ay) * nca + z1;
+          const int qb = k0 == 0 ? 0 : cell_start[k0 - 1], qe = cell_start[k1];
+          if (dx == 0 && dy == 0) {
+            for (int q = qb; q < qe; ++q) {
+              const int j = cell_list[q];
+              if (j == i) continue;
+              if ((bits[c0 >> 5] >> (c0 & 31)) & 1u) colc[o++] = (col_t)j;
+              ++c0;
+            }
+          } else {
+            const int cend = c0 + (qe - qb);
+            int c = c0;
+            while (c < cend) {
+              const uint32_t w = bits[c >> 5] >> (c & 31);
+              if (w == 0u) { c += 32 - (c & 31); continue; }
+              c += __ffs(w) - 1;
+              if (c >= cend) break;
+              colc[o++] = (col_t)cell_list[qb + (c - c0)];
+              ++c;
+            }
+            c0 = cend;
+          }
+        }
+      }
       continue;
     }
     cov_scan(i, [&](int j) {

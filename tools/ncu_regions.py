@@ -11,6 +11,7 @@ import sys
 
 
 MIN_LINE = 0
+SKIP = []          # (lo, hi) line ranges of inlined helpers: charged to their caller
 
 
 def main(path, fname, specs):
@@ -53,7 +54,7 @@ def main(path, fname, specs):
     acc["other"] = [0.0, 0.0, {}]
     last = None
     for addr, f, ln, i, s, rs in sass:
-        if f == fname and ln >= MIN_LINE:
+        if f == fname and ln >= MIN_LINE and not any(lo <= ln <= hi for lo, hi in SKIP):
             last = ln
         reg = "other"
         if last is not None:
@@ -73,6 +74,11 @@ def main(path, fname, specs):
 
 if __name__ == "__main__":
     args = sys.argv[1:]
-    if args[0].startswith("--min-line="):
-        MIN_LINE = int(args.pop(0).split("=")[1])
+    while args[0].startswith("--"):
+        opt = args.pop(0)
+        if opt.startswith("--min-line="):
+            MIN_LINE = int(opt.split("=")[1])
+        elif opt.startswith("--skip="):
+            lo, hi = opt.split("=")[1].split("-")
+            SKIP.append((int(lo), int(hi)))
     main(args[0], args[1], args[2:])
