@@ -427,6 +427,21 @@ def main():
             flop = (VOXEL_FLOP + graph_flop(n_mean, 5152, 9094)) * B
             roof = {"kernel": dom_name, "bound": "tensor", "achieved": flop / (avg_ms / 1e3) / 1e12,
                     "peak": bf16_sus, "unit": "TFLOP/s", "traffic": None}
+        # DRAM traffic of the dominant kernel: dram__bytes_read+write per pose
+        # from the committed ncu --set full capture, scaled to this launch
+        tr_key = {"gnn": "gnn_mma_kernel<3, 0, 16>" if precision == "bf16" else None,
+                  "conv1": "conv_umma_kernel<Cfg<16, 8, 32, 5, 1, 0, 0, 0, 1>>",
+                  "conv2": "conv_umma_kernel<Cfg<16, 32, 32, 3, 1, 1, 0, 0, 1>>",
+                  "featurize": "graph_csr_kernel<0>"}.get(dom_name)
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")))
+            if tr_key in tr:
+                roof["traffic"] = tr[tr_key]["bytes_per_pose"] * B
+                roof["traffic_unit"] = "bytes per launch"
+                roof["traffic_source"] = ("profiles/r01/ncu_traffic.json: ncu --set full dram__bytes_read.sum + "
+                                          "dram__bytes_write.sum of a 2048-pose launch, scaled per pose")
+        except (OSError, ValueError):
+            pass
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["peak_kind"] = f"{peak_kind} bf16 sustained"
         roof["stage_ms_per_step"] = {n: round(v / K, 4) for n, v in zip(names, stage_ms)}

@@ -115,12 +115,10 @@ template <int SPLIT, int NT>
 __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[3][4], const uint32_t (&alo)[3][4],
                                        const uint32_t* __restrict__ fhi, const uint32_t* __restrict__ flo,
                                        int lane) {
-  float C[NT][4];   // small cross terms accumulate separately: independent MMA chains
+  // small cross terms first, the hi.hi product last, all into one
+  // accumulator: NT independent chains keep the tensor pipe busy
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    D[nt][0] = D[nt][1] = D[nt][2] = D[nt][3] = 0.f;
-    C[nt][0] = C[nt][1] = C[nt][2] = C[nt][3] = 0.f;
-  }
+  for (int nt = 0; nt < NT; ++nt) D[nt][0] = D[nt][1] = D[nt][2] = D[nt][3] = 0.f;
 #pragma unroll
   for (int kt = 0; kt < 3; ++kt)
 #pragma unroll
@@ -128,17 +126,11 @@ __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[
       const uint2 bh = *reinterpret_cast<const uint2*>(fhi + ((kt * NT + nt) * 32 + lane) * 2);
       if (SPLIT == 3) {
         const uint2 bl = *reinterpret_cast<const uint2*>(flo + ((kt * NT + nt) * 32 + lane) * 2);
-        mma_bf16(C[nt], alo[kt], bh.x, bh.y);
-        mma_bf16(C[nt], ahi[kt], bl.x, bl.y);
+        mma_bf16(D[nt], alo[kt], bh.x, bh.y);
+        mma_bf16(D[nt], ahi[kt], bl.x, bl.y);
       }
       mma_bf16(D[nt], ahi[kt], bh.x, bh.y);
     }
-  if (SPLIT == 3) {
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) D[nt][q] += C[nt][q];
-  }
 }
 
 // Rows with at least kHeavyDeg neighbours are summed by a whole warp (8
