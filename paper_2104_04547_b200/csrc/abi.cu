@@ -491,6 +491,37 @@ static WsPlan plan_ws(const fs_model& m, int64_t P, int64_t N, int64_t E, int pr
   return w;
 }
 
+// ---- graph/voxel branch overlap ---------------------------------------------
+// The radius graph (graph head input) and the voxel head are independent until
+// the SG-CNN: with FS_OVERLAP=1 the graph kernels run on a library-owned side
+// stream forked from and joined back into the caller's stream (per device and
+// host thread, so concurrent callers stay independent).  Off by default: the
+// persistent tcgen05 conv kernels lose more to the co-resident graph CTAs
+// (conv1 5.3 -> 6.6 ms, conv2 6.0 -> 12.6 ms per 16,384 poses) than the
+// overlap hides (measured: 58.4 vs 58.2 ms per step).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+static SideStream* side_stream() {
+  static const bool off = getenv("FS_OVERLAP") == nullptr;
+  if (off) return nullptr;
+  static thread_local std::map<int, SideStream> streams;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  SideStream& ss = streams[dev];
+  if (!ss.s) {
+    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+      ss = SideStream{};
+      return nullptr;
+    }
+  }
+  return &ss;
+}
+
 // ---- pocket cache (fs_pocket_prepare / fs_score_poses_cached) --------------
 struct PocketCacheLayout {
   int64_t off_n, off_T, off_pp, off_ppact, off_wl, off_hcov, off_f, bytes;
@@ -824,14 +855,23 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   if ((rc = launch_node_offsets(*b, node_off, W + w.scan, scan_ws_bytes(N > P ? N : P) + 1024, st))) return rc;
   const fs_model_desc& d = m->d;
   const bool late = d.fusion_mode == FS_MODE_LATE;
+  // graph branch (node features + radius graph) on the side stream
+  SideStream* ss = side_stream();
+  cudaStream_t gst = st;
+  if (ss) {
+    FS_CUDA_CHECK(cudaEventRecord(ss->fork, st));
+    FS_CUDA_CHECK(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+    gst = ss->s;
+  }
   // featurize (models.py:638-651)
-  if ((rc = launch_node_features(*b, node_off, d.c_elem, d.box_size, W + w.feats, false, st))) return rc;
+  if ((rc = launch_node_features(*b, node_off, d.c_elem, d.box_size, W + w.feats, false, gst))) return rc;
   // radius graph: one fused launch, pose-private CSR slices of max_edges
   // entries per edge type (rows = start offset + degree)
   if ((rc = launch_graph_csr(*b, node_off, d.cov_thresh, d.noncov_thresh, (int64_t*)(W + w.row_cov),
                              (int32_t*)(W + w.deg_cov), (col_t*)(W + w.col_cov), nullptr, (int64_t*)(W + w.row_ncov),
-                             (int32_t*)(W + w.deg_ncov), (col_t*)(W + w.col_ncov), nullptr, max_edges, err, st)))
+                             (int32_t*)(W + w.deg_ncov), (col_t*)(W + w.col_ncov), nullptr, max_edges, err, gst)))
     return rc;
+  if (ss) FS_CUDA_CHECK(cudaEventRecord(ss->join, gst));
   if (precision == FS_PREC_BF16) {
     if ((rc = launch_voxelize(*b, d.grid_extent, m->cgrid, d.box_size, FS_GRID_NDHWC_BF16, W + w.grid, err, st))) return rc;
     if ((rc = umma::voxel_convs(d, (const char*)m->blob + m->umma_off, m->P(m->c1b), m->P(m->c2b),
@@ -843,6 +883,7 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
     if ((rc = voxel_head_fp32(*m, P, W, w, st))) return rc;
   }
   if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st))) return rc;
+  if (ss) FS_CUDA_CHECK(cudaStreamWaitEvent(st, ss->join, 0));
   if ((rc = graph_head(*m, P, max_atoms, W, w, err, late || pred_g, precision, st))) return rc;
   if (!late && (rc = fusion_head(*m, P, W, w, scores, st))) return rc;
   if ((rc = launch_finalize(P, d.fusion_mode, (float*)(W + w.pv), (float*)(W + w.pg), scores, err, st))) return rc;
@@ -962,11 +1003,19 @@ int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch*
   int rc;
   mark_stage(ST_FEATURIZE, st);
   FS_CUDA_CHECK(cudaMemsetAsync(err, 0, 4 * (size_t)P, st));
+  SideStream* ss = side_stream();
+  cudaStream_t gst = st;
+  if (ss) {
+    FS_CUDA_CHECK(cudaEventRecord(ss->fork, st));
+    FS_CUDA_CHECK(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+    gst = ss->s;
+  }
   if ((rc = launch_graph_fact(*b, d.cov_thresh, d.noncov_thresh, d.box_size, d.c_elem, S, max_edges, max_pocket_atoms,
                               cnt, aff, (float*)(W + w.feats), (int64_t*)(W + w.row_cov), (int32_t*)(W + w.deg_cov),
                               (col_t*)(W + w.col_cov), (int64_t*)(W + w.row_ncov), (int32_t*)(W + w.deg_ncov),
-                              (col_t*)(W + w.col_ncov), err, st)))
+                              (col_t*)(W + w.col_ncov), err, gst)))
     return rc;
+  if (ss) FS_CUDA_CHECK(cudaEventRecord(ss->join, gst));
   mark_stage(ST_CONV1, st);
   if ((rc = launch_conv1_fact(*b, (const char*)cache, L.bytes, L.off_pp, L.off_ppact, L.off_wl, d.c_elem,
                               d.box_size, umma::act1_ptr(W + w.umma), st)))
@@ -975,6 +1024,7 @@ int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch*
                                     P, W + w.umma, (float*)(W + w.p2), st)))
     return rc;
   if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st))) return rc;
+  if (ss) FS_CUDA_CHECK(cudaStreamWaitEvent(st, ss->join, 0));
   GnnMmaArgs x{};
   x.fact_cnt = cnt; x.fact_stride = S; x.fact_aff = aff; x.pose_target = b->pose_target;
   x.cache = (const char*)cache; x.cache_stride = L.bytes;
