@@ -87,6 +87,15 @@ __device__ __forceinline__ bool exact_edge(const PoseView& pv, double xi, double
   return true;
 }
 
+// Out-of-line copy for the in-band case of the fp32 decision: keeps the fp64
+// code out of the hot candidate loops (inlined, it would be predicated into
+// every iteration).
+__device__ __noinline__ bool exact_edge_slow(PoseView pv, double xi, double yi, double zi, int j, double rmax2,
+                                             double t) {
+  double d;
+  return exact_edge(pv, xi, yi, zi, j, rmax2, t, &d);
+}
+
 template <bool DIST>
 __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -369,21 +378,49 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     const int i = cell_list[idx];
     double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
     const float4 fi = pf[i];
-    int cnt = 0;
-    uint32_t word = 0u;
-    uint32_t* bits = covbits + (size_t)i * (kCovBits / 32 + 1);
-    const int ncand = cov_cand(i, [&](int j, int c) {
-      const float4 fj = pf[j];
-      const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
-      const bool hit = decide(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, xi, yi, zi, j, a.tc);
-      cnt += hit;
-      if (c < kCovBits) {
-        word |= (uint32_t)hit << (c & 31);
-        if ((c & 31) == 31) { bits[c >> 5] = word; word = 0u; }
+    int cnt = 0, c0 = 0;
+    bool over = false;
+    uint32_t w0 = 0u, w1 = 0u, w2 = 0u;   // hit bits of candidates 0..95
+    const int ri = (int)fi.w;
+    const int key = keys[i] - ri * NC;
+    const int cz = key % nca, cy = (key / nca) % nca, cx = key / (nca * nca);
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int ax = cx + dx;
+      if (ax < 0 || ax >= nca) continue;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int ay = cy + dy;
+        if (ay < 0 || ay >= nca) continue;
+        const int z0 = max(cz - 1, 0), z1 = min(cz + 1, nca - 1);
+        const int k0 = ri * NC + (ax * nca + ay) * nca + z0, k1 = ri * NC + (ax * nca + ay) * nca + z1;
+        const int qb = k0 == 0 ? 0 : cell_start[k0 - 1], qe = cell_start[k1];
+        // one stencil column: hits collected run-locally, merged once
+        uint64_t rm = 0ull;
+        int len = 0;
+        for (int q = qb; q < qe; ++q) {
+          const int j = cell_list[q];
+          if (j == i) continue;
+          const float4 fj = pf[j];
+          const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
+          const bool hit = decide(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, xi, yi, zi, j, a.tc);
+          if (len < 64) rm |= (uint64_t)hit << len;
+          else { over = true; cnt += hit; }
+          ++len;
+        }
+        cnt += __popcll(rm);
+        if (c0 < kCovBits) {
+          const int sh = c0 & 31;
+          const uint64_t x = rm << sh;
+          const uint32_t p0 = (uint32_t)x, p1 = (uint32_t)(x >> 32), p2 = sh ? (uint32_t)(rm >> (64 - sh)) : 0u;
+          if (c0 < 32) { w0 |= p0; w1 |= p1; w2 |= p2; }
+          else if (c0 < 64) { w1 |= p0; w2 |= p1; }
+          else { w2 |= p0; }
+        }
+        c0 += len;
       }
-    });
-    if (ncand < kCovBits && (ncand & 31)) bits[ncand >> 5] = word;
-    bits[kCovBits / 32] = (uint32_t)ncand;
+    }
+    uint32_t* bits = covbits + (size_t)i * (kCovBits / 32 + 1);
+    bits[0] = w0; bits[1] = w1; bits[2] = w2;
+    bits[kCovBits / 32] = over ? 0xffffffffu : (uint32_t)c0;   // > kCovBits: the fill re-tests
     offc[i] = cnt;
   }
   __syncthreads();
@@ -600,8 +637,7 @@ __device__ __forceinline__ bool fact_decide(const PoseView& pv, bool prefilter, 
     if (d2f > hi2) return false;
     if (d2f <= lo2) return true;
   }
-  double d;
-  return exact_edge(pv, xi, yi, zi, j, rmax2, t, &d);
+  return exact_edge_slow(pv, xi, yi, zi, j, rmax2, t);
 }
 
 __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a) {
