@@ -41,20 +41,28 @@ constexpr int kC1Threads = 256;
 __global__ void __launch_bounds__(kC1Threads) conv1_fact_kernel(Conv1FactArgs a) {
   extern __shared__ __align__(16) float wl[];           // [k^3][c_elem][32]
   __shared__ int4 atoms[kC1MaxLig];                      // (ix, iy, iz, ligand channel)
+  __shared__ uint32_t near_hw[kC1G * kC1G][kC1MaxLig / 32];   // atoms whose 5x5 (h, w) window covers the column
+  __shared__ uint32_t near_d[kC1G][kC1MaxLig / 32];            // atoms whose 5-plane d window covers the plane
   __shared__ uint32_t touched[kC1G3 / 32];
   __shared__ int s_cnt;
   __shared__ uint16_t tlist[kC1G3];
   const int nw = kC1K * kC1K * kC1K * a.c_elem * kC1Out;
   const char* c0 = a.cache;   // the weights are identical in every pocket slot
-  for (int i = threadIdx.x; i < nw / 4; i += blockDim.x)
-    reinterpret_cast<float4*>(wl)[i] = reinterpret_cast<const float4*>(c0 + a.off_wl)[i];
+  // weight row R (32 floats = 8 float4) is stored with its float4 q at slot
+  // (q + R) & 7: the lanes of a warp read different rows, which would all
+  // hit the same 4 banks unswizzled (128-byte row stride)
+  for (int i = threadIdx.x; i < nw / 4; i += blockDim.x) {
+    const int row = i >> 3, q = i & 7;
+    reinterpret_cast<float4*>(wl)[row * 8 + ((q + row) & 7)] = reinterpret_cast<const float4*>(c0 + a.off_wl)[i];
+  }
   const double half = a.box / 2.0, gd = kC1G;
   for (int p = blockIdx.x; p < a.b.n_poses; p += gridDim.x) {
     const PoseView pv = pose_view(a.b, p);
     const int nL = (int)pv.na;
     if (nL > kC1MaxLig || pv.np_ == 0) continue;         // not factorable (flagged by graph_fact_kernel)
     __syncthreads();                                     // previous pose done with atoms/touched/tlist
-    for (int i = threadIdx.x; i < kC1G3 / 32; i += blockDim.x) touched[i] = 0u;
+    for (int i = threadIdx.x; i < kC1G * kC1G * (kC1MaxLig / 32); i += blockDim.x) (&near_hw[0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < kC1G * (kC1MaxLig / 32); i += blockDim.x) (&near_d[0][0])[i] = 0u;
     if (threadIdx.x == 0) s_cnt = 0;
     for (int s = threadIdx.x; s < nL; s += blockDim.x) {
       double x, y, z; int32_t e, r;
@@ -69,24 +77,55 @@ __global__ void __launch_bounds__(kC1Threads) conv1_fact_kernel(Conv1FactArgs a)
       atoms[s] = make_int4(ax(x), ax(y), ax(z), min(max(e, 0), a.c_elem - 1));
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nL * 125; i += blockDim.x) {
-      const int4 at = atoms[i / 125];
-      const int k = i % 125;
-      const int d = at.x + k / 25 - kC1R, h = at.y + (k / 5) % 5 - kC1R, w = at.z + k % 5 - kC1R;
-      if (d < 0 || d >= kC1G || h < 0 || h >= kC1G || w < 0 || w >= kC1G) continue;
-      const int v = (d * kC1G + h) * kC1G + w;
-      atomicOr(&touched[v >> 5], 1u << (v & 31));
+    for (int i = threadIdx.x; i < nL * 30; i += blockDim.x) {
+      const int sidx = i / 30, k = i % 30;
+      const int4 at = atoms[sidx];
+      const uint32_t bit = 1u << (sidx & 31);
+      if (k < 25) {
+        const int h = at.y + k / 5 - kC1R, w = at.z + k % 5 - kC1R;
+        if (h >= 0 && h < kC1G && w >= 0 && w < kC1G) atomicOr(&near_hw[h * kC1G + w][sidx >> 5], bit);
+      } else {
+        const int d = at.x + (k - 25) - kC1R;
+        if (d >= 0 && d < kC1G) atomicOr(&near_d[d][sidx >> 5], bit);
+      }
     }
     __syncthreads();
     const char* pc = a.cache + static_cast<int64_t>(a.b.pose_target[p]) * a.cache_stride;
     const uint4* ppact = reinterpret_cast<const uint4*>(pc + a.off_ppact);
     uint4* op = reinterpret_cast<uint4*>(a.out) + static_cast<int64_t>(p) * (kC1Out / 8) * kC1G3;
     // untouched voxels: copy; touched ones: list them
-    for (int u = threadIdx.x; u < (kC1Out / 8) * kC1G3; u += blockDim.x) {
-      const int v = u & (kC1G3 - 1);
-      const bool t = (touched[v >> 5] >> (v & 31)) & 1u;
-      if (!t) op[u] = __ldg(ppact + u);
-      else if (u < kC1G3) tlist[atomicAdd(&s_cnt, 1)] = static_cast<uint16_t>(v);
+    // touched-voxel bitmask, then the copy of the untouched ones with 4
+    // independent 16-byte loads in flight per thread
+    for (int vw = threadIdx.x; vw < kC1G3 / 32; vw += blockDim.x) {
+      uint32_t m = 0u;
+      for (int b = 0; b < 32; ++b) {
+        const int v = 32 * vw + b;
+        uint32_t any = 0u;
+#pragma unroll
+        for (int wd = 0; wd < kC1MaxLig / 32; ++wd) any |= near_hw[v & 255][wd] & near_d[v >> 8][wd];
+        m |= (any ? 1u : 0u) << b;
+      }
+      touched[vw] = m;
+    }
+    __syncthreads();
+    constexpr int kUnits = (kC1Out / 8) * kC1G3;
+    for (int u0 = threadIdx.x; u0 < kUnits; u0 += 4 * kC1Threads) {
+      uint4 x[4];
+      bool t[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int u = u0 + r * kC1Threads;
+        const int v = u & (kC1G3 - 1);
+        t[r] = u >= kUnits || ((touched[v >> 5] >> (v & 31)) & 1u);
+        if (!t[r]) x[r] = __ldg(ppact + u);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int u = u0 + r * kC1Threads;
+        if (u >= kUnits) continue;
+        if (!t[r]) op[u] = x[r];
+        else if (u < kC1G3) tlist[atomicAdd(&s_cnt, 1)] = static_cast<uint16_t>(u);
+      }
     }
     __syncthreads();
     const float* pp = reinterpret_cast<const float*>(pc + a.off_pp);
@@ -101,17 +140,23 @@ __global__ void __launch_bounds__(kC1Threads) conv1_fact_kernel(Conv1FactArgs a)
         const float4 x = __ldg(src + q);
         acc[4 * q] = x.x; acc[4 * q + 1] = x.y; acc[4 * q + 2] = x.z; acc[4 * q + 3] = x.w;
       }
-      // out[o] += W[v_atom - o + r] (cross-correlation, 'same'), atom order
-      for (int s = 0; s < nL; ++s) {
-        const int4 at = atoms[s];
-        const int kd = at.x - d + kC1R, kh = at.y - h + kC1R, kw = at.z - w + kC1R;
-        if ((unsigned)kd >= kC1K || (unsigned)kh >= kC1K || (unsigned)kw >= kC1K) continue;
-        const int k = (kd * kC1K + kh) * kC1K + kw;
-        const float4* wk = reinterpret_cast<const float4*>(wl + (k * a.c_elem + at.w) * kC1Out);
+      // out[o] += W[v_atom - o + r] (cross-correlation, 'same'), in atom
+      // order over exactly the atoms whose window covers this voxel
 #pragma unroll
-        for (int q = 0; q < kC1Out / 4; ++q) {
-          const float4 x = wk[q];
-          acc[4 * q] += x.x; acc[4 * q + 1] += x.y; acc[4 * q + 2] += x.z; acc[4 * q + 3] += x.w;
+      for (int wd = 0; wd < kC1MaxLig / 32; ++wd) {
+        uint32_t bits = near_hw[v & 255][wd] & near_d[d][wd];
+        while (bits) {
+          const int sidx = 32 * wd + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int4 at = atoms[sidx];
+          const int k = ((at.x - d + kC1R) * kC1K + (at.y - h + kC1R)) * kC1K + (at.z - w + kC1R);
+          const int row = k * a.c_elem + at.w;
+          const float4* wk = reinterpret_cast<const float4*>(wl) + row * 8;
+#pragma unroll
+          for (int q = 0; q < kC1Out / 4; ++q) {
+            const float4 x = wk[(q + row) & 7];
+            acc[4 * q] += x.x; acc[4 * q + 1] += x.y; acc[4 * q + 2] += x.z; acc[4 * q + 3] += x.w;
+          }
         }
       }
 #pragma unroll
