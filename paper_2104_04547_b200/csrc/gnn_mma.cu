@@ -70,6 +70,13 @@ __device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void mma_bf16_k8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo_idx, float hi_idx) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo_idx, hi_idx);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -441,26 +448,39 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     put_a<SPLIT>(ahi[0], alo[0], 3, h[1][2], h[1][3]);
     put_a<SPLIT>(ahi[1], alo[1], 0, h[0][4], h[0][5]);
     put_a<SPLIT>(ahi[1], alo[1], 1, h[1][4], h[1][5]);
-    put_a<SPLIT>(ahi[1], alo[1], 2, 0.f, 0.f);
-    put_a<SPLIT>(ahi[1], alo[1], 3, 0.f, 0.f);
     const bool v0 = valid(tile * 16 + g), v1 = valid(tile * 16 + g + 8);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       float Dg[4] = {0.f, 0.f, 0.f, 0.f}, Dv[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int kt = 0; kt < 2; ++kt) {
-        const uint2 bgh = *reinterpret_cast<const uint2*>(g_hi + ((kt * 32 + j) * 32 + lane) * 2);
-        const uint2 bvh = *reinterpret_cast<const uint2*>(g_hi + ((kt * 32 + 16 + j) * 32 + lane) * 2);
+      // k 0..15: m16n8k16; k 16..23: m16n8k8 (the k16 fragments' first
+      // registers; rows 24..31 are zero padding)
+      {
+        const uint2 bgh = *reinterpret_cast<const uint2*>(g_hi + (j * 32 + lane) * 2);
+        const uint2 bvh = *reinterpret_cast<const uint2*>(g_hi + ((16 + j) * 32 + lane) * 2);
         if (SPLIT == 3) {
-          const uint2 bgl = *reinterpret_cast<const uint2*>(g_lo + ((kt * 32 + j) * 32 + lane) * 2);
-          const uint2 bvl = *reinterpret_cast<const uint2*>(g_lo + ((kt * 32 + 16 + j) * 32 + lane) * 2);
-          mma_bf16(Dg, alo[kt], bgh.x, bgh.y);
-          mma_bf16(Dg, ahi[kt], bgl.x, bgl.y);
-          mma_bf16(Dv, alo[kt], bvh.x, bvh.y);
-          mma_bf16(Dv, ahi[kt], bvl.x, bvl.y);
+          const uint2 bgl = *reinterpret_cast<const uint2*>(g_lo + (j * 32 + lane) * 2);
+          const uint2 bvl = *reinterpret_cast<const uint2*>(g_lo + ((16 + j) * 32 + lane) * 2);
+          mma_bf16(Dg, alo[0], bgh.x, bgh.y);
+          mma_bf16(Dv, alo[0], bvh.x, bvh.y);
+          mma_bf16(Dg, ahi[0], bgl.x, bgl.y);
+          mma_bf16(Dv, ahi[0], bvl.x, bvl.y);
         }
-        mma_bf16(Dg, ahi[kt], bgh.x, bgh.y);
-        mma_bf16(Dv, ahi[kt], bvh.x, bvh.y);
+        mma_bf16(Dg, ahi[0], bgh.x, bgh.y);
+        mma_bf16(Dv, ahi[0], bvh.x, bvh.y);
+      }
+      {
+        const uint32_t bgh = g_hi[((32 + j) * 32 + lane) * 2];
+        const uint32_t bvh = g_hi[((32 + 16 + j) * 32 + lane) * 2];
+        if (SPLIT == 3) {
+          const uint32_t bgl = g_lo[((32 + j) * 32 + lane) * 2];
+          const uint32_t bvl = g_lo[((32 + 16 + j) * 32 + lane) * 2];
+          mma_bf16_k8(Dg, alo[1][0], alo[1][1], bgh);
+          mma_bf16_k8(Dv, alo[1][0], alo[1][1], bvh);
+          mma_bf16_k8(Dg, ahi[1][0], ahi[1][1], bgl);
+          mma_bf16_k8(Dv, ahi[1][0], ahi[1][1], bvl);
+        }
+        mma_bf16_k8(Dg, ahi[1][0], ahi[1][1], bgh);
+        mma_bf16_k8(Dv, ahi[1][0], ahi[1][1], bvh);
       }
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
