@@ -99,6 +99,7 @@ struct GnnMmaArgs {
   const int32_t* fact_cnt; int64_t fact_stride; const int32_t* fact_aff; const int32_t* pose_target;
   const char* cache; int64_t cache_stride; int64_t off_hcov, off_f, off_T, off_n;
   float* dump_hcov; float* dump_f; int64_t dump_ld;
+  int heavy_cap;
 };
 int gnn_mma_phase_words();
 int gnn_mma_gather_words();
@@ -988,7 +989,7 @@ int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch*
   const int max_atoms = b->max_pose_atoms > 0 ? b->max_pose_atoms : FS_MAX_POSE_ATOMS;
   // compact node slice per pose; poses whose touched set does not fit the
   // tensor-core SG-CNN's shared memory are flagged FS_ERR_NOT_FACTORED
-  int64_t S = (int64_t)((max_atoms + 15) & ~15) + 32;
+  int64_t S = (int64_t)((max_atoms + 15 + 15) & ~15);   // nc = nLp + nA <= max_atoms + 15
   if (S > gnn_mma_max_nodes()) S = gnn_mma_max_nodes();
   const int64_t N = (int64_t)P * S;
   WsPlan w = plan_ws(*m, P, N, (int64_t)P * max_edges, FS_PREC_BF16);

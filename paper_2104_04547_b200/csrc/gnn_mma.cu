@@ -51,6 +51,7 @@ struct GnnMmaArgs {
   // ---- pocket preparation dumps (plain path): node states after the covalent
   // phase [P][dump_ld][24] and per-node pool terms [P][dump_ld][128]
   float* dump_hcov; float* dump_f; int64_t dump_ld;
+  int heavy_cap;                          // rows of the heavy-sum buffer (set by launch_gnn_mma)
 };
 
 constexpr int kMaxMmaWarps = 24;   // smem reduction buffers are sized for this many warps
@@ -146,7 +147,7 @@ __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[
 // together.  Both forms read 8 (row, neighbour) pairs per 12 lane-instructions.
 constexpr int kHeavyDeg = 32;
 constexpr int kBins = kHeavyDeg + 1;
-constexpr int kCtlWords = 4 + 2 * kBins;
+constexpr int kCtlWords = 6 + 2 * kBins;
 
 __device__ __forceinline__ void acc_row(float (&a)[6], const float* __restrict__ src) {
 #pragma unroll
@@ -159,6 +160,7 @@ __device__ __forceinline__ void acc_row(float (&a)[6], const float* __restrict__
 template <int SPLIT, bool FACT, int kMmaWarps>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a) {
   extern __shared__ __align__(16) float sm[];
+  __shared__ int wcnt[kMmaWarps];
   const int p = blockIdx.x;
   int64_t base;
   int n, nL = 0, nLp = 0;
@@ -181,27 +183,34 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     return;
   }
   const int ntiles = (n + 15) / 16, npad = ntiles * 16;
-  const int srows = max(npad + 1, kMaxMmaWarps * 16);  // S doubles as the pool's reduction buffers (3 x warps x 128 floats)
-  // H: node states [npad + 1][24], row npad stays zero (padded gathers read it)
-  // S: neighbour sums [srows][24], row npad is the sink of padded tile slots
-  float* H = sm;
-  float* S = H + (npad + 1) * 24;
-  uint32_t* WF = reinterpret_cast<uint32_t*>(S + srows * 24);   // phase fragments
-  float* WB = reinterpret_cast<float*>(WF + kPhaseWords);       // phase biases [72]
-  int* CTL = reinterpret_cast<int*>(WB + 72);                  // counters[2], n_heavy, -, hist[kBins], start[kBins]
+  const int hrows = max(npad + 1, kMaxMmaWarps * 16);   // Hn doubles as the pool's reduction buffers
+  // Hc / Hn: node states [npad + 1][24], double buffered (row npad stays zero:
+  // padded gathers read it).  HS: neighbour sums of the heavy rows.
+  float* Hc = sm;
+  float* Hn = Hc + hrows * 24;      // both buffers hrows: either may end as Hn
+  float* HS = Hn + hrows * 24;
+  uint32_t* WF = reinterpret_cast<uint32_t*>(HS + a.heavy_cap * 24);   // phase fragments
+  float* WB = reinterpret_cast<float*>(WF + kPhaseWords);            // phase biases [72]
+  int* CTL = reinterpret_cast<int*>(WB + 72);    // item ctr[2], heavy-done ctr[2], -, -, hist[kBins], cursor[kBins]
+  int* hist = CTL + 6;
   uint16_t* PERM = reinterpret_cast<uint16_t*>(CTL + kCtlWords);   // gather order [npad]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
 #define COLS(c) ((c) < 2 ? 2 * t + (c) : (c) < 4 ? 6 + 2 * t + (c) : 12 + 2 * t + (c))
 
-  // ---- embedding h0 = tanh(X.We + be); padded rows (and row npad) are zero.
-  // Factored: pocket rows start from their cached post-covalent state. ----
+  // ---- embedding h0 = tanh(X.We + be) into both buffers (rows a phase does
+  // not update must read the same in either); padded rows and row npad are
+  // zero.  Factored: pocket rows start from their cached post-covalent state.
   for (int i = threadIdx.x; i <= npad; i += blockDim.x) {
     if (FACT && i >= nLp && i < n) {
       const float4* src = reinterpret_cast<const float4*>(
           reinterpret_cast<const float*>(pc + a.off_hcov) + static_cast<int64_t>(a.fact_aff[base + i]) * 24);
 #pragma unroll
-      for (int k = 0; k < 6; ++k) reinterpret_cast<float4*>(H + i * 24)[k] = src[k];
+      for (int k = 0; k < 6; ++k) {
+        const float4 v = src[k];
+        reinterpret_cast<float4*>(Hc + i * 24)[k] = v;
+        reinterpret_cast<float4*>(Hn + i * 24)[k] = v;
+      }
       continue;
     }
     const bool emb = FACT ? i < nL : i < n;
@@ -217,60 +226,135 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       }
     }
 #pragma unroll
-    for (int k = 0; k < 24; k += 4)
-      *reinterpret_cast<float4*>(H + i * 24 + k) =
-          emb ? make_float4(fs_tanh(acc[k]), fs_tanh(acc[k + 1]), fs_tanh(acc[k + 2]), fs_tanh(acc[k + 3]))
-                : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < 24; k += 4) {
+      const float4 v = emb ? make_float4(fs_tanh(acc[k]), fs_tanh(acc[k + 1]), fs_tanh(acc[k + 2]), fs_tanh(acc[k + 3]))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(Hc + i * 24 + k) = v;
+      *reinterpret_cast<float4*>(Hn + i * 24 + k) = v;
+    }
   }
+
+  // GRU update of 16 rows held by the warp (lane: rows g and g+8, columns
+  // COLS) from their neighbour sums s and states h; ok[rr] = 0 for padding
+  const uint32_t* zr_hi = WF;
+  const uint32_t* zr_lo = WF + kZrWords;
+  const uint32_t* hh_hi = WF + 2 * kZrWords;
+  const uint32_t* hh_lo = WF + 2 * kZrWords + kHhWords;
+  auto gru16 = [&](const float (&sv)[2][6], const float (&h)[2][6], float (&hn)[2][6], const bool (&ok)[2]) {
+    float bz[6], br[6], bh[6];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) { bz[c] = WB[COLS(c)]; br[c] = WB[24 + COLS(c)]; bh[c] = WB[48 + COLS(c)]; }
+    uint32_t ahi[3][4], alo[3][4];
+    build_a48<SPLIT>(sv, h, ahi, alo);
+    float Dzr[6][4];
+    gemm48<SPLIT, 6>(Dzr, ahi, alo, zr_hi, zr_lo, lane);
+    // D n-tile j holds (row g: cols 8j+2t, 8j+2t+1; row g+8: same)
+    float z[2][6], rh[2][6];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int c = 2 * j + e;
+          z[rr][c] = fs_sigmoid(Dzr[j][2 * rr + e] + bz[c]);
+          rh[rr][c] = fs_sigmoid(Dzr[3 + j][2 * rr + e] + br[c]) * h[rr][c];
+        }
+    // A = [s | r*h]: the s part (k-tile 0 and half of k-tile 1) is reused
+    put_a<SPLIT>(ahi[1], alo[1], 2, rh[0][0], rh[0][1]);
+    put_a<SPLIT>(ahi[1], alo[1], 3, rh[1][0], rh[1][1]);
+    put_a<SPLIT>(ahi[2], alo[2], 0, rh[0][2], rh[0][3]);
+    put_a<SPLIT>(ahi[2], alo[2], 1, rh[1][2], rh[1][3]);
+    put_a<SPLIT>(ahi[2], alo[2], 2, rh[0][4], rh[0][5]);
+    put_a<SPLIT>(ahi[2], alo[2], 3, rh[1][4], rh[1][5]);
+    float Dh[3][4];
+    gemm48<SPLIT, 3>(Dh, ahi, alo, hh_hi, hh_lo, lane);
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 2 * j + e;
+          const float hh = fs_tanh(Dh[j][2 * rr + e] + bh[c]);
+          hn[rr][c] = ok[rr] ? fmaf(z[rr][c], hh - h[rr][c], h[rr][c]) : 0.f;
+        }
+  };
+  auto load_h = [&](int row, float (&h)[6]) {
+#pragma unroll
+    for (int c = 0; c < 6; c += 2) {
+      const float2 hv = *reinterpret_cast<const float2*>(Hc + row * 24 + COLS(c));
+      h[c] = hv.x; h[c + 1] = hv.y;
+    }
+  };
+  auto store_hn = [&](int row, const float (&v)[6]) {
+#pragma unroll
+    for (int c = 0; c < 6; c += 2) *reinterpret_cast<float2*>(Hn + row * 24 + COLS(c)) = make_float2(v[c], v[c + 1]);
+  };
 
   int gstep = 0;
   for (int ph = 0; ph < 2; ++ph) {
     __syncthreads();
     if (!FACT && ph == 1 && a.dump_hcov) {   // pocket preparation: post-covalent states
       float* o = a.dump_hcov + static_cast<int64_t>(p) * a.dump_ld * 24;
-      for (int i = threadIdx.x; i < n * 24; i += blockDim.x) o[i] = H[i];
+      for (int i = threadIdx.x; i < n * 24; i += blockDim.x) o[i] = Hc[i];
     }
     // factored covalent phase: only the ligand rows move
     const int prow = FACT && ph == 0 ? nLp : npad;
     for (int i = threadIdx.x; i < kPhaseWords; i += blockDim.x) WF[i] = a.wfrag[ph][i];
     for (int i = threadIdx.x; i < 72; i += blockDim.x) WB[i] = a.wbias[ph][i];
-    if (threadIdx.x < kBins) CTL[4 + threadIdx.x] = 0;
-    if (threadIdx.x < 2) CTL[threadIdx.x] = 0;
+    if (threadIdx.x < kBins) hist[threadIdx.x] = 0;
+    if (threadIdx.x < 4) CTL[threadIdx.x] = 0;
     const int64_t* rows = ph == 0 ? a.row_cov : a.row_ncov;
     const int32_t* degs = ph == 0 ? a.deg_cov : a.deg_ncov;
     const col_t* colv = ph == 0 ? a.col_cov : a.col_ncov;
     __syncthreads();
-    // gather order: counting sort by degree, descending (bin 0 = heavy rows).
-    // The order inside a bin is arbitrary: a row's sum never depends on
-    // where it is gathered, so the result stays deterministic.
-    int* key = reinterpret_cast<int*>(S);     // S is scratch until the first step
+    // gather order: counting sort by degree, descending (bin 0: >= kHeavyDeg).
+    // Where a row lands never changes its result (its sum has a fixed order,
+    // its GRU row is independent of the tile's other rows).
     for (int i = threadIdx.x; i < prow; i += blockDim.x) {
       const int d = i < n ? degs[base + i] : 0;
-      const int bin = kHeavyDeg - min(d, kHeavyDeg);
-      key[i] = (bin << 16) | atomicAdd(&CTL[4 + bin], 1);
+      atomicAdd(&hist[kHeavyDeg - min(d, kHeavyDeg)], 1);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       int acc = 0;
-      for (int b = 0; b < kBins; ++b) { CTL[4 + kBins + b] = acc; acc += CTL[4 + b]; }
-      CTL[2] = CTL[4];
+      for (int b = 0; b < kBins; ++b) { const int c = hist[b]; hist[kBins + b] = acc; acc += c; }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < prow; i += blockDim.x)
-      PERM[CTL[4 + kBins + (key[i] >> 16)] + (key[i] & 0xffff)] = static_cast<uint16_t>(i);
+    // heavy rows beyond the HS capacity join the first light tiles; which rows
+    // those are must be deterministic (heavy and light sums differ in order),
+    // so bin 0 is placed in ascending row order by a block prefix count
+    const int nh = min(hist[1 + kBins] - hist[kBins], a.heavy_cap);
+    {
+      int run = 0;
+      for (int i0 = 0; i0 < prow; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        const bool hv = i < prow && (i < n ? degs[base + i] : 0) >= kHeavyDeg;
+        const unsigned m = __ballot_sync(0xffffffffu, hv);
+        if (lane == 0) wcnt[warp] = __popc(m);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < kMmaWarps; ++w) { const int c = wcnt[w]; before += w < warp ? c : 0; total += c; }
+        if (hv) PERM[run + before + __popc(m & ((1u << lane) - 1u))] = static_cast<uint16_t>(i);
+        run += total;
+        __syncthreads();
+      }
+    }
+    for (int i = threadIdx.x; i < prow; i += blockDim.x) {
+      const int d = i < n ? degs[base + i] : 0;
+      if (d < kHeavyDeg) PERM[atomicAdd(&hist[kBins + kHeavyDeg - d], 1)] = static_cast<uint16_t>(i);
+    }
     __syncthreads();
-    const int nh = CTL[2];
-    const int nitems = nh + (prow - nh + 15) / 16;
-
-    const uint32_t* zr_hi = WF;
-    const uint32_t* zr_lo = WF + kZrWords;
-    const uint32_t* hh_hi = WF + 2 * kZrWords;
-    const uint32_t* hh_lo = WF + 2 * kZrWords + kHhWords;
+    const int nlt = (prow - nh + 15) / 16, nht = (nh + 15) / 16;
+    const int nitems = nh + nlt + nht;
 
     for (int step = 0; step < a.k_steps[ph]; ++step) {
-      // ---- pass 1: S = neighbour sums of H (items handed out dynamically,
-      // heaviest first) ----
+      // Items, handed out in order by a counter: heavy-row sums (-> HS), then
+      // the degree-sorted light tiles (gather + GRU), then the heavy tiles
+      // (GRU from HS, after every heavy sum is in).
       int* ctr = CTL + (gstep & 1);
+      int* hdone = CTL + 2 + (gstep & 1);
       for (int item = warp; item < nitems;) {
         if (item < nh) {
           // one heavy row: lane (q = lane/4, t) sums neighbours q, q+8, ...
@@ -283,7 +367,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
             for (int u = 0; u < 4; ++u) j[u] = q + 8 * u < d ? __ldg(c + q + 8 * u) : npad;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc_row(s6, H + j[u] * 24 + 2 * t);
+            for (int u = 0; u < 4; ++u) acc_row(s6, Hc + j[u] * 24 + 2 * t);
           }
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
@@ -296,19 +380,22 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           if (g == 0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-              *reinterpret_cast<float2*>(S + row * 24 + 2 * t + 8 * k) = make_float2(s6[2 * k], s6[2 * k + 1]);
+              *reinterpret_cast<float2*>(HS + item * 24 + 2 * t + 8 * k) = make_float2(s6[2 * k], s6[2 * k + 1]);
           }
-        } else {
+          __syncwarp();
+          if (lane == 0) { __threadfence_block(); atomicAdd(hdone, 1); }
+        } else if (item < nh + nlt) {
           // 16 degree-sorted light rows; lane (g, t) owns rows g and g+8.
           // Exhausted slots read the all-zero row `npad` (x + 0 == x, so the
-          // sums stay exactly CSR-ordered).
+          // sums stay exactly CSR-ordered).  The sums land in the lane's
+          // A-fragment positions and feed the GRU directly.
           const int k0 = nh + (item - nh) * 16 + g, k1 = k0 + 8;
           const int r0 = k0 < prow ? PERM[k0] : npad, r1 = k1 < prow ? PERM[k1] : npad;
           const int d0 = r0 < n ? degs[base + r0] : 0, d1 = r1 < n ? degs[base + r1] : 0;
           const col_t* c0 = colv + (r0 < n ? rows[base + r0] : 0);
           const col_t* c1 = colv + (r1 < n ? rows[base + r1] : 0);
           const int dm = max(d0, d1);
-          float a0[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, a1[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          float sv[2][6] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}};
           int q = 0;
           for (; q + 8 <= dm; q += 8) {
             int j0[8], j1[8];
@@ -318,8 +405,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             for (int u = 0; u < 8; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-              acc_row(a0, H + j0[u] * 24 + 2 * t);
-              acc_row(a1, H + j1[u] * 24 + 2 * t);
+              acc_row(sv[0], Hc + j0[u] * 24 + 2 * t);
+              acc_row(sv[1], Hc + j1[u] * 24 + 2 * t);
             }
           }
           for (; q < dm; q += 4) {
@@ -330,89 +417,54 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             for (int u = 0; u < 4; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              acc_row(a0, H + j0[u] * 24 + 2 * t);
-              acc_row(a1, H + j1[u] * 24 + 2 * t);
+              acc_row(sv[0], Hc + j0[u] * 24 + 2 * t);
+              acc_row(sv[1], Hc + j1[u] * 24 + 2 * t);
             }
           }
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            *reinterpret_cast<float2*>(S + r0 * 24 + 2 * t + 8 * k) = make_float2(a0[2 * k], a0[2 * k + 1]);
-            *reinterpret_cast<float2*>(S + r1 * 24 + 2 * t + 8 * k) = make_float2(a1[2 * k], a1[2 * k + 1]);
+          // acc_row's column order (2t + 8k, +1) is COLS
+          float h[2][6], hn[2][6];
+          load_h(r0, h[0]);
+          load_h(r1, h[1]);
+          const bool ok[2] = {valid(r0), valid(r1)};
+          gru16(sv, h, hn, ok);
+          if (r0 < npad) store_hn(r0, hn[0]);
+          if (r1 < npad) store_hn(r1, hn[1]);
+        } else {
+          // heavy tile: 16 heavy rows' sums from HS
+          const int i0 = (item - nh - nlt) * 16 + g, i1 = i0 + 8;
+          const int r0 = i0 < nh ? PERM[i0] : npad, r1 = i1 < nh ? PERM[i1] : npad;
+          if (lane == 0) {
+            while (*reinterpret_cast<volatile int*>(hdone) < nh) { }
+            __threadfence_block();
           }
+          __syncwarp();
+          float sv[2][6], h[2][6], hn[2][6];
+#pragma unroll
+          for (int c = 0; c < 6; c += 2) {
+            const float2 v0 = i0 < nh ? *reinterpret_cast<const float2*>(HS + i0 * 24 + COLS(c)) : make_float2(0.f, 0.f);
+            const float2 v1 = i1 < nh ? *reinterpret_cast<const float2*>(HS + i1 * 24 + COLS(c)) : make_float2(0.f, 0.f);
+            sv[0][c] = v0.x; sv[0][c + 1] = v0.y;
+            sv[1][c] = v1.x; sv[1][c + 1] = v1.y;
+          }
+          load_h(r0, h[0]);
+          load_h(r1, h[1]);
+          const bool ok[2] = {valid(r0), valid(r1)};
+          gru16(sv, h, hn, ok);
+          if (r0 < npad) store_hn(r0, hn[0]);
+          if (r1 < npad) store_hn(r1, hn[1]);
         }
         int next = 0;
         if (lane == 0) next = atomicAdd(ctr, 1) + kMmaWarps;
         item = __shfl_sync(0xffffffffu, next, 0);
       }
-      if (threadIdx.x == 0) CTL[(gstep + 1) & 1] = 0;   // next step's counter (last used 2 steps ago)
+      // counters of the next step (last used two steps ago)
+      if (threadIdx.x == 0) { CTL[(gstep + 1) & 1] = 0; CTL[2 + ((gstep + 1) & 1)] = 0; }
       ++gstep;
       __syncthreads();
-
-      // ---- pass 2: GRU update of every 16-row tile, in place ----
-      for (int tile = warp; tile < prow / 16; tile += kMmaWarps) {
-        float bz[6], br[6], bh[6];
-#pragma unroll
-        for (int c = 0; c < 6; ++c) { bz[c] = WB[COLS(c)]; br[c] = WB[24 + COLS(c)]; bh[c] = WB[48 + COLS(c)]; }
-        float s[2][6], h[2][6];
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int row = tile * 16 + g + 8 * rr;
-#pragma unroll
-          for (int c = 0; c < 6; c += 2) {
-            const float2 sv = *reinterpret_cast<const float2*>(S + row * 24 + COLS(c));
-            const float2 hv = *reinterpret_cast<const float2*>(H + row * 24 + COLS(c));
-            s[rr][c] = sv.x; s[rr][c + 1] = sv.y;
-            h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
-          }
-        }
-        uint32_t ahi[3][4], alo[3][4];
-        build_a48<SPLIT>(s, h, ahi, alo);
-        float Dzr[6][4];
-        gemm48<SPLIT, 6>(Dzr, ahi, alo, zr_hi, zr_lo, lane);
-        // D n-tile j holds (row g: cols 8j+2t, 8j+2t+1; row g+8: same)
-        float z[2][6], rh[2][6];
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-              const int c = 2 * j + e;
-              z[rr][c] = fs_sigmoid(Dzr[j][2 * rr + e] + bz[c]);
-              rh[rr][c] = fs_sigmoid(Dzr[3 + j][2 * rr + e] + br[c]) * h[rr][c];
-            }
-        // A = [s | r*h]: the s part (k-tile 0 and half of k-tile 1) is reused
-        put_a<SPLIT>(ahi[1], alo[1], 2, rh[0][0], rh[0][1]);
-        put_a<SPLIT>(ahi[1], alo[1], 3, rh[1][0], rh[1][1]);
-        put_a<SPLIT>(ahi[2], alo[2], 0, rh[0][2], rh[0][3]);
-        put_a<SPLIT>(ahi[2], alo[2], 1, rh[1][2], rh[1][3]);
-        put_a<SPLIT>(ahi[2], alo[2], 2, rh[0][4], rh[0][5]);
-        put_a<SPLIT>(ahi[2], alo[2], 3, rh[1][4], rh[1][5]);
-        float Dh[3][4];
-        gemm48<SPLIT, 3>(Dh, ahi, alo, hh_hi, hh_lo, lane);
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int row = tile * 16 + g + 8 * rr;
-          float hn[6];
-#pragma unroll
-          for (int j = 0; j < 3; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int c = 2 * j + e;
-              const float hh = fs_tanh(Dh[j][2 * rr + e] + bh[c]);
-              hn[c] = valid(row) ? fmaf(z[rr][c], hh - h[rr][c], h[rr][c]) : 0.f;
-            }
-#pragma unroll
-          for (int c = 0; c < 6; c += 2)
-            *reinterpret_cast<float2*>(H + row * 24 + COLS(c)) = make_float2(hn[c], hn[c + 1]);
-        }
-      }
-      __syncthreads();
+      float* tmp = Hc; Hc = Hn; Hn = tmp;
     }
   }
-  float* Hc = H;
-  float* Hn = S;
-  float* RED = S;   // [warps][128], written only after every warp is done with the staged fragments
+  float* RED = Hn;   // [warps][128] (+ [warps][128] doubles), written only after every warp is done with the staged fragments
 
   // ---- gated gather + mean pool: [gate|val] = h.[Gg|Gf] (K 24->32, N 256) ----
   float acc[16][2];
@@ -421,7 +473,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   // gather fragments: stage into the (now free) neighbour-sum buffer when it
   // is large enough, else read them through L1
   const uint32_t* gsrc = a.gfrag;
-  if (srows * 24 >= kGatherWords) {
+  if (hrows * 24 >= kGatherWords) {
     uint32_t* gs = reinterpret_cast<uint32_t*>(Hn);
     for (int i = threadIdx.x; i < kGatherWords; i += blockDim.x) gs[i] = a.gfrag[i];
     gsrc = gs;
@@ -544,14 +596,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   }
 }
 
-size_t gnn_mma_smem_bytes(int max_nodes) {
+static size_t gnn_smem_bytes(int max_nodes, int heavy_cap) {
   const int npad = (max_nodes + 15) / 16 * 16;
-  const int srows = npad + 1 > kMaxMmaWarps * 16 ? npad + 1 : kMaxMmaWarps * 16;
-  return static_cast<size_t>(npad + 1 + srows) * 24 * 4 + kPhaseWords * 4 + 72 * 4 + kCtlWords * 4 +
+  const int hrows = npad + 1 > kMaxMmaWarps * 16 ? npad + 1 : kMaxMmaWarps * 16;
+  return static_cast<size_t>(2 * hrows + heavy_cap) * 24 * 4 + kPhaseWords * 4 + 72 * 4 + kCtlWords * 4 +
          static_cast<size_t>(npad) * 2 + 64;
 }
+constexpr size_t kSmemLimit = 227 * 1024;
+constexpr int kMaxHeavy = 64;
 
-bool gnn_mma_fits(int max_nodes) { return gnn_mma_smem_bytes(max_nodes) <= 227 * 1024; }
+// The heavy-row capacity is a constant: which rows take the heavy path (and so
+// their summation order) must not depend on the batch a pose is scored in.
+size_t gnn_mma_smem_bytes(int max_nodes) { return gnn_smem_bytes(max_nodes, kMaxHeavy); }
+
+bool gnn_mma_fits(int max_nodes) { return gnn_mma_smem_bytes(max_nodes) <= kSmemLimit; }
 
 int gnn_mma_max_nodes() {
   int n = 16;
@@ -574,9 +632,11 @@ static int gnn_warps() {
   return w == 20 ? 20 : 16;
 }
 
-int launch_gnn_mma(const GnnMmaArgs& a, int split, int n_poses, int max_nodes, cudaStream_t st) {
+int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes, cudaStream_t st) {
   if (n_poses <= 0) return FS_OK;
   if (!gnn_mma_fits(max_nodes)) return FS_ECAPACITY;
+  GnnMmaArgs a = a_in;
+  a.heavy_cap = kMaxHeavy;
   const size_t smem = gnn_mma_smem_bytes(max_nodes);
   const int w = gnn_warps();
   if (a.fact_cnt)
