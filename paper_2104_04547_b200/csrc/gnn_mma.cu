@@ -626,10 +626,11 @@ static int launch_gnn_mma_t(const GnnMmaArgs& a, int n_poses, size_t smem, cudaS
   return FS_OK;
 }
 
-// warps per pose (FS_GNN_WARPS = 16 | 20; more warps = fewer registers each)
+// warps per pose: FS_GNN_WARPS = 16 | 20 | 24 (more warps hide more gather
+// latency with fewer registers each; 20 measured fastest)
 static int gnn_warps() {
-  static const int w = getenv("FS_GNN_WARPS") ? atoi(getenv("FS_GNN_WARPS")) : 16;
-  return w == 20 ? 20 : 16;
+  static const int w = getenv("FS_GNN_WARPS") ? atoi(getenv("FS_GNN_WARPS")) : 20;
+  return w == 16 || w == 24 ? w : 20;
 }
 
 int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes, cudaStream_t st) {
@@ -639,10 +640,15 @@ int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes
   a.heavy_cap = kMaxHeavy;
   const size_t smem = gnn_mma_smem_bytes(max_nodes);
   const int w = gnn_warps();
-  if (a.fact_cnt)
-    return w == 20 ? launch_gnn_mma_t<3, true, 20>(a, n_poses, smem, st) : launch_gnn_mma_t<3, true, 16>(a, n_poses, smem, st);
-  if (split != 3) return launch_gnn_mma_t<1, false, 16>(a, n_poses, smem, st);
-  return w == 20 ? launch_gnn_mma_t<3, false, 20>(a, n_poses, smem, st) : launch_gnn_mma_t<3, false, 16>(a, n_poses, smem, st);
+  if (a.fact_cnt) {
+    if (w == 16) return launch_gnn_mma_t<3, true, 16>(a, n_poses, smem, st);
+    if (w == 24) return launch_gnn_mma_t<3, true, 24>(a, n_poses, smem, st);
+    return launch_gnn_mma_t<3, true, 20>(a, n_poses, smem, st);
+  }
+  if (split != 3) return launch_gnn_mma_t<1, false, 20>(a, n_poses, smem, st);
+  if (w == 16) return launch_gnn_mma_t<3, false, 16>(a, n_poses, smem, st);
+  if (w == 24) return launch_gnn_mma_t<3, false, 24>(a, n_poses, smem, st);
+  return launch_gnn_mma_t<3, false, 20>(a, n_poses, smem, st);
 }
 
 }  // namespace fs
