@@ -16,6 +16,7 @@ top-k (merged on device), inside the timed region.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -267,6 +268,7 @@ def main():
     launches0 = L.fs_launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     errs = []
+    gc.disable()        # no collector pauses inside the timed regions
     with Clocks(local) as clk:
         t_start.record()
         top = (None, None)
@@ -403,6 +405,7 @@ def main():
                         "phase, untouched pocket nodes) reused from a per-target cache; algorithmic work per "
                         "pose and the roofline are those of the full path (SURVEY 8d/8f-4)"}
 
+    gc.enable()
     if rank == 0:
         hbm, bf16_burst, bf16_sus, peak_kind = peaks()
         names = N.STAGES[:-1]

@@ -385,34 +385,40 @@ static int pack_model(fs_model& m, const ParamMap& pm, std::vector<float>& h) {
         for (int t2 = 0; t2 < dg; ++t2) acc += msg[(size_t)c * dg + t2] * W[q][(size_t)t2 * dg + k];
         return acc;
       };
+      // gate pre-activations carry the ex2 scale of their activation
+      // (fs_sigmoid_pre / fs_tanh_pre): z, r by -log2(e), h~ by 2 log2(e)
       std::vector<double> Wzr((size_t)48 * 48), Whh((size_t)48 * 24);
+      const double sc[3] = {kNegLog2e, kNegLog2e, kTwoLog2e};
       for (int c = 0; c < 24; ++c)
         for (int k = 0; k < 24; ++k) {
-          Wzr[(size_t)c * 48 + k] = fold(0, c, k);
-          Wzr[(size_t)c * 48 + 24 + k] = fold(1, c, k);
-          Wzr[(size_t)(24 + c) * 48 + k] = U[0][(size_t)c * dg + k];
-          Wzr[(size_t)(24 + c) * 48 + 24 + k] = U[1][(size_t)c * dg + k];
-          Whh[(size_t)c * 24 + k] = fold(2, c, k);
-          Whh[(size_t)(24 + c) * 24 + k] = U[2][(size_t)c * dg + k];
+          Wzr[(size_t)c * 48 + k] = sc[0] * fold(0, c, k);
+          Wzr[(size_t)c * 48 + 24 + k] = sc[1] * fold(1, c, k);
+          Wzr[(size_t)(24 + c) * 48 + k] = sc[0] * U[0][(size_t)c * dg + k];
+          Wzr[(size_t)(24 + c) * 48 + 24 + k] = sc[1] * U[1][(size_t)c * dg + k];
+          Whh[(size_t)c * 24 + k] = sc[2] * fold(2, c, k);
+          Whh[(size_t)(24 + c) * 24 + k] = sc[2] * U[2][(size_t)c * dg + k];
         }
       uint32_t* wf = reinterpret_cast<uint32_t*>(&h[m.gm_wf[ph]]);
       const int zr = 3 * 6 * 64, hh = 3 * 3 * 64;
       frags(Wzr, 48, 48, wf, wf + zr);
       frags(Whh, 48, 24, wf + 2 * zr, wf + 2 * zr + hh);
       for (int q = 0; q < 3; ++q)
-        for (int k = 0; k < 24; ++k) h[m.gm_wb[ph] + q * 24 + k] = (float)B[q][k];
+        for (int k = 0; k < 24; ++k) h[m.gm_wb[ph] + q * 24 + k] = (float)(sc[q] * B[q][k]);
     }
     const double* ggw = need("graph/gather_gate_w"); const double* ggb = need("graph/gather_gate_b");
     const double* gfw = need("graph/gather_feat_w"); const double* gfb = need("graph/gather_feat_b");
     std::vector<double> Gm((size_t)32 * 256, 0.0);
     for (int c = 0; c < 24; ++c)
       for (int k = 0; k < 128; ++k) {
-        Gm[(size_t)c * 256 + k] = ggw[(size_t)c * 128 + k];
-        Gm[(size_t)c * 256 + 128 + k] = gfw[(size_t)c * 128 + k];
+        Gm[(size_t)c * 256 + k] = kNegLog2e * ggw[(size_t)c * 128 + k];
+        Gm[(size_t)c * 256 + 128 + k] = kTwoLog2e * gfw[(size_t)c * 128 + k];
       }
     uint32_t* gf = reinterpret_cast<uint32_t*>(&h[m.gm_gf]);
     frags(Gm, 32, 256, gf, gf + gnn_mma_gather_words() / 2);
-    for (int k = 0; k < 128; ++k) { h[m.gm_gb + k] = (float)ggb[k]; h[m.gm_gb + 128 + k] = (float)gfb[k]; }
+    for (int k = 0; k < 128; ++k) {
+      h[m.gm_gb + k] = (float)(kNegLog2e * ggb[k]);
+      h[m.gm_gb + 128 + k] = (float)(kTwoLog2e * gfb[k]);
+    }
   }
   if ((rc = copy("graph/dense1_w", m.gd1w, (size_t)m.gn * m.w1))) return rc;
   if ((rc = copy("graph/dense1_b", m.gd1b, m.w1))) return rc;

@@ -118,6 +118,21 @@ __device__ __forceinline__ float fs_tanh(float x) {
   return 1.0f - 2.0f * fs_rcp(1.0f + e);
 }
 
+// Pre-scaled forms for the tensor-core SG-CNN, whose packed weights and biases
+// already carry the exponent scale (so the GEMM output is the ex2 argument):
+//   fs_sigmoid_pre(u) = sigmoid(x) with u = -log2(e) x
+//   fs_tanh_pre(u)    = tanh(x)    with u = 2 log2(e) x
+// ex2(+inf) = inf and rcp(inf) = 0 give the right limits without clamps.
+__device__ __forceinline__ float fs_ex2(float u) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(u));
+  return r;
+}
+__device__ __forceinline__ float fs_sigmoid_pre(float u) { return fs_rcp(1.0f + fs_ex2(u)); }
+__device__ __forceinline__ float fs_tanh_pre(float u) { return fmaf(-2.0f, fs_rcp(1.0f + fs_ex2(u)), 1.0f); }
+constexpr double kNegLog2e = -1.4426950408889634074;
+constexpr double kTwoLog2e = 2.8853900817779268147;
+
 #define FS_ACT_NONE 0
 #define FS_ACT_RELU 1
 #define FS_ACT_LEAKY 2

@@ -257,8 +257,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           const int c = 2 * j + e;
-          z[rr][c] = fs_sigmoid(Dzr[j][2 * rr + e] + bz[c]);
-          rh[rr][c] = fs_sigmoid(Dzr[3 + j][2 * rr + e] + br[c]) * h[rr][c];
+          z[rr][c] = fs_sigmoid_pre(Dzr[j][2 * rr + e] + bz[c]);
+          rh[rr][c] = fs_sigmoid_pre(Dzr[3 + j][2 * rr + e] + br[c]) * h[rr][c];
         }
     // A = [s | r*h]: the s part (k-tile 0 and half of k-tile 1) is reused
     put_a<SPLIT>(ahi[1], alo[1], 2, rh[0][0], rh[0][1]);
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int c = 2 * j + e;
-          const float hh = fs_tanh(Dh[j][2 * rr + e] + bh[c]);
+          const float hh = fs_tanh_pre(Dh[j][2 * rr + e] + bh[c]);
           hn[rr][c] = ok[rr] ? fmaf(z[rr][c], hh - h[rr][c], h[rr][c]) : 0.f;
         }
   };
@@ -538,8 +538,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       for (int e = 0; e < 2; ++e) {
         const int col = 8 * j + 2 * t + e;
         const float bgv = __ldg(a.gbias + col), bfv = __ldg(a.gbias + 128 + col);
-        const float x0 = v0 ? fs_sigmoid(Dg[e] + bgv) * fs_tanh(Dv[e] + bfv) : 0.f;
-        const float x1 = v1 ? fs_sigmoid(Dg[2 + e] + bgv) * fs_tanh(Dv[2 + e] + bfv) : 0.f;
+        const float x0 = v0 ? fs_sigmoid_pre(Dg[e] + bgv) * fs_tanh_pre(Dv[e] + bfv) : 0.f;
+        const float x1 = v1 ? fs_sigmoid_pre(Dg[2 + e] + bgv) * fs_tanh_pre(Dv[2 + e] + bfv) : 0.f;
         acc[j][e] += x0 + x1;
         if (!FACT && a.dump_f) {   // pocket preparation: per-node pool terms
           float* o = a.dump_f + (static_cast<int64_t>(p) * a.dump_ld + tile * 16 + g) * 128 + col;
