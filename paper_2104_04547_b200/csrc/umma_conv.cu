@@ -130,7 +130,8 @@ __host__ __device__ constexpr int pow2_cols(int x) {
 // ---------------------------------------------------------------------------
 // layer configuration
 // ---------------------------------------------------------------------------
-template <int G_, int CIN_, int COUT_, int KS_, int POSES_, bool POOL_, bool RESID_, bool OUT_F32_, int NSPLIT_>
+template <int G_, int CIN_, int COUT_, int KS_, int POSES_, bool POOL_, bool RESID_, bool OUT_F32_, int NSPLIT_,
+          int PREFETCH_ = 1>
 struct Cfg {
   static constexpr int G = G_, CIN = CIN_, COUT = COUT_, KS = KS_, POSES = POSES_, NSPLIT = NSPLIT_;
   static constexpr bool POOL = POOL_, RESID = RESID_, OUT_F32 = OUT_F32_;
@@ -142,7 +143,8 @@ struct Cfg {
   static constexpr int BOX_BYTES = HP * POSES * WP * 16;  // one TMA box (8 channels)
   static constexpr int CHUNK_BYTES = align_to(BOX_BYTES, 128);
   static constexpr int PLANE_BYTES = CHUNKS * CHUNK_BYTES;
-  static constexpr int RING = KS + 1;
+  // KS planes in use + PREFETCH planes the TMA producer may run ahead
+  static constexpr int RING = KS + PREFETCH_;
   static constexpr int NCTA = COUT / NSPLIT;               // output channels per CTA
   static constexpr int NG = NCTA / 8;
   static constexpr int STEPS_PER_PLANE = (CIN == 8) ? (KS * KS + 1) / 2 : KS * KS * (CIN / 16);
@@ -161,10 +163,10 @@ struct Cfg {
 
 // conv1 8->32 k5 on 16^3; conv2 32->32 k3 +pool; conv3 32->64 k3 (pose pairs);
 // conv4 64->64 k3 +residual +pool (pose pairs, N split over 2 CTAs).
-using C1 = Cfg<16, 8, 32, 5, 1, false, false, false, 1>;
-using C2 = Cfg<16, 32, 32, 3, 1, true, false, false, 1>;
-using C3 = Cfg<8, 32, 64, 3, 2, false, false, false, 1>;
-using C4 = Cfg<8, 64, 64, 3, 2, true, true, true, 2>;
+using C1 = Cfg<16, 8, 32, 5, 1, false, false, false, 1, 1>;   // 105 KB: two CTAs per SM
+using C2 = Cfg<16, 32, 32, 3, 1, true, false, false, 1, 1>;
+using C3 = Cfg<8, 32, 64, 3, 2, false, false, false, 1, 3>;
+using C4 = Cfg<8, 64, 64, 3, 2, true, true, true, 2, 1>;
 
 // Per K-step A-descriptor low word (start-address and LBO fields, 16-byte
 // units) relative to the plane base of the step's kd.
