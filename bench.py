@@ -432,13 +432,14 @@ def main():
                     "peak": bf16_sus, "unit": "TFLOP/s", "traffic": None}
         # DRAM traffic of the dominant kernel: dram__bytes_read+write per pose
         # from the committed ncu --set full capture, scaled to this launch
-        tr_key = {"gnn": "gnn_mma_kernel<3, 0, 16>" if precision == "bf16" else None,
-                  "conv1": "conv_umma_kernel<Cfg<16, 8, 32, 5, 1, 0, 0, 0, 1>>",
-                  "conv2": "conv_umma_kernel<Cfg<16, 32, 32, 3, 1, 1, 0, 0, 1>>",
-                  "featurize": "graph_csr_kernel<0>"}.get(dom_name)
+        tr_prefix = {"gnn": "gnn_mma_kernel<3, 0," if precision == "bf16" else None,
+                     "conv1": "conv_umma_kernel<Cfg<16, 8, 32, 5,",
+                     "conv2": "conv_umma_kernel<Cfg<16, 32, 32, 3,",
+                     "featurize": "graph_csr_kernel<0>"}.get(dom_name)
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")))
-            if tr_key in tr:
+            tr_key = next((k for k in tr if tr_prefix and k.startswith(tr_prefix)), None)
+            if tr_key:
                 roof["traffic"] = tr[tr_key]["bytes_per_pose"] * B
                 roof["traffic_unit"] = "bytes per launch"
                 roof["traffic_source"] = ("profiles/r01/ncu_traffic.json: ncu --set full dram__bytes_read.sum + "
