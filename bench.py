@@ -265,26 +265,60 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches0 = L.fs_launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    errs = []
-    gc.disable()        # no collector pauses inside the timed regions
-    with Clocks(local) as clk:
-        t_start.record()
+
+    def run_steps(stepf):
+        """The K screening steps (L2 flush, stage events, step); returns the
+        running top-k, best-pose accumulator and per-step errors."""
         top = (None, None)
         acc = E.BestPoseAccumulator(n_comp, rank * n_comp, device=dev)
+        errs = []
         for i in range(K):
             flush.zero_()                                  # L2 flush between steps
             evs = stage_events[i]
             arr = (E.C.c_void_p * len(evs))(*[E.C.c_void_p(e.cuda_event) for e in evs])
             L.fs_set_stage_events(arr, len(evs))
-            out, top = step(i * B, (i + 1) * B, top, acc)
+            out, top = stepf(i * B, (i + 1) * B, top, acc)
             L.fs_set_stage_events(None, 0)
             errs.append(out["err"])
+        return top, acc, errs
+
+    def capture(stepf):
+        """The K steps as one CUDA graph (host stalls cannot idle the GPU, no
+        per-launch overhead); None if capture is not possible here."""
+        if os.environ.get("FS_BENCH_EAGER"):
+            return None
+        try:
+            graph = torch.cuda.CUDAGraph()
+            n0 = L.fs_launch_count()
+            with torch.cuda.graph(graph):
+                res = run_steps(stepf)
+            n_launch = L.fs_launch_count() - n0
+            graph.replay()                                 # warm replay
+            torch.cuda.synchronize()
+            return graph, res, n_launch
+        except Exception as exc:                           # noqa: BLE001 -- fall back to eager
+            print(f"bench: CUDA graph capture unavailable ({exc}); timing eagerly", file=sys.stderr)
+            torch.cuda.synchronize()
+            return None
+
+    cap = capture(step)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.fs_launch_count()
+    gc.disable()        # no collector pauses inside the timed regions
+    with Clocks(local) as clk:
+        t_start.record()
+        if cap is not None:
+            graph, (top, acc, errs), launches = cap
+            graph.replay()
+        else:
+            top, acc, errs = run_steps(step)
         gi, gci = finish(top, acc)
         t_end.record()
         torch.cuda.synchronize()
-    launches = L.fs_launch_count() - launches0
+    launches = launches if cap is not None else L.fs_launch_count() - launches0
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
@@ -365,20 +399,17 @@ def main():
         fact_err = int(out_f["err"].ne(0).sum().item())
         max_diff = float((ref_full - ref_fact).abs().max().item())
         fstage = np.zeros(len(N.STAGES) - 1)
+        fcap = capture(fstep)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
-        top = (None, None)
-        acc = E.BestPoseAccumulator(n_comp, rank * n_comp, device=dev)
-        for i in range(K):
-            flush.zero_()
-            evs = stage_events[i]
-            arr = (E.C.c_void_p * len(evs))(*[E.C.c_void_p(e.cuda_event) for e in evs])
-            L.fs_set_stage_events(arr, len(evs))
-            out_f, top = fstep(i * B, (i + 1) * B, top, acc)
-            L.fs_set_stage_events(None, 0)
+        if fcap is not None:
+            fgraph, (top, acc, _), _ = fcap
+            fgraph.replay()
+        else:
+            top, acc, _ = run_steps(fstep)
         gi_f, gci_f = finish(top, acc)
         f1.record()
         torch.cuda.synchronize()
@@ -462,7 +493,9 @@ def main():
                 "e2e": {"value": e2e_value, "unit": "poses/s", "h2d_bytes_per_step": h2d // K,
                         "d2h_bytes_per_step": d2h // K, "topk_equal_device_resident": same_topk,
                         "source": "packed library file (mmap) -> pinned double buffer -> H2D on a copy stream"},
-                "gpu_launches": int(launches), "clocks": clk.summary()}
+                "gpu_launches": int(launches), "clocks": clk.summary(),
+                "launch_mode": "cuda_graph (K steps captured once, replayed in the timed region)" if cap is not None
+                else "eager"}
         if fact is not None:
             line["pocket_factored"] = fact
         if not args.no_cpu_baseline and world == 1:

@@ -34,7 +34,14 @@ void count_launch(const char* file, int line) {
 
 static thread_local cudaEvent_t* g_stage_events = nullptr;   // [ST_COUNT] or null
 void mark_stage(int stage, cudaStream_t st) {
-  if (g_stage_events && g_stage_events[stage]) cudaEventRecord(g_stage_events[stage], st);
+  if (!g_stage_events || !g_stage_events[stage]) return;
+  // inside a CUDA-graph capture the record must be an external (timed) node
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(g_stage_events[stage], st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(g_stage_events[stage], st);
 }
 
 // ---- launchers defined in the other translation units ----------------------
