@@ -110,18 +110,29 @@ class HostStager:
 
 
 class Screen:
-    """Scores a DeviceLibrary batch by batch with a running device top-k."""
+    """Scores a DeviceLibrary batch by batch with a running device top-k.
+
+    ``pocket_cache`` (DeviceModel.prepare_pockets of the library's pockets)
+    switches to the pocket-factored scorer: same
+    scores to fp32 rounding; non-factorable poses come back flagged
+    FS_ERR_NOT_FACTORED (rescore them with a plain Screen)."""
 
     def __init__(self, model: E.DeviceModel, precision="bf16", batch_size=8192, k=100,
-                 max_edges_per_pose=32768):
+                 max_edges_per_pose=32768, pocket_cache=None):
+        if pocket_cache is not None and precision != "bf16":
+            raise ValueError("the pocket-factored scorer is bf16 only")
         self.model = model
         self.precision = precision
         self.B = batch_size
         self.k = k
         self.max_edges_per_pose = max_edges_per_pose
+        self.pocket_cache = pocket_cache
 
     def score(self, batch: E.PoseBatch, outputs=("scores",)):
         # no host sync: overflow shows up in err (checked after the screen)
+        if self.pocket_cache is not None:
+            return self.model.score_poses_cached(batch, self.pocket_cache, self.max_edges_per_pose, outputs,
+                                                 rescore=False)
         return self.model.score_poses(batch, self.precision, self.max_edges_per_pose, outputs, retry=False)
 
     def run(self, source, keep_scores=False, best_compounds=None, compound_base=0, direction="max"):

@@ -100,3 +100,20 @@ def test_empty_compound_reports_no_pose(setup):
     bs, bp = (t.cpu().numpy() for t in acc.result())
     assert bp.tolist() == [4, -1, 5]
     assert bs[0] == np.float32(1.5) and np.isnan(bs[1]) and bs[2] == np.float32(-2.0)
+
+
+def test_factored_screen_matches_full_screen(setup):
+    import torch
+    E, screen, dm, pockets, lib = setup
+    if not dm.supports("bf16"):
+        pytest.skip("bf16 unsupported")
+    dlib = screen.DeviceLibrary(lib, pockets, torch.device("cuda"))
+    cache = dm.prepare_pockets(dlib.pocket_xyz, dlib.pocket_elem, dlib.pocket_role, dlib.pocket_off)
+    full = screen.Screen(dm, "bf16", batch_size=50, k=15).run(dlib, keep_scores=True, best_compounds=40)
+    fact = screen.Screen(dm, "bf16", batch_size=50, k=15, pocket_cache=cache).run(dlib, keep_scores=True,
+                                                                                 best_compounds=40)
+    assert int(fact["err"].abs().sum()) == 0
+    assert (fact["scores"] - full["scores"]).abs().max().item() < 2e-6
+    assert torch.equal(fact["topk_idx"], full["topk_idx"])
+    assert torch.equal(fact["best_pose"], full["best_pose"])
+    assert torch.equal(fact["topk_compound_idx"], full["topk_compound_idx"])
