@@ -201,6 +201,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   // ---- embedding h0 = tanh(X.We + be) into both buffers (rows a phase does
   // not update must read the same in either); padded rows and row npad are
   // zero.  Factored: pocket rows start from their cached post-covalent state.
+  // We and be are staged in the (not yet used) fragment area for float4
+  // broadcast reads.
+  float* WE = reinterpret_cast<float*>(WF);   // [F][24] then be[24]
+  for (int i = threadIdx.x; i < a.F * 24; i += blockDim.x) WE[i] = a.we[i];
+  for (int i = threadIdx.x; i < 24; i += blockDim.x) WE[a.F * 24 + i] = a.be[i];
+  __syncthreads();
   for (int i = threadIdx.x; i <= npad; i += blockDim.x) {
     if (FACT && i >= nLp && i < n) {
       const float4* src = reinterpret_cast<const float4*>(
@@ -216,13 +222,24 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     const bool emb = FACT ? i < nL : i < n;
     float acc[24];
 #pragma unroll
-    for (int k = 0; k < 24; ++k) acc[k] = emb ? a.be[k] : 0.f;
+    for (int k = 0; k < 24; k += 4) {
+      const float4 b4 = *reinterpret_cast<const float4*>(WE + a.F * 24 + k);
+      acc[k] = emb ? b4.x : 0.f; acc[k + 1] = emb ? b4.y : 0.f;
+      acc[k + 2] = emb ? b4.z : 0.f; acc[k + 3] = emb ? b4.w : 0.f;
+    }
     if (emb) {
       const float* x = a.feats + (base + i) * a.F;
       for (int f = 0; f < a.F; ++f) {
         const float xv = x[f];
+        const float4* w4 = reinterpret_cast<const float4*>(WE + f * 24);
 #pragma unroll
-        for (int k = 0; k < 24; ++k) acc[k] = fmaf(xv, __ldg(a.we + f * 24 + k), acc[k]);
+        for (int k = 0; k < 6; ++k) {
+          const float4 w = w4[k];
+          acc[4 * k] = fmaf(xv, w.x, acc[4 * k]);
+          acc[4 * k + 1] = fmaf(xv, w.y, acc[4 * k + 1]);
+          acc[4 * k + 2] = fmaf(xv, w.z, acc[4 * k + 2]);
+          acc[4 * k + 3] = fmaf(xv, w.w, acc[4 * k + 3]);
+        }
       }
     }
 #pragma unroll
