@@ -7,14 +7,24 @@
 //
 // im2col-free design.  Every output plane d is one or two M=128 tiles whose
 // rows are output voxels (8 consecutive w) x 16 row groups ((h, pose)).  The
-// input planes d-r..d+r are staged by TMA into a shared-memory ring laid out
+// padded input planes are staged by TMA into a shared-memory ring laid out
 // chunk-major: [8-channel chunk][h+2r][pose][w+2r] x 16 bytes (zero padding
 // comes from TMA out-of-bounds fill).  In that layout the A operand of
-// kernel offset (kd,kh,kw) is just a *shifted* K-major no-swizzle UMMA
+// kernel offset (kh,kw) is just a *shifted* K-major no-swizzle UMMA
 // descriptor: core-matrix rows (8 w) are 16 B apart, row groups (h,pose) are
-// SBO = (w+2r)*16 B apart, the two K chunks of one MMA are LBO apart.  So the
-// 27 (or 125) shifted GEMMs read the staged plane 27x from SMEM with zero
-// data movement -- HBM/L2 traffic is one read of each activation.
+// SBO = (w+2r)*16 B apart, the two K chunks of one MMA are LBO apart.
+//
+// Plane-stacked N.  Input plane q feeds the KS output planes d = q-KS+1..q
+// (kernel plane kd = q-d).  Their weights are stored side by side along N
+// ([kd descending][cout]), so ONE MMA per (kh,kw,chunk) step contracts the
+// staged A tile against all of them: N = cout x (#output planes), up to 160
+// (conv1) / 96 (conv2) / 192 (conv3).  Each A tile is read from shared
+// memory once per input plane instead of once per (input, output) plane
+// pair -- the 32-channel layers were bound by exactly those A re-reads
+// (4 KB of operand per 131 kFLOP MMA).  Output planes accumulate in a ring
+// of kSlots TMEM slots (d mod kSlots, contiguous columns, so a stacked MMA
+// writes consecutive slots); the epilogue drains a finished plane, zeroes
+// its slot with tcgen05.st (so every MMA accumulates) and hands it back.
 //   16^3 layers: one pose per tile, 2 tiles (w halves) per plane.
 //   8^3 layers : two poses per tile, h rows of the pair interleaved (the TMA
 //                box spans (w, pose, h) so its dense fill is the interleave).
@@ -122,6 +132,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_zero32(uint32_t taddr) {
+  const uint32_t z = 0;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(z)
+      : "memory");
+}
+
 __host__ __device__ constexpr int align_to(int x, int a) { return (x + a - 1) / a * a; }
 __host__ __device__ constexpr int pow2_cols(int x) {
   return x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : x <= 256 ? 256 : 512;
@@ -130,8 +148,10 @@ __host__ __device__ constexpr int pow2_cols(int x) {
 // ---------------------------------------------------------------------------
 // layer configuration
 // ---------------------------------------------------------------------------
+constexpr int kSlots = 8;   // TMEM accumulator slots (output planes in flight) per tile
+
 template <int G_, int CIN_, int COUT_, int KS_, int POSES_, bool POOL_, bool RESID_, bool OUT_F32_, int NSPLIT_,
-          int PREFETCH_ = 1>
+          int RING_ = 4>
 struct Cfg {
   static constexpr int G = G_, CIN = CIN_, COUT = COUT_, KS = KS_, POSES = POSES_, NSPLIT = NSPLIT_;
   static constexpr bool POOL = POOL_, RESID = RESID_, OUT_F32 = OUT_F32_;
@@ -143,30 +163,36 @@ struct Cfg {
   static constexpr int BOX_BYTES = HP * POSES * WP * 16;  // one TMA box (8 channels)
   static constexpr int CHUNK_BYTES = align_to(BOX_BYTES, 128);
   static constexpr int PLANE_BYTES = CHUNKS * CHUNK_BYTES;
-  // KS planes in use + PREFETCH planes the TMA producer may run ahead
-  static constexpr int RING = KS + PREFETCH_;
+  static constexpr int RING = RING_;                       // staged input planes (each consumed once)
   static constexpr int NCTA = COUT / NSPLIT;               // output channels per CTA
   static constexpr int NG = NCTA / 8;
   static constexpr int STEPS_PER_PLANE = (CIN == 8) ? (KS * KS + 1) / 2 : KS * KS * (CIN / 16);
   static constexpr int KSTEPS = KS * STEPS_PER_PLANE;
-  static constexpr int W_BYTES = KSTEPS * 2 * NG * 128;    // per N slice
-  static constexpr int ACC_COLS = TILES * NCTA;
-  static constexpr int TMEM_COLS = pow2_cols(2 * ACC_COLS);
+  static constexpr int JSTEP = NG * 128;                   // bytes of one kernel plane's N rows (one K chunk)
+  static constexpr int STEP_BYTES = 2 * KS * JSTEP;        // one (kh,kw,chunk) step: [kc][kd desc][cout]
+  static constexpr int W_BYTES = STEPS_PER_PLANE * STEP_BYTES;   // per N slice
+  static constexpr int SLOT_COLS = NCTA;
+  static constexpr int TMEM_COLS = pow2_cols(TILES * kSlots * NCTA);
+  static_assert(TILES * kSlots * NCTA <= 512, "TMEM budget");
+  static_assert(G % kSlots == 0 && kSlots >= KS, "slot ring");
+  static_assert(KS * NCTA <= 256 && NCTA % 16 == 0, "stacked N");
   static constexpr int NPLANES = G + KS - 1;               // padded planes per unit
-  static constexpr uint32_t IDESC = idesc_bf16(128, NCTA);
   static constexpr uint32_t SBO = WP * 16;
   static constexpr int RING_OFF = align_to(W_BYTES, 1024);
   static constexpr int BAR_OFF = RING_OFF + RING * PLANE_BYTES;
-  static constexpr int SMEM = BAR_OFF + 256;
+  // a 512-column TMEM allocation admits one CTA per SM: request enough shared
+  // memory that the scheduler never co-locates two (the second would block
+  // in tcgen05.alloc until the first, persistent one exits)
+  static constexpr int SMEM = (TMEM_COLS == 512 && BAR_OFF + 256 < 116 * 1024) ? 116 * 1024 : BAR_OFF + 256;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
 // conv1 8->32 k5 on 16^3; conv2 32->32 k3 +pool; conv3 32->64 k3 (pose pairs);
 // conv4 64->64 k3 +residual +pool (pose pairs, N split over 2 CTAs).
-using C1 = Cfg<16, 8, 32, 5, 1, false, false, false, 1, 1>;   // 105 KB: two CTAs per SM
-using C2 = Cfg<16, 32, 32, 3, 1, true, false, false, 1, 1>;
-using C3 = Cfg<8, 32, 64, 3, 2, false, false, false, 1, 3>;
-using C4 = Cfg<8, 64, 64, 3, 2, true, true, true, 2, 1>;
+using C1 = Cfg<16, 8, 32, 5, 1, false, false, false, 1, 6>;
+using C2 = Cfg<16, 32, 32, 3, 1, true, false, false, 1, 4>;
+using C3 = Cfg<8, 32, 64, 3, 2, false, false, false, 1, 4>;
+using C4 = Cfg<8, 64, 64, 3, 2, true, true, true, 2, 3>;
 
 // Per K-step A-descriptor low word (start-address and LBO fields, 16-byte
 // units) relative to the plane base of the step's kd.
@@ -210,11 +236,11 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
   unsigned char* wsm = smem;
   unsigned char* ring = smem + L::RING_OFF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
-  uint64_t* full = bars;                   // [RING]
-  uint64_t* empty = bars + L::RING;        // [RING]
-  uint64_t* tfull = bars + 2 * L::RING;    // [2]
-  uint64_t* tempty = tfull + 2;            // [2]
-  uint64_t* wbar = tempty + 2;             // [1]
+  uint64_t* full = bars;                   // [RING]   plane staged
+  uint64_t* empty = bars + L::RING;        // [RING]   plane's MMAs done
+  uint64_t* tfull = bars + 2 * L::RING;    // [kSlots] output plane accumulated
+  uint64_t* tempty = tfull + kSlots;       // [kSlots] slot drained and zeroed
+  uint64_t* wbar = tempty + kSlots;        // [1]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wbar + 1);
 
   const int nsl = blockIdx.y;              // N slice
@@ -222,7 +248,7 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < L::RING; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
+    for (int i = 0; i < kSlots; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
     mbar_init(wbar, 1);
     fence_barrier_init();
   }
@@ -260,59 +286,65 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
     }
   } else if (warp == 1) {
     // ===================== UMMA issuer =====================
-    // The whole warp walks the schedule (so descriptor math stays warp-
-    // uniform) and lane 0 issues.  Descriptor words are built from
-    // compile-time per-step offsets: one integer add per MMA.
+    // The whole warp walks the schedule (descriptor math stays warp-uniform)
+    // and lane 0 issues.  Input plane q: one stacked MMA per step and tile
+    // (two where the output planes q-KS+1..q wrap around the slot ring).
     mbar_wait(wbar, 0);
     const uint32_t wbase = smem_u32(wsm);
     const uint32_t rbase = smem_u32(ring);
     constexpr uint32_t A_HI = ((L::SBO >> 4) & 0x3FFFu) | (1u << 14);
     constexpr uint32_t B_HI = (128u >> 4) | (1u << 14);
     constexpr uint32_t A_LBO = (L::CIN == 8) ? 0u : ((static_cast<uint32_t>(L::CHUNK_BYTES) >> 4) << 16);
-    constexpr uint32_t B_STEP = (2u * L::NG * 128u) >> 4;
-    const uint32_t b_lo0 = ((wbase >> 4) & 0x3FFFu) | (((L::NG * 128u) >> 4) << 16);
-    uint32_t gq0 = 0, ac = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      for (int d = 0; d < L::G; ++d, ++ac) {
-        // planes d .. d+KS-1 of this unit must be resident
-        const int qlo = d == 0 ? 0 : d + L::KS - 1;
-        for (int q = qlo; q <= d + L::KS - 1; ++q) {
-          const uint32_t g = gq0 + q;
-          mbar_wait(&full[g % L::RING], (g / L::RING) & 1);
+    constexpr uint32_t B_STEP = L::STEP_BYTES >> 4;
+    constexpr uint32_t B_J = L::JSTEP >> 4;
+    const uint32_t b_lo0 = ((wbase >> 4) & 0x3FFFu) | (((L::KS * L::JSTEP) >> 4) << 16);
+    uint32_t gq = 0, uo = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, uo += L::G) {
+      for (int q = 0; q < L::NPLANES; ++q, ++gq) {
+        const uint32_t rs = gq % L::RING;
+        mbar_wait(&full[rs], (gq / L::RING) & 1);
+        const int dlo = q - L::KS + 1 > 0 ? q - L::KS + 1 : 0;
+        const int dhi = q < L::G - 1 ? q : L::G - 1;
+        if (q < L::G) {   // output plane q enters: its slot must be drained and zeroed
+          const uint32_t o = uo + q;
+          mbar_wait(&tempty[o % kSlots], (o / kSlots) & 1);
         }
-        const int a = ac & 1;
-        mbar_wait(&tempty[a], ((ac >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t slot0 = (gq0 + d) % L::RING;
+        // [dlo, dhi] split where it crosses a multiple of kSlots (G % kSlots == 0,
+        // so output d of every unit lives in slot d % kSlots)
+        const int dmid = (dlo / kSlots + 1) * kSlots;      // first plane of the next slot cycle
+        const int nseg = dhi >= dmid ? 2 : 1;
+        const uint32_t pbase = rbase + rs * L::PLANE_BYTES;
+#pragma unroll 1
+        for (int sg = 0; sg < nseg; ++sg) {
+          const int a = sg == 0 ? dlo : dmid;
+          const int b = sg == 0 ? (nseg == 2 ? dmid - 1 : dhi) : dhi;
+          const uint32_t idesc = idesc_bf16(128, (b - a + 1) * L::NCTA);
+          const uint32_t j0 = static_cast<uint32_t>(L::KS - 1 - q + a);   // kd = q - a, stored descending
 #pragma unroll
-        for (int wh = 0; wh < L::TILES; ++wh) {
-          const uint32_t dtm = tmem_base + a * L::ACC_COLS + wh * L::NCTA;
-#pragma unroll
-          for (int kd = 0; kd < L::KS; ++kd) {
-            uint32_t slot = slot0 + kd;
-            if (slot >= static_cast<uint32_t>(L::RING)) slot -= L::RING;
-            const uint32_t a_lo0 = (((rbase + slot * L::PLANE_BYTES + wh * 128u) >> 4) & 0x3FFFu) | A_LBO;
+          for (int wh = 0; wh < L::TILES; ++wh) {
+            const uint32_t dtm = tmem_base + (wh * kSlots + (a % kSlots)) * L::SLOT_COLS;
+            const uint32_t a_lo0 = (((pbase + wh * 128u) >> 4) & 0x3FFFu) | A_LBO;
+            const uint32_t b_lo1 = b_lo0 + j0 * B_J;
 #pragma unroll
             for (int s2 = 0; s2 < L::STEPS_PER_PLANE; ++s2) {
               const uint32_t a_lo = a_lo0 + a_step_lo<L>(s2);
-              const uint32_t b_lo = b_lo0 + (kd * L::STEPS_PER_PLANE + s2) * B_STEP;
+              const uint32_t b_lo = b_lo1 + s2 * B_STEP;
               if (lane == 0)
                 umma_bf16(dtm, (static_cast<uint64_t>(A_HI) << 32) | a_lo,
-                          (static_cast<uint64_t>(B_HI) << 32) | b_lo, L::IDESC, (kd | s2) != 0 ? 1u : 0u);
+                          (static_cast<uint64_t>(B_HI) << 32) | b_lo, idesc, 1u);
             }
           }
         }
         if (lane == 0) {
-          umma_commit(&tfull[a]);
-          // padded plane d is not read by later outputs of this unit
-          umma_commit(&empty[slot0]);
+          umma_commit(&empty[rs]);                         // plane q is read by no later MMA
+          if (q >= L::KS - 1) {                            // output plane q-KS+1 is complete
+            const uint32_t o = uo + q - L::KS + 1;
+            umma_commit(&tfull[o % kSlots]);
+          }
         }
         __syncwarp();
       }
-      if (lane == 0)
-        for (int q = L::G; q < L::NPLANES; ++q) umma_commit(&empty[(gq0 + q) % L::RING]);
-      __syncwarp();
-      gq0 += L::NPLANES;
     }
   } else {
     // ===================== epilogue (warps 2..5) =====================
@@ -321,26 +353,39 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
     const int grp = r >> 3, wl = r & 7;
     const int h = grp / L::POSES, ps = grp % L::POSES;
     const int n0 = nsl * L::NCTA;
+    const uint32_t tq = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+    // every slot starts zeroed (MMAs always accumulate)
+#pragma unroll 1
+    for (int s = 0; s < kSlots; ++s)
+#pragma unroll
+      for (int wh = 0; wh < L::TILES; ++wh)
+#pragma unroll
+        for (int c0 = 0; c0 < L::NCTA; c0 += 32) tmem_zero32(tq + (wh * kSlots + s) * L::SLOT_COLS + c0);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    for (int s = 0; s < kSlots; ++s) mbar_arrive(&tempty[s]);
     float bias[L::NCTA];
 #pragma unroll
     for (int j = 0; j < L::NCTA; ++j) bias[j] = prm.bias[n0 + j];
     float pmax[L::POOL ? L::TILES * L::NCTA : 1];
-    uint32_t ac = 0;
+    uint32_t o = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int pose = u * L::POSES + ps;
       const bool live = pose < prm.n_poses;
-      for (int d = 0; d < L::G; ++d, ++ac) {
-        const int a = ac & 1;
-        mbar_wait(&tfull[a], (ac >> 1) & 1);
+      for (int d = 0; d < L::G; ++d, ++o) {
+        const int slot = o % kSlots;
+        mbar_wait(&tfull[slot], (o / kSlots) & 1);
         tc_fence_after();
 #pragma unroll
         for (int wh = 0; wh < L::TILES; ++wh) {
           const int w = wh * 8 + wl;
           float v[L::NCTA];
 #pragma unroll
-          for (int c0 = 0; c0 < L::NCTA; c0 += 32)
-            tmem_ld32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + a * L::ACC_COLS + wh * L::NCTA + c0,
-                      v + c0);
+          for (int c0 = 0; c0 < L::NCTA; c0 += 32) {
+            const uint32_t ta = tq + (wh * kSlots + slot) * L::SLOT_COLS + c0;
+            tmem_ld32(ta, v + c0);
+            tmem_zero32(ta);
+          }
 #pragma unroll
           for (int j = 0; j < L::NCTA; ++j) v[j] = fmaxf(v[j] + bias[j], 0.0f);
           // chunk-major activations: [pose][C/8][d][h][w][8]
@@ -412,8 +457,9 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
             }
           }
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
-        mbar_arrive(&tempty[a]);
+        mbar_arrive(&tempty[slot]);
       }
     }
   }
@@ -476,7 +522,7 @@ static int launch_layer(const void* in, ConvParams prm, cudaStream_t st) {
   FS_CUDA_CHECK(cudaFuncSetAttribute(conv_umma_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
   const int units = (prm.n_poses + L::POSES - 1) / L::POSES;
   static const bool one_per_sm = getenv("FS_UMMA_ONE_CTA_PER_SM") != nullptr;
-  const int per_sm = (!one_per_sm && (227 * 1024) / (L::SMEM + 1024) >= 2) ? 2 : 1;
+  const int per_sm = (!one_per_sm && L::TMEM_COLS <= 256 && (227 * 1024) / (L::SMEM + 1024) >= 2) ? 2 : 1;
   const int ctas = max(1, min(units, g_num_sms * per_sm / L::NSPLIT));
   dim3 grid(ctas, L::NSPLIT);
   conv_umma_kernel<L><<<grid, 192, L::SMEM, st>>>(map, prm);
@@ -506,7 +552,10 @@ static uint16_t to_bf16(double x) {
   return static_cast<uint16_t>(u >> 16);
 }
 
-// B operand layout per N slice: [kstep][kchunk 2][n-group][8 rows][8 ch] bf16.
+// B operand layout per N slice: [step (kh,kw,chunk)][kchunk 2][kd descending]
+// [n-group][8 rows][8 ch] bf16 -- the N rows of one step are the KS kernel
+// planes side by side, so a stacked MMA over output planes a..b of input
+// plane q reads the contiguous rows of kd = q-a down to q-b.
 template <class L>
 static void pack_layer(const double* w, char* out) {
   // w: reference [O][C][k][k][k]
@@ -514,23 +563,23 @@ static void pack_layer(const double* w, char* out) {
   for (int sl = 0; sl < L::NSPLIT; ++sl) {
     uint16_t* o = reinterpret_cast<uint16_t*>(out + static_cast<size_t>(sl) * L::W_BYTES);
     std::memset(o, 0, L::W_BYTES);
-    for (int kd = 0; kd < K; ++kd)
-      for (int s = 0; s < L::STEPS_PER_PLANE; ++s)
-        for (int kc = 0; kc < 2; ++kc) {
-          int kh, kw, c0;
-          if constexpr (L::CIN == 8) {
-            const int off = 2 * s + kc;
-            if (off >= K * K) continue;     // zero-weight dummy chunk
-            kh = off / K; kw = off % K; c0 = 0;
-          } else {
-            constexpr int CP = L::CIN / 16;
-            const int cp = s % CP, off = s / CP;
-            kh = off / K; kw = off % K; c0 = 16 * cp + 8 * kc;
-          }
-          const int ks = kd * L::STEPS_PER_PLANE + s;
+    for (int s = 0; s < L::STEPS_PER_PLANE; ++s)
+      for (int kc = 0; kc < 2; ++kc) {
+        int kh, kw, c0;
+        if constexpr (L::CIN == 8) {
+          const int off = 2 * s + kc;
+          if (off >= K * K) continue;     // zero-weight dummy chunk
+          kh = off / K; kw = off % K; c0 = 0;
+        } else {
+          constexpr int CP = L::CIN / 16;
+          const int cp = s % CP, off = s / CP;
+          kh = off / K; kw = off % K; c0 = 16 * cp + 8 * kc;
+        }
+        for (int j = 0; j < K; ++j) {
+          const int kd = K - 1 - j;
           for (int n = 0; n < L::NCTA; ++n) {
             const int oc = sl * L::NCTA + n;
-            const size_t core = (static_cast<size_t>(ks) * 2 + kc) * L::NG + n / 8;
+            const size_t core = ((static_cast<size_t>(s) * 2 + kc) * K + j) * L::NG + n / 8;
             for (int e = 0; e < 8; ++e) {
               const int ic = c0 + e;
               const double v = w[((((size_t)oc * C + ic) * K + kd) * K + kh) * K + kw];
@@ -538,6 +587,7 @@ static void pack_layer(const double* w, char* out) {
             }
           }
         }
+      }
   }
 }
 
