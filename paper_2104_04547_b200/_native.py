@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfusionb200.so")
+# FS_LIB: an alternative in-tree build (A/B kernel experiments)
+LIB_PATH = os.environ.get("FS_LIB") or os.path.join(HERE, "libfusionb200.so")
 
 FS_OK, FS_EINVAL, FS_ECAPACITY, FS_ECUDA, FS_ENOTSUP = 0, -1, -2, -3, -4
 FS_ERR_ROLE, FS_ERR_NAN, FS_ERR_NONFINITE, FS_ERR_EDGE_CAP, FS_ERR_TOO_LARGE = 1, 2, 4, 8, 16

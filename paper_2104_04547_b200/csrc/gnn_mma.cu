@@ -119,6 +119,16 @@ __device__ __forceinline__ void build_a48(const float (&L)[2][6], const float (&
   put_a<SPLIT>(hi[2], lo[2], 3, R[1][4], R[1][5]);
 }
 
+__device__ __forceinline__ void mma_bf16_c(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
+                                           const float (&c)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%11,%12,%13};"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c[0]), "f"(c[1]), "f"(c[2]),
+        "f"(c[3]));
+}
+
 template <int SPLIT, int NT>
 __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[3][4], const uint32_t (&alo)[3][4],
                                        const uint32_t* __restrict__ fhi, const uint32_t* __restrict__ flo,
@@ -149,13 +159,27 @@ constexpr int kHeavyDeg = 32;
 constexpr int kBins = kHeavyDeg + 1;
 constexpr int kCtlWords = 6 + 2 * kBins;
 
-__device__ __forceinline__ void acc_row(float (&a)[6], const float* __restrict__ src) {
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const float2 v = *reinterpret_cast<const float2*>(src + 8 * k);
-    a[2 * k] += v.x; a[2 * k + 1] += v.y;
-  }
+// Node-state rows are stored lane-major: the 6 columns lane t owns in the
+// MMA fragments ({2t,2t+1, 8+2t,9+2t, 16+2t,17+2t}) sit contiguously at
+// 6t..6t+5, so a gathered row is two loads per lane (one 16-byte, one
+// 8-byte) instead of three 8-byte ones, with fewer bank conflicts.  The
+// 16-byte half is at 6t (t even) or 6t+2 (t odd); sums are kept in that
+// storage order and mapped to fragment order once per row.
+__device__ __forceinline__ void acc_row(float (&q)[4], float (&d)[2], const float* __restrict__ row, int t) {
+  const float* b = row + 6 * t;
+  const float4 v = *reinterpret_cast<const float4*>(b + ((t & 1) << 1));
+  const float2 w = *reinterpret_cast<const float2*>(b + ((t & 1) ? 0 : 4));
+  q[0] += v.x; q[1] += v.y; q[2] += v.z; q[3] += v.w;
+  d[0] += w.x; d[1] += w.y;
 }
+__device__ __forceinline__ void frag_order(const float (&q)[4], const float (&d)[2], int t, float (&o)[6]) {
+  const bool odd = t & 1;
+  o[0] = odd ? d[0] : q[0]; o[1] = odd ? d[1] : q[1];
+  o[2] = odd ? q[0] : q[2]; o[3] = odd ? q[1] : q[3];
+  o[4] = odd ? q[2] : d[0]; o[5] = odd ? q[3] : d[1];
+}
+// storage position of natural column c (c = 8k + 2t + e -> 6t + 2k + e)
+__host__ __device__ constexpr int hpos(int c) { return 6 * ((c % 8) / 2) + 2 * (c / 8) + (c % 2); }
 
 template <int SPLIT, bool FACT, int kMmaWarps>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a) {
@@ -197,6 +221,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
 #define COLS(c) ((c) < 2 ? 2 * t + (c) : (c) < 4 ? 6 + 2 * t + (c) : 12 + 2 * t + (c))
+#define PCOL(c) (6 * t + (c))   // storage position of the lane's c-th state column
 
   // ---- embedding h0 = tanh(X.We + be) into both buffers (rows a phase does
   // not update must read the same in either); padded rows and row npad are
@@ -242,10 +267,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         }
       }
     }
+    float hv[24];   // storage order
+#pragma unroll
+    for (int c = 0; c < 24; ++c) hv[hpos(c)] = emb ? fs_tanh(acc[c]) : 0.f;
 #pragma unroll
     for (int k = 0; k < 24; k += 4) {
-      const float4 v = emb ? make_float4(fs_tanh(acc[k]), fs_tanh(acc[k + 1]), fs_tanh(acc[k + 2]), fs_tanh(acc[k + 3]))
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v = make_float4(hv[k], hv[k + 1], hv[k + 2], hv[k + 3]);
       *reinterpret_cast<float4*>(Hc + i * 24 + k) = v;
       *reinterpret_cast<float4*>(Hn + i * 24 + k) = v;
     }
@@ -300,13 +327,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   auto load_h = [&](int row, float (&h)[6]) {
 #pragma unroll
     for (int c = 0; c < 6; c += 2) {
-      const float2 hv = *reinterpret_cast<const float2*>(Hc + row * 24 + COLS(c));
+      const float2 hv = *reinterpret_cast<const float2*>(Hc + row * 24 + PCOL(c));
       h[c] = hv.x; h[c + 1] = hv.y;
     }
   };
   auto store_hn = [&](int row, const float (&v)[6]) {
 #pragma unroll
-    for (int c = 0; c < 6; c += 2) *reinterpret_cast<float2*>(Hn + row * 24 + COLS(c)) = make_float2(v[c], v[c + 1]);
+    for (int c = 0; c < 6; c += 2) *reinterpret_cast<float2*>(Hn + row * 24 + PCOL(c)) = make_float2(v[c], v[c + 1]);
   };
 
   int gstep = 0;
@@ -378,14 +405,15 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           const int row = PERM[item];
           const int d = degs[base + row];
           const col_t* c = colv + rows[base + row];
-          float s6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          float sq[4] = {0.f, 0.f, 0.f, 0.f}, sd[2] = {0.f, 0.f};
           for (int q = g; q < d; q += 32) {
             int j[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) j[u] = q + 8 * u < d ? __ldg(c + q + 8 * u) : npad;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc_row(s6, Hc + j[u] * 24 + 2 * t);
+            for (int u = 0; u < 4; ++u) acc_row(sq, sd, Hc + j[u] * 24, t);
           }
+          float s6[6] = {sq[0], sq[1], sq[2], sq[3], sd[0], sd[1]};   // storage order
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
             float v = s6[k];
@@ -395,9 +423,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             s6[k] = v;
           }
           if (g == 0) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-              *reinterpret_cast<float2*>(HS + item * 24 + 2 * t + 8 * k) = make_float2(s6[2 * k], s6[2 * k + 1]);
+            float* b = HS + item * 24 + 6 * t;
+            *reinterpret_cast<float4*>(b + ((t & 1) << 1)) = make_float4(s6[0], s6[1], s6[2], s6[3]);
+            *reinterpret_cast<float2*>(b + ((t & 1) ? 0 : 4)) = make_float2(s6[4], s6[5]);
           }
           __syncwarp();
           if (lane == 0) { __threadfence_block(); atomicAdd(hdone, 1); }
@@ -412,7 +440,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           const col_t* c0 = colv + (r0 < n ? rows[base + r0] : 0);
           const col_t* c1 = colv + (r1 < n ? rows[base + r1] : 0);
           const int dm = max(d0, d1);
-          float sv[2][6] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}};
+          float sq[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}}, sd[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
           int q = 0;
           for (; q + 8 <= dm; q += 8) {
             int j0[8], j1[8];
@@ -422,8 +450,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             for (int u = 0; u < 8; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-              acc_row(sv[0], Hc + j0[u] * 24 + 2 * t);
-              acc_row(sv[1], Hc + j1[u] * 24 + 2 * t);
+              acc_row(sq[0], sd[0], Hc + j0[u] * 24, t);
+              acc_row(sq[1], sd[1], Hc + j1[u] * 24, t);
             }
           }
           for (; q < dm; q += 4) {
@@ -434,11 +462,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             for (int u = 0; u < 4; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              acc_row(sv[0], Hc + j0[u] * 24 + 2 * t);
-              acc_row(sv[1], Hc + j1[u] * 24 + 2 * t);
+              acc_row(sq[0], sd[0], Hc + j0[u] * 24, t);
+              acc_row(sq[1], sd[1], Hc + j1[u] * 24, t);
             }
           }
-          // acc_row's column order (2t + 8k, +1) is COLS
+          float sv[2][6];
+          frag_order(sq[0], sd[0], t, sv[0]);
+          frag_order(sq[1], sd[1], t, sv[1]);
           float h[2][6], hn[2][6];
           load_h(r0, h[0]);
           load_h(r1, h[1]);
@@ -458,8 +488,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           float sv[2][6], h[2][6], hn[2][6];
 #pragma unroll
           for (int c = 0; c < 6; c += 2) {
-            const float2 v0 = i0 < nh ? *reinterpret_cast<const float2*>(HS + i0 * 24 + COLS(c)) : make_float2(0.f, 0.f);
-            const float2 v1 = i1 < nh ? *reinterpret_cast<const float2*>(HS + i1 * 24 + COLS(c)) : make_float2(0.f, 0.f);
+            const float2 v0 = i0 < nh ? *reinterpret_cast<const float2*>(HS + i0 * 24 + PCOL(c)) : make_float2(0.f, 0.f);
+            const float2 v1 = i1 < nh ? *reinterpret_cast<const float2*>(HS + i1 * 24 + PCOL(c)) : make_float2(0.f, 0.f);
             sv[0][c] = v0.x; sv[0][c + 1] = v0.y;
             sv[1][c] = v1.x; sv[1][c + 1] = v1.y;
           }
@@ -490,10 +520,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   // gather fragments: stage into the (now free) neighbour-sum buffer when it
   // is large enough, else read them through L1
   const uint32_t* gsrc = a.gfrag;
-  if (hrows * 24 >= kGatherWords) {
+  const float* gb = a.gbias;
+  if (hrows * 24 >= kGatherWords + 256) {
     uint32_t* gs = reinterpret_cast<uint32_t*>(Hn);
     for (int i = threadIdx.x; i < kGatherWords; i += blockDim.x) gs[i] = a.gfrag[i];
+    float* gbs = reinterpret_cast<float*>(gs + kGatherWords);
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) gbs[i] = a.gbias[i];
     gsrc = gs;
+    gb = gbs;
   }
   __syncthreads();
   const uint32_t* g_hi = gsrc;
@@ -505,7 +539,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       const int row = tile * 16 + g + 8 * rr;
 #pragma unroll
       for (int c = 0; c < 6; c += 2) {
-        const float2 hv = *reinterpret_cast<const float2*>(Hc + row * 24 + COLS(c));
+        const float2 hv = *reinterpret_cast<const float2*>(Hc + row * 24 + PCOL(c));
         h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
       }
     }
@@ -520,22 +554,29 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     const bool v0 = valid(tile * 16 + g), v1 = valid(tile * 16 + g + 8);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      float Dg[4] = {0.f, 0.f, 0.f, 0.f}, Dv[4] = {0.f, 0.f, 0.f, 0.f};
-      // k 0..15: m16n8k16; k 16..23: m16n8k8 (the k16 fragments' first
-      // registers; rows 24..31 are zero padding)
+      // biases enter as the first MMA's C operand
+      float Dg[4], Dv[4];
       {
+        const float2 bg = *reinterpret_cast<const float2*>(gb + 8 * j + 2 * t);
+        const float2 bv = *reinterpret_cast<const float2*>(gb + 128 + 8 * j + 2 * t);
+        const float Cg[4] = {bg.x, bg.y, bg.x, bg.y}, Cv[4] = {bv.x, bv.y, bv.x, bv.y};
+        // k 0..15: m16n8k16; k 16..23: m16n8k8 (the k16 fragments' first
+        // registers; rows 24..31 are zero padding)
         const uint2 bgh = *reinterpret_cast<const uint2*>(g_hi + (j * 32 + lane) * 2);
         const uint2 bvh = *reinterpret_cast<const uint2*>(g_hi + ((16 + j) * 32 + lane) * 2);
         if (SPLIT == 3) {
           const uint2 bgl = *reinterpret_cast<const uint2*>(g_lo + (j * 32 + lane) * 2);
           const uint2 bvl = *reinterpret_cast<const uint2*>(g_lo + ((16 + j) * 32 + lane) * 2);
-          mma_bf16(Dg, alo[0], bgh.x, bgh.y);
-          mma_bf16(Dv, alo[0], bvh.x, bvh.y);
+          mma_bf16_c(Dg, alo[0], bgh.x, bgh.y, Cg);
+          mma_bf16_c(Dv, alo[0], bvh.x, bvh.y, Cv);
           mma_bf16(Dg, ahi[0], bgl.x, bgl.y);
           mma_bf16(Dv, ahi[0], bvl.x, bvl.y);
+          mma_bf16(Dg, ahi[0], bgh.x, bgh.y);
+          mma_bf16(Dv, ahi[0], bvh.x, bvh.y);
+        } else {
+          mma_bf16_c(Dg, ahi[0], bgh.x, bgh.y, Cg);
+          mma_bf16_c(Dv, ahi[0], bvh.x, bvh.y, Cv);
         }
-        mma_bf16(Dg, ahi[0], bgh.x, bgh.y);
-        mma_bf16(Dv, ahi[0], bvh.x, bvh.y);
       }
       {
         const uint32_t bgh = g_hi[((32 + j) * 32 + lane) * 2];
@@ -554,9 +595,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = 8 * j + 2 * t + e;
-        const float bgv = __ldg(a.gbias + col), bfv = __ldg(a.gbias + 128 + col);
-        const float x0 = v0 ? fs_sigmoid_pre(Dg[e] + bgv) * fs_tanh_pre(Dv[e] + bfv) : 0.f;
-        const float x1 = v1 ? fs_sigmoid_pre(Dg[2 + e] + bgv) * fs_tanh_pre(Dv[2 + e] + bfv) : 0.f;
+        const float x0 = v0 ? fs_sigmoid_pre(Dg[e]) * fs_tanh_pre(Dv[e]) : 0.f;
+        const float x1 = v1 ? fs_sigmoid_pre(Dg[2 + e]) * fs_tanh_pre(Dv[2 + e]) : 0.f;
         acc[j][e] += x0 + x1;
         if (!FACT && a.dump_f) {   // pocket preparation: per-node pool terms
           float* o = a.dump_f + (static_cast<int64_t>(p) * a.dump_ld + tile * 16 + g) * 128 + col;
