@@ -107,6 +107,7 @@ struct GnnMmaArgs {
   const char* cache; int64_t cache_stride; int64_t off_hcov, off_f, off_T, off_n;
   float* dump_hcov; float* dump_f; int64_t dump_ld;
   int heavy_cap;
+  int ids_padded;
 };
 int gnn_mma_phase_words();
 int gnn_mma_gather_words();
@@ -619,9 +620,10 @@ static int voxel_tail(const fs_model& m, int P, char* ws, const WsPlan& w, bool 
   return FS_OK;
 }
 
+// ids_padded: the CSR came from graph_csr/graph_fact (rows padded to 4 ids)
 static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const WsPlan& w,
                       const int32_t* err, bool want_pred, int precision, cudaStream_t st,
-                      const GnnMmaArgs* extra = nullptr) {
+                      const GnnMmaArgs* extra = nullptr, bool ids_padded = true) {
   GnnArgs g{};
   g.feats = (float*)(ws + w.feats); g.F = m.F; g.node_off = (int64_t*)(ws + w.node_off);
   g.row_cov = (int64_t*)(ws + w.row_cov); g.col_cov = (col_t*)(ws + w.col_cov);
@@ -648,6 +650,7 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
     q.gfrag = reinterpret_cast<const uint32_t*>(m.P(m.gm_gf)); q.gbias = m.P(m.gm_gb);
     q.k_steps[0] = m.d.k_cov; q.k_steps[1] = m.d.k_noncov;
     q.lat = g.lat; q.ld_lat = g.ld_lat; q.err = err;
+    q.ids_padded = ids_padded ? 1 : 0;
     // bf16 hi/lo 3-pass (fp32-class, default) or single bf16 pass (FS_GNN_SPLIT=1)
     static const int split = (getenv("FS_GNN_SPLIT") && atoi(getenv("FS_GNN_SPLIT")) == 1) ? 1 : 3;
     rc = launch_gnn_mma(q, split, P, max_nodes, st);
@@ -1105,7 +1108,7 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const d
     // max nodes per pose bounds the GNN's shared-memory state; the host
     // passes it implicitly via n_nodes (worst case: one pose holds them all)
     int max_nodes = (int)(n_nodes < FS_MAX_POSE_ATOMS ? n_nodes : FS_MAX_POSE_ATOMS);
-    if ((rc = graph_head(*m, P, max_nodes, W, w, err, late || pred_g, precision, st))) return rc;
+    if ((rc = graph_head(*m, P, max_nodes, W, w, err, late || pred_g, precision, st, nullptr, false))) return rc;
   }
   if (want_f) {
     if (!late && (rc = fusion_head(*m, P, W, w, scores, st))) return rc;

@@ -52,6 +52,7 @@ struct GnnMmaArgs {
   // phase [P][dump_ld][24] and per-node pool terms [P][dump_ld][128]
   float* dump_hcov; float* dump_f; int64_t dump_ld;
   int heavy_cap;                          // rows of the heavy-sum buffer (set by launch_gnn_mma)
+  int ids_padded;                         // CSR rows padded to 4 ids with the zero row (graph_csr.cu)
 };
 
 constexpr int kMaxMmaWarps = 24;   // smem reduction buffers are sized for this many warps
@@ -439,31 +440,56 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           const int d0 = r0 < n ? degs[base + r0] : 0, d1 = r1 < n ? degs[base + r1] : 0;
           const col_t* c0 = colv + (r0 < n ? rows[base + r0] : 0);
           const col_t* c1 = colv + (r1 < n ? rows[base + r1] : 0);
-          const int dm = max(d0, d1);
           float sq[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}}, sd[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
-          int q = 0;
-          for (; q + 8 <= dm; q += 8) {
-            int j0[8], j1[8];
+          if (a.ids_padded) {
+            // rows padded to 4 ids with the zero row `npad` (graph_csr.cu):
+            // ids come 4 at a time; past a row's padded extent the lane reads
+            // row npad (x + 0 == x: sums stay exactly CSR-ordered)
+            const int e0 = (d0 + 3) & ~3, e1 = (d1 + 3) & ~3;
+            const int dm = max(e0, e1);
+            auto ids4 = [&](const col_t* c, int q, int e, int* j) {
+              if (q < e) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(c + q));
+                j[0] = v.x & 0xffffu; j[1] = v.x >> 16; j[2] = v.y & 0xffffu; j[3] = v.y >> 16;
+              } else {
+                j[0] = j[1] = j[2] = j[3] = npad;
+              }
+            };
+            int q = 0;
+            for (; q + 8 <= dm; q += 8) {
+              int j0[8], j1[8];
+              ids4(c0, q, e0, j0); ids4(c0, q + 4, e0, j0 + 4);
+              ids4(c1, q, e1, j1); ids4(c1, q + 4, e1, j1 + 4);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) j0[u] = q + u < d0 ? __ldg(c0 + q + u) : npad;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              acc_row(sq[0], sd[0], Hc + j0[u] * 24, t);
-              acc_row(sq[1], sd[1], Hc + j1[u] * 24, t);
+              for (int u = 0; u < 8; ++u) {
+                acc_row(sq[0], sd[0], Hc + j0[u] * 24, t);
+                acc_row(sq[1], sd[1], Hc + j1[u] * 24, t);
+              }
             }
-          }
-          for (; q < dm; q += 4) {
-            int j0[4], j1[4];
+            if (q < dm) {
+              int j0[4], j1[4];
+              ids4(c0, q, e0, j0);
+              ids4(c1, q, e1, j1);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) j0[u] = q + u < d0 ? __ldg(c0 + q + u) : npad;
+              for (int u = 0; u < 4; ++u) {
+                acc_row(sq[0], sd[0], Hc + j0[u] * 24, t);
+                acc_row(sq[1], sd[1], Hc + j1[u] * 24, t);
+              }
+            }
+          } else {
+            // packed CSR (rows built from reference edge lists): one id per load
+            const int dm = max(d0, d1);
+            for (int q = 0; q < dm; q += 4) {
+              int j0[4], j1[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
+              for (int u = 0; u < 4; ++u) j0[u] = q + u < d0 ? __ldg(c0 + q + u) : npad;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              acc_row(sq[0], sd[0], Hc + j0[u] * 24, t);
-              acc_row(sq[1], sd[1], Hc + j1[u] * 24, t);
+              for (int u = 0; u < 4; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                acc_row(sq[0], sd[0], Hc + j0[u] * 24, t);
+                acc_row(sq[1], sd[1], Hc + j1[u] * 24, t);
+              }
             }
           }
           float sv[2][6];

@@ -428,6 +428,10 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     a.deg_cov[base + i] = offc[i];
     a.deg_ncov[base + i] = offn[i];
+    if (!DIST) {   // scoring path: rows padded to 4 entries (see pad_rows)
+      offc[i] = (offc[i] + 3) & ~3;
+      offn[i] = (offn[i] + 3) & ~3;
+    }
   }
   block_exclusive_scan(offc, n, warp_tot);
   block_exclusive_scan(offn, n, warp_tot);
@@ -494,6 +498,13 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
           ++o;
         }
       }
+    }
+  }
+  if (!DIST) {
+    const col_t padv = (col_t)((n + 15) & ~15);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int d = a.deg_ncov[base + i];
+      for (int k = offn[i] + d; k & 3; ++k) coln[k] = padv;
     }
   }
   // ---- fill covalent rows.  Scoring path (no distances): rows stay in the
@@ -572,6 +583,15 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       if (DIST) distc[y + 1] = dv;
     }
   }
+  if (!DIST) {
+    // pad covalent rows to 4 entries with the all-zero node-state row (the
+    // message-passing kernels read neighbour ids four at a time)
+    const col_t padv = (col_t)((n + 15) & ~15);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int d = a.deg_cov[base + i];
+      for (int k = offc[i] + d; k & 3; ++k) colc[k] = padv;
+    }
+  }
 }
 
 int launch_graph_csr(const fs_pose_batch& b, const int64_t* node_off, double tc, double tn, int64_t* row_cov,
@@ -583,7 +603,8 @@ int launch_graph_csr(const fs_pose_batch& b, const int64_t* node_off, double tc,
   a.b = b; a.node_off = node_off; a.tc = tc; a.tn = tn;
   a.row_cov = row_cov; a.deg_cov = deg_cov; a.col_cov = col_cov; a.dist_cov = dist_cov;
   a.row_ncov = row_ncov; a.deg_ncov = deg_ncov; a.col_ncov = col_ncov; a.dist_ncov = dist_ncov;
-  a.cap = cap; a.err = err;
+  // scoring path: pose slices start 4-aligned (rows are padded to 4 entries)
+  a.cap = (dist_cov || dist_ncov) ? cap : (cap & ~static_cast<int64_t>(3)); a.err = err;
   int atoms = b.max_pose_atoms > 0 ? b.max_pose_atoms : FS_MAX_POSE_ATOMS;
   if (atoms > FS_MAX_POSE_ATOMS) atoms = FS_MAX_POSE_ATOMS;
   a.smem_atoms = atoms;
@@ -741,7 +762,11 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
     if (c) offn[nLp + rank[j]] = c;
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < nc; r += blockDim.x) { a.deg_cov[nb + r] = offc[r]; a.deg_ncov[nb + r] = offn[r]; }
+  for (int r = threadIdx.x; r < nc; r += blockDim.x) {
+    a.deg_cov[nb + r] = offc[r]; a.deg_ncov[nb + r] = offn[r];
+    offc[r] = (offc[r] + 3) & ~3;   // rows padded to 4 entries (see the end)
+    offn[r] = (offn[r] + 3) & ~3;
+  }
   block_exclusive_scan(offc, nc, warp_tot);
   block_exclusive_scan(offn, nc, warp_tot);
   if (offc[nc] > a.cap || offn[nc] > a.cap) { give_up(FS_ERR_EDGE_CAP); return; }
@@ -809,6 +834,15 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
       }
     }
   }
+  // pad every row to 4 entries with the all-zero node-state row
+  __syncthreads();
+  {
+    const col_t padv = (col_t)((nc + 15) & ~15);
+    for (int r = threadIdx.x; r < nc; r += blockDim.x) {
+      for (int k = offc[r] + a.deg_cov[nb + r]; k & 3; ++k) colc[k] = padv;
+      for (int k = offn[r] + a.deg_ncov[nb + r]; k & 3; ++k) coln[k] = padv;
+    }
+  }
   // ligand node features, as node_features_kernel<float> (complexes.py:233-236)
   const int F = a.c_elem + 4;
   for (int s = threadIdx.x; s < nL; s += blockDim.x) {
@@ -831,7 +865,7 @@ int launch_graph_fact(const fs_pose_batch& b, double tc, double tn, double box, 
   if (!(tc >= 1.2 && tc <= 5.9) || !(tn >= 1.2 && tn <= 5.9)) return FS_EINVAL;
   if (b.n_poses <= 0) return FS_OK;
   GraphFactArgs a;
-  a.b = b; a.tc = tc; a.tn = tn; a.box = box; a.c_elem = c_elem; a.S = S; a.cap = cap;
+  a.b = b; a.tc = tc; a.tn = tn; a.box = box; a.c_elem = c_elem; a.S = S; a.cap = cap & ~static_cast<int64_t>(3);
   a.cnt = cnt; a.aff = aff; a.feats = feats;
   a.row_cov = row_cov; a.deg_cov = deg_cov; a.col_cov = col_cov;
   a.row_ncov = row_ncov; a.deg_ncov = deg_ncov; a.col_ncov = col_ncov;
