@@ -84,10 +84,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_idx, float hi_idx) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 // split a pair into (hi, lo) bf16x2 words
+__device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1);
 __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
   float2 hf = __bfloat1622float2(h);
-  __nv_bfloat162 l = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
+  fadd2(x0, x1, -hf.x, -hf.y);   // exact: x - bf16(x)
+  __nv_bfloat162 l = __floats2bfloat162_rn(x0, x1);
   hi = *reinterpret_cast<uint32_t*>(&h);
   lo = *reinterpret_cast<uint32_t*>(&l);
 }
@@ -166,12 +168,54 @@ constexpr int kCtlWords = 6 + 2 * kBins;
 // 8-byte) instead of three 8-byte ones, with fewer bank conflicts.  The
 // 16-byte half is at 6t (t even) or 6t+2 (t odd); sums are kept in that
 // storage order and mapped to fragment order once per row.
+// packed fp32 add (sm_100 FADD2): two IEEE round-to-nearest adds, bitwise
+// the same as two FADDs, one issue slot
+__device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1) {
+  asm("{\n.reg .b64 ra, rb;\n"
+      "mov.b64 ra, {%0, %1};\n"
+      "mov.b64 rb, {%2, %3};\n"
+      "add.rn.f32x2 ra, ra, rb;\n"
+      "mov.b64 {%0, %1}, ra;\n}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void fmul2(float& a0, float& a1, float b0, float b1) {
+  asm("{\n.reg .b64 ra, rb;\n"
+      "mov.b64 ra, {%0, %1};\n"
+      "mov.b64 rb, {%2, %3};\n"
+      "mul.rn.f32x2 ra, ra, rb;\n"
+      "mov.b64 {%0, %1}, ra;\n}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(b0), "f"(b1));
+}
+// a = a * b + c
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float b0, float b1, float c0, float c1) {
+  asm("{\n.reg .b64 ra, rb, rc;\n"
+      "mov.b64 ra, {%0, %1};\n"
+      "mov.b64 rb, {%2, %3};\n"
+      "mov.b64 rc, {%4, %5};\n"
+      "fma.rn.f32x2 ra, ra, rb, rc;\n"
+      "mov.b64 {%0, %1}, ra;\n}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+// (sigmoid, sigmoid) / (tanh, tanh) of a pre-scaled pair (see fs_sigmoid_pre)
+__device__ __forceinline__ void sigmoid_pre2(float& u0, float& u1) {
+  u0 = fs_ex2(u0); u1 = fs_ex2(u1);
+  fadd2(u0, u1, 1.0f, 1.0f);
+  u0 = fs_rcp(u0); u1 = fs_rcp(u1);
+}
+__device__ __forceinline__ void tanh_pre2(float& u0, float& u1) {
+  sigmoid_pre2(u0, u1);
+  ffma2(u0, u1, -2.0f, -2.0f, 1.0f, 1.0f);
+}
 __device__ __forceinline__ void acc_row(float (&q)[4], float (&d)[2], const float* __restrict__ row, int t) {
   const float* b = row + 6 * t;
   const float4 v = *reinterpret_cast<const float4*>(b + ((t & 1) << 1));
   const float2 w = *reinterpret_cast<const float2*>(b + ((t & 1) ? 0 : 4));
-  q[0] += v.x; q[1] += v.y; q[2] += v.z; q[3] += v.w;
-  d[0] += w.x; d[1] += w.y;
+  fadd2(q[0], q[1], v.x, v.y);
+  fadd2(q[2], q[3], v.z, v.w);
+  fadd2(d[0], d[1], w.x, w.y);
 }
 __device__ __forceinline__ void frag_order(const float (&q)[4], const float (&d)[2], int t, float (&o)[6]) {
   const bool odd = t & 1;
@@ -294,17 +338,21 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     float Dzr[6][4];
     gemm48<SPLIT, 6>(Dzr, ahi, alo, zr_hi, zr_lo, lane);
     // D n-tile j holds (row g: cols 8j+2t, 8j+2t+1; row g+8: same)
+    // elementwise work on column pairs (2j, 2j+1) with packed fp32 ops
     float z[2][6], rh[2][6];
 #pragma unroll
     for (int j = 0; j < 3; ++j)
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int c = 2 * j + e;
-          z[rr][c] = fs_sigmoid_pre(Dzr[j][2 * rr + e] + bz[c]);
-          rh[rr][c] = fs_sigmoid_pre(Dzr[3 + j][2 * rr + e] + br[c]) * h[rr][c];
-        }
+      for (int rr = 0; rr < 2; ++rr) {
+        const int c = 2 * j;
+        z[rr][c] = Dzr[j][2 * rr]; z[rr][c + 1] = Dzr[j][2 * rr + 1];
+        fadd2(z[rr][c], z[rr][c + 1], bz[c], bz[c + 1]);
+        sigmoid_pre2(z[rr][c], z[rr][c + 1]);
+        rh[rr][c] = Dzr[3 + j][2 * rr]; rh[rr][c + 1] = Dzr[3 + j][2 * rr + 1];
+        fadd2(rh[rr][c], rh[rr][c + 1], br[c], br[c + 1]);
+        sigmoid_pre2(rh[rr][c], rh[rr][c + 1]);
+        fmul2(rh[rr][c], rh[rr][c + 1], h[rr][c], h[rr][c + 1]);
+      }
     // A = [s | r*h]: the s part (k-tile 0 and half of k-tile 1) is reused
     put_a<SPLIT>(ahi[1], alo[1], 2, rh[0][0], rh[0][1]);
     put_a<SPLIT>(ahi[1], alo[1], 3, rh[1][0], rh[1][1]);
@@ -317,13 +365,16 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
-      for (int j = 0; j < 3; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = 2 * j + e;
-          const float hh = fs_tanh_pre(Dh[j][2 * rr + e] + bh[c]);
-          hn[rr][c] = ok[rr] ? fmaf(z[rr][c], hh - h[rr][c], h[rr][c]) : 0.f;
-        }
+      for (int j = 0; j < 3; ++j) {
+        const int c = 2 * j;
+        float u0 = Dh[j][2 * rr], u1 = Dh[j][2 * rr + 1];
+        fadd2(u0, u1, bh[c], bh[c + 1]);
+        tanh_pre2(u0, u1);                                 // hh
+        fadd2(u0, u1, -h[rr][c], -h[rr][c + 1]);          // hh - h
+        ffma2(u0, u1, z[rr][c], z[rr][c + 1], h[rr][c], h[rr][c + 1]);   // h + z (hh - h)
+        hn[rr][c] = ok[rr] ? u0 : 0.f;
+        hn[rr][c + 1] = ok[rr] ? u1 : 0.f;
+      }
   };
   auto load_h = [&](int row, float (&h)[6]) {
 #pragma unroll
@@ -619,15 +670,21 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         mma_bf16_k8(Dv, ahi[1][0], ahi[1][1], bvh);
       }
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = 8 * j + 2 * t + e;
-        const float x0 = v0 ? fs_sigmoid_pre(Dg[e]) * fs_tanh_pre(Dv[e]) : 0.f;
-        const float x1 = v1 ? fs_sigmoid_pre(Dg[2 + e]) * fs_tanh_pre(Dv[2 + e]) : 0.f;
-        acc[j][e] += x0 + x1;
+      {
+        // rows g (D[0], D[1]) and g+8 (D[2], D[3]), columns 8j+2t, +1
+        sigmoid_pre2(Dg[0], Dg[1]); sigmoid_pre2(Dg[2], Dg[3]);
+        tanh_pre2(Dv[0], Dv[1]); tanh_pre2(Dv[2], Dv[3]);
+        fmul2(Dg[0], Dg[1], Dv[0], Dv[1]);
+        fmul2(Dg[2], Dg[3], Dv[2], Dv[3]);
+        const float x00 = v0 ? Dg[0] : 0.f, x01 = v0 ? Dg[1] : 0.f;
+        const float x10 = v1 ? Dg[2] : 0.f, x11 = v1 ? Dg[3] : 0.f;
+        float s0 = x00, s1 = x01;
+        fadd2(s0, s1, x10, x11);
+        fadd2(acc[j][0], acc[j][1], s0, s1);
         if (!FACT && a.dump_f) {   // pocket preparation: per-node pool terms
-          float* o = a.dump_f + (static_cast<int64_t>(p) * a.dump_ld + tile * 16 + g) * 128 + col;
-          if (v0) o[0] = x0;
-          if (v1) o[8 * 128] = x1;
+          float* o = a.dump_f + (static_cast<int64_t>(p) * a.dump_ld + tile * 16 + g) * 128 + 8 * j + 2 * t;
+          if (v0) { o[0] = x00; o[1] = x01; }
+          if (v1) { o[8 * 128] = x10; o[8 * 128 + 1] = x11; }
         }
       }
     }
