@@ -55,7 +55,8 @@ int launch_edge_counts(const int64_t* node_off, int n_poses, const int64_t* row_
 int launch_edges(const int64_t* node_off, int n_poses, const int64_t* row_ptr, const int32_t* col, const double* dist, const int64_t* edge_off, int64_t* edges, double* dists, cudaStream_t st);
 int launch_graph_csr(const fs_pose_batch& b, const int64_t* node_off, double tc, double tn, int64_t* row_cov,
                      int32_t* deg_cov, col_t* col_cov, double* dist_cov, int64_t* row_ncov, int32_t* deg_ncov,
-                     col_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st);
+                     col_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st,
+                     float* feats = nullptr, int c_elem = 0, double box = 0.0);
 int launch_graph_fact(const fs_pose_batch& b, double tc, double tn, double box, int c_elem, int64_t S, int64_t cap,
                       int max_pocket, int32_t* cnt, int32_t* aff, float* feats, int64_t* row_cov, int32_t* deg_cov,
                       col_t* col_cov, int64_t* row_ncov, int32_t* deg_ncov, col_t* col_ncov, int32_t* err,
@@ -881,12 +882,12 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
     gst = ss->s;
   }
   // featurize (models.py:638-651)
-  if ((rc = launch_node_features(*b, node_off, d.c_elem, d.box_size, W + w.feats, false, gst))) return rc;
-  // radius graph: one fused launch, pose-private CSR slices of max_edges
-  // entries per edge type (rows = start offset + degree)
+  // radius graph + node features: one fused launch, pose-private CSR slices
+  // of max_edges entries per edge type (rows = start offset + degree)
   if ((rc = launch_graph_csr(*b, node_off, d.cov_thresh, d.noncov_thresh, (int64_t*)(W + w.row_cov),
                              (int32_t*)(W + w.deg_cov), (col_t*)(W + w.col_cov), nullptr, (int64_t*)(W + w.row_ncov),
-                             (int32_t*)(W + w.deg_ncov), (col_t*)(W + w.col_ncov), nullptr, max_edges, err, gst)))
+                             (int32_t*)(W + w.deg_ncov), (col_t*)(W + w.col_ncov), nullptr, max_edges, err, gst,
+                             (float*)(W + w.feats), d.c_elem, d.box_size)))
     return rc;
   if (ss) FS_CUDA_CHECK(cudaEventRecord(ss->join, gst));
   if (precision == FS_PREC_BF16) {

@@ -29,6 +29,8 @@ struct GraphCsrArgs {
   int64_t cap;          // entries per pose per edge type
   int32_t* err;
   int smem_atoms;
+  float* feats;         // optional node features [N][c_elem + 4] (node_features_kernel<float>)
+  int c_elem; double box;
 };
 
 constexpr int kCsrThreads = 256;
@@ -137,9 +139,19 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   // ---- atoms, validation, bounding box ----
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   int flags = 0;
+  float* fo = a.feats ? a.feats + base * (a.c_elem + 4) : nullptr;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double x, y, z; int32_t e, r;
     pv.atom(i, x, y, z, e, r);
+    if (fo) {   // node features (complexes.py:233-236), as node_features_kernel<float>
+      const int F = a.c_elem + 4, ec = min(max(e, 0), a.c_elem - 1);
+      float* f = fo + (int64_t)i * F;
+      for (int c = 0; c < a.c_elem; ++c) f[c] = c == ec ? 1.f : 0.f;
+      f[a.c_elem] = (float)r;
+      f[a.c_elem + 1] = (float)__dadd_rn(__ddiv_rn(x, a.box), 0.5);
+      f[a.c_elem + 2] = (float)__dadd_rn(__ddiv_rn(y, a.box), 0.5);
+      f[a.c_elem + 3] = (float)__dadd_rn(__ddiv_rn(z, a.box), 0.5);
+    }
     if (r != 0 && r != 1) flags |= FS_ERR_ROLE;
     if (!isfinite(x) || !isfinite(y) || !isfinite(z)) flags |= FS_ERR_NONFINITE;
     pf[i] = make_float4((float)x, (float)y, (float)z, (float)r);
@@ -596,10 +608,12 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
 
 int launch_graph_csr(const fs_pose_batch& b, const int64_t* node_off, double tc, double tn, int64_t* row_cov,
                      int32_t* deg_cov, col_t* col_cov, double* dist_cov, int64_t* row_ncov, int32_t* deg_ncov,
-                     col_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st) {
+                     col_t* col_ncov, double* dist_ncov, int64_t cap, int32_t* err, cudaStream_t st,
+                     float* feats, int c_elem, double box) {
   if (!(tc >= 1.2 && tc <= 5.9) || !(tn >= 1.2 && tn <= 5.9)) return FS_EINVAL;   // complexes.py:228-231
   if (b.n_poses <= 0) return FS_OK;
   GraphCsrArgs a;
+  a.feats = feats; a.c_elem = c_elem; a.box = box;
   a.b = b; a.node_off = node_off; a.tc = tc; a.tn = tn;
   a.row_cov = row_cov; a.deg_cov = deg_cov; a.col_cov = col_cov; a.dist_cov = dist_cov;
   a.row_ncov = row_ncov; a.deg_ncov = deg_ncov; a.col_ncov = col_ncov; a.dist_ncov = dist_ncov;
