@@ -475,6 +475,16 @@ def main():
                 roof["traffic_unit"] = "bytes per launch"
                 roof["traffic_source"] = ("profiles/r01/ncu_traffic.json: ncu --set full dram__bytes_read.sum + "
                                           "dram__bytes_write.sum of a 2048-pose launch, scaled per pose")
+                if dom_name == "gnn":
+                    # neither HBM nor the tensor pipe binds this kernel: its node
+                    # states never leave shared memory; the measured on-chip
+                    # pipe utilisation of the same capture says what does
+                    e = tr[tr_key]
+                    roof["onchip"] = {k: round(e[k], 1) for k in
+                                      ("smem_wavefront_pct", "issue_active_pct", "hmma_pipe_pct", "mufu_xu_pct",
+                                       "warps_active_pct") if k in e}
+                    roof["onchip"]["note"] = ("latency-bound gather + GRU chains at one pose per SM (228 KB of "
+                                              "fp32 node state); DESIGN.md section 3.2")
         except (OSError, ValueError):
             pass
         roof["frac"] = roof["achieved"] / roof["peak"]
