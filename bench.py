@@ -490,6 +490,10 @@ def main():
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["peak_kind"] = f"{peak_kind} bf16 sustained"
         roof["stage_ms_per_step"] = {n: round(v / K, 4) for n, v in zip(names, stage_ms)}
+        if os.environ.get("FS_OVERLAP", "2") == "2":
+            roof["stage_note"] = ("voxel branch (voxelize, conv1-4, dense) runs on a side stream concurrently "
+                                  "with the radius graph: featurize/conv/dense are event deltas across two "
+                                  "streams; gnn is exact")
         roof["dominant_share"] = float(stage_ms[dom] / stage_ms.sum())
         line = {"metric": METRIC, "value": value, "unit": "poses/s", "n_gpus": world, "steps": K, "warmup": W,
                 "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
