@@ -70,12 +70,14 @@ class Clocks:
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.mark_at = 0
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20",
                  "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.mark_at = 0
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -85,6 +87,14 @@ class Clocks:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def ready(self, timeout=5.0):
+        """Wait for the sampler's first line (nvidia-smi starts slowly), then
+        mark where the timed region's samples begin."""
+        t0 = time.perf_counter()
+        while self.proc and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+        self.mark_at = len(self.lines)
 
     def __exit__(self, *a):
         if self.proc:
@@ -97,7 +107,10 @@ class Clocks:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        # samples taken during the timed region (after ready()); a region
+        # shorter than the 20 ms sampling period falls back to the last one
+        lines = self.lines[self.mark_at:] or self.lines[-1:]
+        for ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -309,6 +322,7 @@ def main():
     launches0 = L.fs_launch_count()
     gc.disable()        # no collector pauses inside the timed regions
     with Clocks(local) as clk:
+        clk.ready()
         t_start.record()
         if cap is not None:
             graph, (top, acc, errs), launches = cap
