@@ -78,6 +78,48 @@ __global__ void voxelize_smem_kernel(fs_pose_batch b, VoxParams v, void* out, in
   }
 }
 
+// bf16 NDHWC with a multiple of 8 channels (the tcgen05 conv input): counts
+// packed two per 32-bit shared word (a count never exceeds the pose's atom
+// count, < 2^16, so a half never carries into the other), half the shared
+// memory of the u32 grid (3 CTAs per SM instead of 1); one 16-byte store per
+// 8 channels of a voxel.  Same values as voxelize_smem_kernel (counts are
+// exact in fp32, one RN rounding to bf16).
+__global__ void voxelize_bf16_kernel(fs_pose_batch b, VoxParams v, __nv_bfloat16* out, int32_t* err) {
+  extern __shared__ uint4 cnt4[];
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(cnt4);
+  const int p = blockIdx.x;
+  const int vox = v.g * v.g * v.g, wpv = v.channels / 2;   // words per voxel
+  const int words = vox * wpv;
+  for (int i = threadIdx.x; i < words / 4; i += blockDim.x) cnt4[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  PoseView pv = pose_view(b, p);
+  int flags = 0;
+  for (int64_t i = threadIdx.x; i < pv.n(); i += blockDim.x) {
+    double x, y, z; int32_t e, r;
+    pv.atom(i, x, y, z, e, r);
+    if (r != 0 && r != 1) { flags |= FS_ERR_ROLE; continue; }
+    bool nan = false;
+    int ix = vox_axis(x, v, nan), iy = vox_axis(y, v, nan), iz = vox_axis(z, v, nan);
+    if (nan) { flags |= FS_ERR_NAN; continue; }
+    const int ch = r * v.c_elem + min(max(e, 0), v.c_elem - 1);
+    const int vi = (ix * v.g + iy) * v.g + iz;
+    atomicAdd(&cnt[vi * wpv + (ch >> 1)], (ch & 1) ? 65536u : 1u);
+  }
+  if (flags) atomicOr(&err[p], flags);
+  __syncthreads();
+  uint4* o = reinterpret_cast<uint4*>(out + (int64_t)p * vox * v.channels);
+  for (int i = threadIdx.x; i < words / 4; i += blockDim.x) {   // 8 channels per 16-byte store
+    const uint4 c = cnt4[i];
+    uint4 pk;
+    __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+    b2[0] = __floats2bfloat162_rn((float)(c.x & 0xffffu), (float)(c.x >> 16));
+    b2[1] = __floats2bfloat162_rn((float)(c.y & 0xffffu), (float)(c.y >> 16));
+    b2[2] = __floats2bfloat162_rn((float)(c.z & 0xffffu), (float)(c.z >> 16));
+    b2[3] = __floats2bfloat162_rn((float)(c.w & 0xffffu), (float)(c.w >> 16));
+    o[i] = pk;
+  }
+}
+
 // Large grids: global atomics into a zeroed output (fp64 / fp32 layouts only).
 __global__ void voxelize_global_kernel(fs_pose_batch b, VoxParams v, void* out, int32_t* err) {
   const int p = blockIdx.x;
@@ -515,7 +557,12 @@ int launch_voxelize(const fs_pose_batch& b, int g, int c_elem, double box, int l
   v.half = box / 2.0; v.box = box; v.gd = (double)g;
   const int64_t cells = (int64_t)v.channels * g * g * g;
   const size_t smem = (size_t)cells * 4;
-  if (smem <= 200 * 1024) {
+  if (layout == FS_GRID_NDHWC_BF16 && v.channels % 8 == 0 && cells * 2 <= 200 * 1024 &&
+      b.max_pose_atoms > 0 && b.max_pose_atoms < 65536) {
+    const size_t sm2 = (size_t)cells * 2;
+    FS_CUDA_CHECK(cudaFuncSetAttribute(voxelize_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    voxelize_bf16_kernel<<<b.n_poses, 512, sm2, st>>>(b, v, (__nv_bfloat16*)out, err);
+  } else if (smem <= 200 * 1024) {
     FS_CUDA_CHECK(cudaFuncSetAttribute(voxelize_smem_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     voxelize_smem_kernel<<<b.n_poses, 512, smem, st>>>(b, v, out, err);

@@ -108,6 +108,30 @@ def test_pocket_batch_format_equals_complex_format(pkg):
     torch.cuda.synchronize()
 
 
+def test_voxelize_bf16_layout_equals_reference_layout(pkg):
+    """The tcgen05 conv input (NDHWC bf16, counts packed two per shared word)
+    holds exactly the reference grid, including a voxel that collects 300
+    atoms of one channel (bf16 rounds above 256 like float->bf16 RNE)."""
+    cx, E, models, synth = pkg
+    import torch
+    pocket = synth.make_pocket(1000, seed=5)
+    lib = synth.make_poses(4, poses_per_compound=3, seed=6)
+    xyz = lib.xyz.copy()
+    s0, e0 = int(lib.atom_off[0]), int(lib.atom_off[1])
+    pk_xyz = pocket.xyz.copy()
+    pk_xyz[:300] = 0.25                                  # 300 pocket atoms in one voxel
+    pk_el = pocket.elem.copy()
+    pk_el[:300] = 1
+    b = E.batch_from_arrays(xyz, lib.elem, lib.role, lib.atom_off,
+                            pocket=(pk_xyz, pk_el, pocket.role, np.array([0, 1000])), pose_target=lib.target)
+    ref, err = E.voxelize(b)
+    got, err2 = E.voxelize(b, layout=2)
+    assert int(err.abs().sum()) == 0 and int(err2.abs().sum()) == 0
+    want = ref.permute(0, 2, 3, 4, 1).to(torch.float32).to(torch.bfloat16)
+    assert torch.equal(got.view(torch.int16), want.contiguous().view(torch.int16))
+    assert float(ref.max()) >= 300
+
+
 def test_featurizer_edge_cases(pkg):
     cx, E, models, synth = pkg
     # empty-neighbourhood complex, single atom, coincident atoms
