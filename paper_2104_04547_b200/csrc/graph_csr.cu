@@ -37,13 +37,45 @@ constexpr int kCsrThreads = 256;
 constexpr int kCsrWarps = kCsrThreads / 32;
 constexpr int kCellsAxis = 9;           // cells grow past t_cov for boxes > 9*t_cov
 constexpr int kMaskWords = 2;         // bipartite bitmask path for |S| <= 64
-constexpr int kCovBits = 96;          // covalent candidates per row whose hit bits are kept (3 CTAs/SM)
+constexpr int kCovBits = 96;          // covalent candidates per row whose hit bits are kept
+constexpr int kCovWords = kCovBits / 32;
+constexpr int kCellWords = 2 * kCellsAxis * kCellsAxis * kCellsAxis + 2;
 
+// 46 bytes per atom + cell table: <= 55.75 KB at the workload's 1,064 atoms,
+// so four 256-thread CTAs share an SM (three at the former 74 KB)
 __host__ __device__ inline size_t graph_csr_smem_bytes(int n) {
-  n = (n + 3) & ~3;   // keeps every sub-array 16-byte aligned
-  const size_t cells = 2 * kCellsAxis * kCellsAxis * kCellsAxis + 2;
-  return (size_t)n * 16 + (size_t)n * 4 * 4 + (size_t)(n + 1) * 4 * 2 + (size_t)n * kMaskWords * 4 + cells * 4 +
-         (size_t)n * (kCovBits / 32 + 1) * 4 + 512;
+  n = (n + 3) & ~3;   // keeps every sub-array 8-byte aligned
+  return (size_t)n * 16 + (size_t)n * 2 * 5 + (size_t)n * kMaskWords * 4 + (size_t)kCellWords * 4 +
+         (size_t)n * kCovWords * 4 + (size_t)(n + 31) / 32 * 4 + 16;
+}
+
+// Exclusive scan of u16 counts c[0..n) into out[i] = base + prefix (int64,
+// global); returns the total.  Starts with a barrier.
+__device__ int block_scan_u16_to_global(const uint16_t* c, int n, int64_t* out, int64_t base, int* warp_tot) {
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  int sum = 0;
+  for (int i = lo; i < hi; ++i) sum += c[i];
+  int incl = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { int v = warp_tot[w]; warp_tot[w] = run; run += v; }
+    warp_tot[31] = run;
+  }
+  __syncthreads();
+  int run = warp_tot[warp] + incl - sum;
+  for (int i = lo; i < hi; ++i) { out[i] = base + run; run += c[i]; }
+  const int tot = warp_tot[31];
+  __syncthreads();
+  return tot;
 }
 
 // in-place exclusive scan of a[0..n) (n+1-th entry receives the total).
@@ -125,15 +157,15 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   if (n > a.smem_atoms) { fail(FS_ERR_TOO_LARGE); return; }
   const int SA = (a.smem_atoms + 3) & ~3;   // 16-byte aligned sub-arrays
   float4* pf = reinterpret_cast<float4*>(smem_raw);
-  int* keys = reinterpret_cast<int*>(pf + SA);
-  int* cell_list = keys + SA;
-  int* role_list = cell_list + SA;      // role 0 ids ascending, then role 1 ids ascending
-  int* rank = role_list + SA;           // position of atom i inside its role's list
-  int* offc = rank + SA;                // [n+1]
-  int* offn = offc + SA + 1;            // [n+1]
-  uint32_t* mask = reinterpret_cast<uint32_t*>(offn + SA + 1);   // [|L|][kMaskWords]
+  uint16_t* keys = reinterpret_cast<uint16_t*>(pf + SA);   // (role, cell) key < 2^16
+  uint16_t* cell_list = keys + SA;      // atoms in (role, cell) order (first: role ranks)
+  uint16_t* role_list = cell_list + SA; // role 0 ids ascending, then role 1 ids ascending
+  uint16_t* offc = role_list + SA;      // covalent degree per row (row starts live in row_cov)
+  uint16_t* offn = offc + SA;           // non-covalent degree per row
+  uint32_t* mask = reinterpret_cast<uint32_t*>(offn + SA);   // [|L|][kMaskWords]
   int* cell_start = reinterpret_cast<int*>(mask + (size_t)SA * kMaskWords);
-  uint32_t* covbits = reinterpret_cast<uint32_t*>(cell_start + 2 * kCellsAxis * kCellsAxis * kCellsAxis + 2);
+  uint32_t* covbits = reinterpret_cast<uint32_t*>(cell_start + kCellWords);   // [n][kCovWords]
+  uint32_t* ovf = covbits + (size_t)SA * kCovWords;   // rows whose hit bits do not cover their candidates
   __syncthreads();
 
   // ---- atoms, validation, bounding box ----
@@ -223,7 +255,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       if (r >= 0) {
         int pos = run[r] + __popc((r == 0 ? m0 : m1) & ((1u << lane) - 1u));
         for (int w = 0; w < warp; ++w) pos += warp_cnt[r][w];
-        keys[i] |= pos << 16;            // stash rank (n <= 4096 < 2^15, key < 2^16)
+        cell_list[i] = (uint16_t)pos;    // rank inside the role (cell_list is filled later)
       }
       for (int w = 0; w < kCsrWarps; ++w) { run[0] += warp_cnt[0][w]; run[1] += warp_cnt[1][w]; }
       __syncthreads();
@@ -233,15 +265,13 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   __syncthreads();
   const int n0 = s_role_cnt[0];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int r = (int)pf[i].w, rk = keys[i] >> 16;
-    rank[i] = rk;
-    role_list[(r == 0 ? 0 : n0) + rk] = i;
-    keys[i] &= 0xffff;
+    const int r = (int)pf[i].w, rk = cell_list[i];
+    role_list[(r == 0 ? 0 : n0) + rk] = (uint16_t)i;
   }
   block_exclusive_scan(cell_start, 2 * NC, warp_tot);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int slot = atomicAdd(&cell_start[keys[i]], 1);   // becomes the cell end
-    cell_list[slot] = i;
+    cell_list[slot] = (uint16_t)i;
   }
   __syncthreads();
   // cell k spans [cell_start[k-1], cell_start[k]) now (cell_start[-1] := 0);
@@ -249,7 +279,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   for (int k = threadIdx.x; k < 2 * NC; k += blockDim.x) {
     const int cb = k == 0 ? 0 : cell_start[k - 1], ce = cell_start[k];
     for (int x = cb + 1; x < ce; ++x) {
-      const int v = cell_list[x];
+      const uint16_t v = cell_list[x];
       int y = x - 1;
       while (y >= cb && cell_list[y] > v) { cell_list[y + 1] = cell_list[y]; --y; }
       cell_list[y + 1] = v;
@@ -279,11 +309,12 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   const int n1 = n - n0;
   const int sr = n0 <= n1 ? 0 : 1;                 // smaller role
   const int nS = sr == 0 ? n0 : n1, nL = n - nS;
-  const int* Slist = role_list + (sr == 0 ? 0 : n0);
-  const int* Llist = role_list + (sr == 0 ? n0 : 0);
+  const uint16_t* Slist = role_list + (sr == 0 ? 0 : n0);
+  const uint16_t* Llist = role_list + (sr == 0 ? n0 : 0);
   const bool use_mask = nS <= 32 * kMaskWords;
   const int W = (nS + 31) / 32;
   for (int i = threadIdx.x; i < n; i += blockDim.x) { offc[i] = 0; offn[i] = 0; }
+  for (int i = threadIdx.x; i < (n + 31) / 32; i += blockDim.x) ovf[i] = 0u;
   if (use_mask) {
     for (int i = threadIdx.x; i < nL * W; i += blockDim.x) mask[i] = 0u;
     __syncthreads();
@@ -430,10 +461,10 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         c0 += len;
       }
     }
-    uint32_t* bits = covbits + (size_t)i * (kCovBits / 32 + 1);
+    uint32_t* bits = covbits + (size_t)i * kCovWords;
     bits[0] = w0; bits[1] = w1; bits[2] = w2;
-    bits[kCovBits / 32] = over ? 0xffffffffu : (uint32_t)c0;   // > kCovBits: the fill re-tests
-    offc[i] = cnt;
+    if (over || c0 > kCovBits) atomicOr(&ovf[i >> 5], 1u << (i & 31));   // the fill re-tests
+    offc[i] = (uint16_t)cnt;
   }
   __syncthreads();
   // ---- degrees -> pose-local offsets, capacity check, row pointers ----
@@ -445,16 +476,15 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       offn[i] = (offn[i] + 3) & ~3;
     }
   }
-  block_exclusive_scan(offc, n, warp_tot);
-  block_exclusive_scan(offn, n, warp_tot);
-  if (offc[n] > a.cap || offn[n] > a.cap) {
+  const int totc = block_scan_u16_to_global(offc, n, a.row_cov + base, cbase, warp_tot);
+  const int totn = block_scan_u16_to_global(offn, n, a.row_ncov + base, cbase, warp_tot);
+  if (totc > a.cap || totn > a.cap) {
     fail(FS_ERR_EDGE_CAP);
     return;
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    a.row_cov[base + i] = cbase + offc[i];
-    a.row_ncov[base + i] = cbase + offn[i];
-  }
+  // pose-local row starts (written by the scans above)
+  auto startc = [&](int i) { return (int)(a.row_cov[base + i] - cbase); };
+  auto startn = [&](int i) { return (int)(a.row_ncov[base + i] - cbase); };
 
   // ---- fill non-covalent rows (ascending neighbour id) ----
   col_t* coln = a.col_ncov + cbase;
@@ -463,7 +493,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     for (int si = warp; si < nS; si += kCsrWarps) {          // S rows: L ids ascending
       const int i = Slist[si];
       double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
-      int w = offn[i];
+      int w = startn(i);
       for (int l0 = 0; l0 < nL; l0 += 32) {
         const int lj = l0 + lane;
         const bool hit = lj < nL && ((mask[lj * W + (si >> 5)] >> (si & 31)) & 1u);
@@ -479,7 +509,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     }
     for (int lj = threadIdx.x; lj < nL; lj += blockDim.x) {  // L rows: S ids ascending
       const int i = Llist[lj];
-      int o = offn[i];
+      int o = startn(i);
       double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
       for (int w = 0; w < W; ++w) {
         uint32_t bits = mask[lj * W + w];
@@ -499,7 +529,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       const float4 fi = pf[i];
       const int ri = (int)fi.w;
       const int ob = ri == 0 ? n0 : 0, oe = ri == 0 ? n : n0;
-      int o = offn[i];
+      int o = startn(i);
       for (int q = ob; q < oe; ++q) {
         const int j = role_list[q];
         const float4 fj = pf[j];
@@ -516,7 +546,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     const col_t padv = (col_t)((n + 15) & ~15);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int d = a.deg_ncov[base + i];
-      for (int k = offn[i] + d; k & 3; ++k) coln[k] = padv;
+      for (int k = startn(i) + d; k & 3; ++k) coln[k] = padv;
     }
   }
   // ---- fill covalent rows.  Scoring path (no distances): rows stay in the
@@ -528,10 +558,10 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   double* distc = DIST ? a.dist_cov + cbase : nullptr;
   for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
     const int i = cell_list[idx];
-    const int rb = offc[i];
+    const int rb = startc(i);
     int o = rb;
-    const uint32_t* bits = covbits + (size_t)i * (kCovBits / 32 + 1);
-    if (!DIST && bits[kCovBits / 32] <= (uint32_t)kCovBits) {
+    const uint32_t* bits = covbits + (size_t)i * kCovWords;
+    if (!DIST && !((ovf[i >> 5] >> (i & 31)) & 1u)) {
       // replay the count pass's hits: candidate index c of a stencil column
       // run maps to cell_list[qb + c - c0] (the row's own atom, skipped by
       // the count pass, only sits in its own column, which is walked)
@@ -601,7 +631,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     const col_t padv = (col_t)((n + 15) & ~15);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int d = a.deg_cov[base + i];
-      for (int k = offc[i] + d; k & 3; ++k) colc[k] = padv;
+      for (int k = startc(i) + d; k & 3; ++k) colc[k] = padv;
     }
   }
 }
