@@ -142,7 +142,7 @@ struct fs_model {
   size_t blob_bytes = 0;
   int cin, f1, f2, k1, k2, G, dn, lv, flat, gn, dg, dpad, F, w1, w2, fd, LW, cgrid;
   size_t c1w, c1b, c2w, c2b, c3w, c3b, c4w, c4b, bn1s, bn1h, bn2s, bn2h;
-  size_t d1w, d1b, d2w, d2b, ow, ob;
+  size_t d1w, d1b, d1t, d2w, d2b, ow, ob;   // d1t: dense1 W^T [dn][flat] (tcgen05 dense1)
   size_t we, be, ph[2], gg, bg, gf, bf, gd1w, gd1b, gd2w, gd2b, gow, gob;
   size_t msg, msgb, msv, msvb, fw[8], fb[8];
   size_t umma_off = 0;   // byte offset of the bf16 UMMA conv weights
@@ -187,7 +187,7 @@ static size_t plan_model(fs_model& m) {
   m.c3w = L.take((size_t)m.k2 * m.k2 * m.k2 * m.f1 * m.f2); m.c3b = L.take(m.f2);
   m.c4w = L.take((size_t)m.k2 * m.k2 * m.k2 * m.f2 * m.f2); m.c4b = L.take(m.f2);
   m.bn1s = L.take(m.f1); m.bn1h = L.take(m.f1); m.bn2s = L.take(m.f2); m.bn2h = L.take(m.f2);
-  m.d1w = L.take((size_t)m.flat * m.dn); m.d1b = L.take(m.dn);
+  m.d1w = L.take((size_t)m.flat * m.dn); m.d1b = L.take(m.dn); m.d1t = L.take((size_t)m.flat * m.dn);
   m.d2w = L.take((size_t)m.dn * m.lv); m.d2b = L.take(m.lv);
   m.ow = L.take(m.lv); m.ob = L.take(1);
   const int D = m.dpad;
@@ -286,6 +286,8 @@ static int pack_model(fs_model& m, const ParamMap& pm, std::vector<float>& h) {
         for (int n = 0; n < m.dn; ++n) h[m.d1w + ours * m.dn + n] = (float)w[ref * m.dn + n];
       }
     for (int n = 0; n < m.dn; ++n) h[m.d1b + n] = (float)b[n];
+    for (int n = 0; n < m.dn; ++n)
+      for (int k = 0; k < m.flat; ++k) h[m.d1t + (size_t)n * m.flat + k] = h[m.d1w + (size_t)k * m.dn + n];
   }
   auto copy = [&](const char* n, size_t off, size_t count) -> int {
     const double* w = need(n);
@@ -484,7 +486,7 @@ static WsPlan plan_ws(const fs_model& m, int64_t P, int64_t N, int64_t E, int pr
     w.grid = w.take(2 * P * G3 * m.cin);
     w.umma = w.take(umma::workspace_bytes(m.d, P));
     w.a1 = w.a2 = w.p1 = w.a3 = w.a4 = 0;
-    w.p2 = w.take(4 * P * Q3 * m.f2);
+    w.p2 = w.take(4 * (int64_t)umma::dense_rows_padded(P) * Q3 * m.f2);   // tcgen05 dense1 reads 128-row tiles
   } else {
     w.grid = w.take(4 * P * G3 * m.cin);
     w.a1 = w.take(4 * P * G3 * m.f1); w.a2 = w.take(4 * P * G3 * m.f1);
@@ -606,13 +608,18 @@ static int voxel_head_fp32(const fs_model& m, int P, char* ws, const WsPlan& w, 
 }
 
 // dense1 -> dense2 (latent_v into lat[:, gn:]) -> optional pred_v
-static int voxel_tail(const fs_model& m, int P, char* ws, const WsPlan& w, bool want_pred, cudaStream_t st) {
+// tc: dense1 on tcgen05 (bf16 path; p2 holds umma::dense_rows_padded(P) rows)
+static int voxel_tail(const fs_model& m, int P, char* ws, const WsPlan& w, bool want_pred, cudaStream_t st,
+                      bool tc = false) {
   float* lat = (float*)(ws + w.lat);
   mark_stage(ST_DENSE, st);
   DenseArgs a{};
   a.x = (float*)(ws + w.p2); a.ldx = m.flat; a.w = m.P(m.d1w); a.b = m.P(m.d1b);
   a.y = (float*)(ws + w.d1); a.ldy = m.dn; a.m = P; a.k = m.flat; a.n = m.dn; a.act = FS_ACT_RELU;
-  int rc = launch_dense(a, st);
+  static const bool force_ffma = getenv("FS_DENSE_FFMA") != nullptr;
+  int rc = tc && !force_ffma && umma::dense_tf32_ok(m.flat, m.dn)
+               ? umma::dense_tf32(a.x, P, m.flat, m.P(m.d1t), m.dn, a.b, a.y, st)
+               : launch_dense(a, st);
   if (rc) return rc;
   a = DenseArgs{};
   a.x = (float*)(ws + w.d1); a.ldx = m.dn; a.w = m.P(m.d2w); a.b = m.P(m.d2b);
@@ -902,7 +909,7 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
         return r;
       if ((r = voxel_head_fp32(*m, P, W, w, vs))) return r;
     }
-    return voxel_tail(*m, P, W, w, late || pred_v, vs);
+    return voxel_tail(*m, P, W, w, late || pred_v, vs, precision == FS_PREC_BF16);
   };
   // FS_OVERLAP=0: serial; 1: graph branch on a side stream; 2 (default):
   // voxel branch on a high-priority side stream, issued first, graph branch
@@ -1063,7 +1070,7 @@ int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch*
   if ((rc = umma::voxel_convs_from2(d, (const char*)m->blob + m->umma_off, m->P(m->c2b), m->P(m->c3b), m->P(m->c4b),
                                     P, W + w.umma, (float*)(W + w.p2), st)))
     return rc;
-  if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st))) return rc;
+  if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st, true))) return rc;
   if (ss) FS_CUDA_CHECK(cudaStreamWaitEvent(st, ss->join, 0));
   GnnMmaArgs x{};
   x.fact_cnt = cnt; x.fact_stride = S; x.fact_aff = aff; x.pose_target = b->pose_target;
@@ -1111,7 +1118,7 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const d
       if ((rc = launch_grid_convert(grids, W + w.grid, P, m->cin, m->G, false, err, st))) return rc;
       if ((rc = voxel_head_fp32(*m, P, W, w, st))) return rc;
     }
-    if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st))) return rc;
+    if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st, precision == FS_PREC_BF16))) return rc;
   }
   if (need_g) {
     int64_t* noff = (int64_t*)(W + w.node_off);

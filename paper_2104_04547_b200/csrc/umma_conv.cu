@@ -81,6 +81,14 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -110,6 +118,15 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
@@ -526,6 +543,139 @@ static int launch_layer(const void* in, ConvParams prm, cudaStream_t st) {
   const int ctas = max(1, min(units, g_num_sms * per_sm / L::NSPLIT));
   dim3 grid(ctas, L::NSPLIT);
   conv_umma_kernel<L><<<grid, 192, L::SMEM, st>>>(map, prm);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// dense1 of the voxel head on tcgen05 (kind::tf32):
+//   y[P][128] = relu(x[P][K] . W + b)      (models.py:316-318, autodiff.py:161-173)
+// x = the pooled conv4 output (fp32, NDHWC flatten order, rows padded to a
+// multiple of 128), wt = W^T fp32 [128][K] in the same K order.  One CTA per
+// 128-pose tile: TMA streams 32-wide K slabs of x and W^T (4-D tensor maps
+// whose boxes land in the K-major no-swizzle core-matrix layout: 8 rows x
+// 16 B, K chunks 128 B apart, 8-row groups 1 KB apart) through a 4-stage
+// ring; one thread issues M=128 N=128 K=8 MMAs into a 128-column TMEM
+// accumulator; 4 epilogue warps add the bias and apply ReLU.  The operands
+// are rounded to tf32 by the tensor core (10-bit mantissa; fp32 accumulate).
+// ---------------------------------------------------------------------------
+namespace dn {
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+constexpr int SMEM = BAR_OFF + 256;
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                           (static_cast<uint32_t>(BM >> 4) << 24);
+}  // namespace dn
+
+__global__ void __launch_bounds__(192, 1) dense_tf32_kernel(const __grid_constant__ CUtensorMap ta,
+                                                            const __grid_constant__ CUtensorMap tb,
+                                                            const float* __restrict__ bias, float* __restrict__ y,
+                                                            int P, int K) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + dn::BAR_OFF);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + dn::STAGES;
+  uint64_t* done = bars + 2 * dn::STAGES;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(done + 1);
+  const int nk = K / dn::BK;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < dn::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(dn::BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int sl = kb % dn::STAGES;
+        mbar_wait(&empty[sl], ((kb / dn::STAGES) & 1) ^ 1);
+        mbar_expect_tx(&full[sl], dn::STAGE_BYTES);
+        unsigned char* st = smem + sl * dn::STAGE_BYTES;
+        tma_load_4d(st, &ta, &full[sl], 0, 0, kb * (dn::BK / 4), blockIdx.x * (dn::BM / 8));
+        tma_load_4d(st + dn::A_BYTES, &tb, &full[sl], 0, 0, kb * (dn::BK / 4), 0);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t base = smem_u32(smem);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int sl = kb % dn::STAGES;
+      mbar_wait(&full[sl], (kb / dn::STAGES) & 1);
+      tc_fence_after();
+      const uint32_t a0 = base + sl * dn::STAGE_BYTES, b0 = a0 + dn::A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < dn::BK / 8; ++kk)   // K = 8 per MMA: two 16-byte chunks, 128 B apart
+        if (lane == 0)
+          umma_tf32(tmem, sdesc(a0 + kk * 256, 128, 1024), sdesc(b0 + kk * 256, 128, 1024), dn::IDESC,
+                    (kb | kk) != 0 ? 1u : 0u);
+      if (lane == 0) umma_commit(&empty[sl]);
+      __syncwarp();
+    }
+    if (lane == 0) umma_commit(done);
+    __syncwarp();
+  } else {
+    const int quad = warp & 3;
+    const int row = blockIdx.x * dn::BM + quad * 32 + lane;
+    mbar_wait(done, 0);
+    tc_fence_after();
+#pragma unroll
+    for (int c0 = 0; c0 < dn::BN; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
+      if (row < P) {
+        float4* o = reinterpret_cast<float4*>(y + static_cast<size_t>(row) * dn::BN + c0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          o[q] = make_float4(fmaxf(v[4 * q] + bias[c0 + 4 * q], 0.f), fmaxf(v[4 * q + 1] + bias[c0 + 4 * q + 1], 0.f),
+                             fmaxf(v[4 * q + 2] + bias[c0 + 4 * q + 2], 0.f),
+                             fmaxf(v[4 * q + 3] + bias[c0 + 4 * q + 3], 0.f));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(dn::BN));
+  }
+}
+
+// fp32 [rows][K] (row stride K) as (4 elems, 8 rows, K/4 chunks, rows/8 groups)
+static int make_dense_map(CUtensorMap* map, const void* base, int rows, int K) {
+  auto fn = encode_fn();
+  if (!fn) return FS_ECUDA;
+  cuuint64_t dims[4] = {4, 8, static_cast<cuuint64_t>(K / 4), static_cast<cuuint64_t>((rows + 7) / 8)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(K) * 4, 16, static_cast<cuuint64_t>(K) * 4 * 8};
+  cuuint32_t box[4] = {4, 8, dn::BK / 4, 16};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? FS_OK : FS_ECUDA;
+}
+
+bool dense_tf32_ok(int K, int N) { return N == dn::BN && K % dn::BK == 0 && K >= dn::BK; }
+
+size_t dense_rows_padded(int64_t P) { return static_cast<size_t>((P + dn::BM - 1) / dn::BM * dn::BM); }
+
+int dense_tf32(const float* x, int P, int K, const float* wt, int N, const float* bias, float* y, cudaStream_t st) {
+  if (P <= 0) return FS_OK;
+  if (!dense_tf32_ok(K, N)) return FS_ENOTSUP;
+  CUtensorMap ta, tb;
+  int rc = make_dense_map(&ta, x, static_cast<int>(dense_rows_padded(P)), K);
+  if (rc) return rc;
+  if ((rc = make_dense_map(&tb, wt, N, K))) return rc;
+  FS_CUDA_CHECK(cudaFuncSetAttribute(dense_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dn::SMEM));
+  dense_tf32_kernel<<<(P + dn::BM - 1) / dn::BM, 192, dn::SMEM, st>>>(ta, tb, bias, y, P, K);
   FS_LAUNCH_CHECK();
   return FS_OK;
 }

@@ -34,5 +34,11 @@ int voxel_convs_from2(const fs_model_desc& d, const char* wblob, const float* b2
 int debug_layer(const fs_model_desc& d, const char* wblob, const float* bias, const float* unused, int layer, int P,
                 const void* in, const void* residual, void* out, cudaStream_t st);
 
+// dense1 on tcgen05 kind::tf32: y[P][N] = relu(x[P][K] . W + b) with
+// wt = W^T [N][K]; x must hold dense_rows_padded(P) rows.  N == 128 only.
+bool dense_tf32_ok(int K, int N);
+size_t dense_rows_padded(int64_t P);
+int dense_tf32(const float* x, int P, int K, const float* wt, int N, const float* bias, float* y, cudaStream_t st);
+
 }  // namespace umma
 }  // namespace fs
