@@ -121,6 +121,26 @@ def test_bf16_scores_within_stated_tolerance(setup):
     assert pear >= 0.99
 
 
+def test_bf16_voxel_latent_close_to_fp32(setup):
+    """Voxel latent of the bf16 path (tcgen05 convs, bf16 activations,
+    tcgen05 tf32 dense1) against the fp32 FFMA path on the same poses."""
+    torch, N, m, dm = setup
+    from paper_2104_04547_b200 import engine as E
+    from paper_2104_04547_b200 import synth
+    pocket = synth.make_pocket(1000, seed=9)
+    lib = synth.make_poses(30, poses_per_compound=10, seed=10).slice(0, 300)   # 3 dense1 tiles, ragged
+    b = E.batch_from_arrays(lib.xyz, lib.elem, lib.role, lib.atom_off,
+                            pocket=(pocket.xyz, pocket.elem, pocket.role, np.array([0, 1000])),
+                            pose_target=lib.target)
+    v32 = dm.score_poses(b, "fp32", outputs=("scores", "lat_v"))["lat_v"].cpu().numpy().astype(np.float64)
+    v16 = dm.score_poses(b, "bf16", outputs=("scores", "lat_v"))["lat_v"].cpu().numpy().astype(np.float64)
+    err = np.abs(v16 - v32).max() / np.abs(v32).max()
+    pear = np.corrcoef(v16.ravel(), v32.ravel())[0, 1]
+    print(f"lat_v bf16 vs fp32: max abs err / max |lat_v| {err:.3e}, Pearson {pear:.6f}")
+    assert err < 2e-2
+    assert pear > 0.9999
+
+
 def test_bf16_batch_invariance_bitwise(setup):
     torch, N, m, dm = setup
     from paper_2104_04547_b200 import engine as E
