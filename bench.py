@@ -445,6 +445,9 @@ def main():
                 "stage_ms_per_step": {n: round(v / K, 4) for n, v in zip(N.STAGES[:-1], fstage)},
                 "max_abs_score_diff_vs_full_path": max_diff, "failed_poses": fact_err,
                 "topk_equal_full_path": bool(torch.equal(gi, gi_f)),
+                # scores differ by <= max_abs_score_diff (fp32 summation order), so
+                # near-ties inside the top-k may swap: report the set overlap too
+                "topk_overlap_full_path": len(set(gi.tolist()) & set(gi_f.tolist())) / max(1, gi.numel()),
                 "compound_topk_equal_full_path": bool(torch.equal(gci, gci_f)),
                 "note": "effective throughput: pocket-invariant work (pocket conv1 channels, pocket covalent "
                         "phase, untouched pocket nodes) reused from a per-target cache; algorithmic work per "

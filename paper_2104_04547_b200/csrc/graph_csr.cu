@@ -130,6 +130,15 @@ __device__ __noinline__ bool exact_edge_slow(PoseView pv, double xi, double yi, 
   return exact_edge(pv, xi, yi, zi, j, rmax2, t, &d);
 }
 
+// exact predicate for the pair (i, j) with i's coordinates first (the
+// bipartite scans' S - L order), out of line like exact_edge_slow
+__device__ __noinline__ bool exact_pair_slow(PoseView pv, int i, int j, double rmax2, double t) {
+  double xi, yi, zi; int32_t e, r;
+  pv.atom(i, xi, yi, zi, e, r);
+  double d;
+  return exact_edge(pv, xi, yi, zi, j, rmax2, t, &d);
+}
+
 template <bool DIST>
 __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -316,34 +325,41 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   for (int i = threadIdx.x; i < n; i += blockDim.x) { offc[i] = 0; offn[i] = 0; }
   for (int i = threadIdx.x; i < (n + 31) / 32; i += blockDim.x) ovf[i] = 0u;
   if (use_mask) {
-    for (int i = threadIdx.x; i < nL * W; i += blockDim.x) mask[i] = 0u;
+    // lanes over L atoms (32 per warp chunk), loop over the S atoms (broadcast
+    // shared reads): each lane builds its L row's hit mask in registers, no
+    // atomics on the mask; S-row counts accumulate per warp chunk.  Same fp32
+    // operands and order (S - L) as the fill, so the same decisions.
+    int* s_ncnt = reinterpret_cast<int*>(red);   // [<= 64], red is free here
+    if (threadIdx.x < 32 * kMaskWords) s_ncnt[threadIdx.x] = 0;
     __syncthreads();
-    for (int si = warp; si < nS; si += kCsrWarps) {
-      const int i = Slist[si];
-      double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
-      const float4 fi = pf[i];
-      int cnt = 0;
-      for (int l0 = 0; l0 < nL; l0 += 32) {
-        const int lj = l0 + lane;
-        bool hit = false;
-        if (lj < nL) {
-          const int j = Llist[lj];
-          const float4 fj = pf[j];
-          const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
-          hit = decide(dx * dx + dy * dy + dz * dz, n_lo2, n_hi2, xi, yi, zi, j, a.tn);
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, hit);
-        cnt += __popc(m);
-        if (hit) atomicOr(&mask[lj * W + (si >> 5)], 1u << (si & 31));
+    for (int l0 = warp * 32; l0 < nL; l0 += kCsrWarps * 32) {
+      const int lj = l0 + lane;
+      const bool lv = lj < nL;
+      const int j = lv ? Llist[lj] : 0;
+      const float4 fj = pf[j];
+      uint32_t m0 = 0u, m1 = 0u;
+      for (int si = 0; si < nS; ++si) {
+        const int i = Slist[si];
+        const float4 fi = pf[i];
+        const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+        const float d2f = dx * dx + dy * dy + dz * dz;
+        bool hit;
+        if (prefilter && d2f > n_hi2) hit = false;
+        else if (prefilter && d2f <= n_lo2) hit = lv;
+        else hit = lv && exact_pair_slow(pv, i, j, rmax2, a.tn);
+        const uint32_t b = hit ? 1u : 0u;
+        if (si < 32) m0 |= b << si; else m1 |= b << (si - 32);
+        const int c = __popc(__ballot_sync(0xffffffffu, hit));
+        if (lane == 0 && c) atomicAdd(&s_ncnt[si], c);
       }
-      if (lane == 0) offn[i] = cnt;
+      if (lv) {
+        mask[lj * W] = m0;
+        if (W > 1) mask[lj * W + 1] = m1;
+        offn[j] = (uint16_t)(__popc(m0) + __popc(m1));
+      }
     }
     __syncthreads();
-    for (int lj = threadIdx.x; lj < nL; lj += blockDim.x) {
-      int c = 0;
-      for (int w = 0; w < W; ++w) c += __popc(mask[lj * W + w]);
-      offn[Llist[lj]] = c;
-    }
+    for (int si = threadIdx.x; si < nS; si += blockDim.x) offn[Slist[si]] = (uint16_t)s_ncnt[si];
   } else {
     // large bipartite sides: one thread per row scans the other role's list
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
