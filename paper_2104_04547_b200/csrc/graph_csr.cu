@@ -302,14 +302,16 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   // the float64 one by < 2^-21*M + 4 ulp; outside [t - delta, t + delta] the
   // fp32 test decides exactly, inside it the float64 predicate runs.
   const float delta = 1e-5f + 2e-6f * (float)absmax;
-  const float c_lo2 = ((float)a.tc - delta) * ((float)a.tc - delta), c_hi2 = ((float)a.tc + delta) * ((float)a.tc + delta);
-  const float n_lo2 = ((float)a.tn - delta) * ((float)a.tn - delta), n_hi2 = ((float)a.tn + delta) * ((float)a.tn + delta);
-  // 1: edge, 0: not, decided in fp32; otherwise the exact float64 predicate
+  // Without the prefilter (|coords| >= 1024 A) the band is everything: every
+  // pair takes the exact path, with no per-candidate prefilter test.
+  const float c_lo2 = prefilter ? ((float)a.tc - delta) * ((float)a.tc - delta) : -1.0f;
+  const float c_hi2 = prefilter ? ((float)a.tc + delta) * ((float)a.tc + delta) : INFINITY;
+  const float n_lo2 = prefilter ? ((float)a.tn - delta) * ((float)a.tn - delta) : -1.0f;
+  const float n_hi2 = prefilter ? ((float)a.tn + delta) * ((float)a.tn + delta) : INFINITY;
+  // 1: edge, 0: not, decided in fp32; inside the band the exact float64 predicate
   auto decide = [&](float d2f, float lo2, float hi2, double xi, double yi, double zi, int j, double t) -> bool {
-    if (prefilter) {
-      if (d2f > hi2) return false;
-      if (d2f <= lo2) return true;
-    }
+    if (d2f > hi2) return false;
+    if (d2f <= lo2) return true;
     double d;
     return exact_edge(pv, xi, yi, zi, j, rmax2, t, &d);
   };
@@ -344,8 +346,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
         const float d2f = dx * dx + dy * dy + dz * dz;
         bool hit;
-        if (prefilter && d2f > n_hi2) hit = false;
-        else if (prefilter && d2f <= n_lo2) hit = lv;
+        if (d2f > n_hi2) hit = false;
+        else if (d2f <= n_lo2) hit = lv;
         else hit = lv && exact_pair_slow(pv, i, j, rmax2, a.tn);
         const uint32_t b = hit ? 1u : 0u;
         if (si < 32) m0 |= b << si; else m1 |= b << (si - 32);
@@ -712,12 +714,11 @@ __host__ __device__ inline size_t graph_fact_smem_bytes(int max_pocket) {
   return np4 * 16 + kFactMaxLig * 16 + np4 * kFactWords * 4 + (np4 + 4) * 4 + 2 * (nc + 4) * 4 + 256;
 }
 
-__device__ __forceinline__ bool fact_decide(const PoseView& pv, bool prefilter, float d2f, float lo2, float hi2,
-                                            double xi, double yi, double zi, int j, double rmax2, double t) {
-  if (prefilter) {
-    if (d2f > hi2) return false;
-    if (d2f <= lo2) return true;
-  }
+// thresholds are (-1, inf) when the prefilter is off: every pair is exact
+__device__ __forceinline__ bool fact_decide(const PoseView& pv, float d2f, float lo2, float hi2, double xi, double yi,
+                                            double zi, int j, double rmax2, double t) {
+  if (d2f > hi2) return false;
+  if (d2f <= lo2) return true;
   return exact_edge_slow(pv, xi, yi, zi, j, rmax2, t);
 }
 
@@ -770,8 +771,10 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
   const bool prefilter = absmax < 1024.0;
   const double rmax = fmax(a.tc, a.tn), rmax2 = __dmul_rn(rmax, rmax);
   const float delta = 1e-5f + 2e-6f * (float)absmax;
-  const float c_lo2 = ((float)a.tc - delta) * ((float)a.tc - delta), c_hi2 = ((float)a.tc + delta) * ((float)a.tc + delta);
-  const float n_lo2 = ((float)a.tn - delta) * ((float)a.tn - delta), n_hi2 = ((float)a.tn + delta) * ((float)a.tn + delta);
+  const float c_lo2 = prefilter ? ((float)a.tc - delta) * ((float)a.tc - delta) : -1.0f;
+  const float c_hi2 = prefilter ? ((float)a.tc + delta) * ((float)a.tc + delta) : INFINITY;
+  const float n_lo2 = prefilter ? ((float)a.tn - delta) * ((float)a.tn - delta) : -1.0f;
+  const float n_hi2 = prefilter ? ((float)a.tn + delta) * ((float)a.tn + delta) : INFINITY;
 
   // ---- non-covalent (ligand x pocket) bitmasks; ligand-ligand covalent degrees ----
   for (int s = warp; s < nL; s += kCsrWarps) {
@@ -785,7 +788,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
       if (j < np) {
         const float4 fj = pf[j];
         const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
-        hit = fact_decide(pv, prefilter, dx * dx + dy * dy + dz * dz, n_lo2, n_hi2, xi, yi, zi, j, rmax2, a.tn);
+        hit = fact_decide(pv, dx * dx + dy * dy + dz * dz, n_lo2, n_hi2, xi, yi, zi, j, rmax2, a.tn);
       }
       cn += __popc(__ballot_sync(0xffffffffu, hit));
       if (hit) atomicOr(&mask[j * kFactWords + (s >> 5)], 1u << (s & 31));
@@ -797,7 +800,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
       if (j < nL && j != s) {
         const float4 fj = lf[j];
         const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
-        hit = fact_decide(pv, prefilter, dx * dx + dy * dy + dz * dz, c_lo2, c_hi2, xi, yi, zi, np + j, rmax2, a.tc);
+        hit = fact_decide(pv, dx * dx + dy * dy + dz * dz, c_lo2, c_hi2, xi, yi, zi, np + j, rmax2, a.tc);
       }
       cc += __popc(__ballot_sync(0xffffffffu, hit));
     }
@@ -857,7 +860,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
       if (j < nL && j != s) {
         const float4 fj = lf[j];
         const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
-        hit = fact_decide(pv, prefilter, dx * dx + dy * dy + dz * dz, c_lo2, c_hi2, xi, yi, zi, np + j, rmax2, a.tc);
+        hit = fact_decide(pv, dx * dx + dy * dy + dz * dz, c_lo2, c_hi2, xi, yi, zi, np + j, rmax2, a.tc);
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       if (hit) {
