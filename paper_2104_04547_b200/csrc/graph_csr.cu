@@ -454,18 +454,27 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         const int z0 = max(cz - 1, 0), z1 = min(cz + 1, nca - 1);
         const int k0 = ri * NC + (ax * nca + ay) * nca + z0, k1 = ri * NC + (ax * nca + ay) * nca + z1;
         const int qb = k0 == 0 ? 0 : cell_start[k0 - 1], qe = cell_start[k1];
-        // one stencil column: hits collected run-locally, merged once
+        // one stencil column: hits collected run-locally, merged once.  The
+        // row's own atom is a candidate here (it always hits: d = 0); the
+        // count drops it at the end and the fill never emits it.
         uint64_t rm = 0ull;
-        int len = 0;
-        for (int q = qb; q < qe; ++q) {
-          const int j = cell_list[q];
-          if (j == i) continue;
-          const float4 fj = pf[j];
-          const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
-          const bool hit = decide(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, xi, yi, zi, j, a.tc);
-          if (len < 64) rm |= (uint64_t)hit << len;
-          else { over = true; cnt += hit; }
-          ++len;
+        const int len = qe - qb;
+        if (len <= 64) {
+          for (int q = qb; q < qe; ++q) {
+            const int j = cell_list[q];
+            const float4 fj = pf[j];
+            const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
+            const bool hit = decide(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, xi, yi, zi, j, a.tc);
+            rm |= (uint64_t)hit << (q - qb);
+          }
+        } else {   // crowded column: counted only, the fill re-tests this row
+          over = true;
+          for (int q = qb; q < qe; ++q) {
+            const int j = cell_list[q];
+            const float4 fj = pf[j];
+            const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
+            cnt += decide(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, xi, yi, zi, j, a.tc);
+          }
         }
         cnt += __popcll(rm);
         if (c0 < kCovBits) {
@@ -482,7 +491,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     uint32_t* bits = covbits + (size_t)i * kCovWords;
     bits[0] = w0; bits[1] = w1; bits[2] = w2;
     if (over || c0 > kCovBits) atomicOr(&ovf[i >> 5], 1u << (i & 31));   // the fill re-tests
-    offc[i] = (uint16_t)cnt;
+    offc[i] = (uint16_t)(cnt - 1);   // minus the row's own atom
   }
   __syncthreads();
   // ---- degrees -> pose-local offsets, capacity check, row pointers ----
@@ -581,8 +590,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     const uint32_t* bits = covbits + (size_t)i * kCovWords;
     if (!DIST && !((ovf[i >> 5] >> (i & 31)) & 1u)) {
       // replay the count pass's hits: candidate index c of a stencil column
-      // run maps to cell_list[qb + c - c0] (the row's own atom, skipped by
-      // the count pass, only sits in its own column, which is walked)
+      // run maps to cell_list[qb + c - c0]; the row's own atom (a candidate
+      // that always hits) is not emitted
       const int ri = (int)pf[i].w;
       const int key = keys[i] - ri * NC;
       const int cz = key % nca, cy = (key / nca) % nca, cx = key / (nca * nca);
@@ -596,26 +605,18 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
           const int z0 = max(cz - 1, 0), z1 = min(cz + 1, nca - 1);
           const int k0 = ri * NC + (ax * nca + ay) * nca + z0, k1 = ri * NC + (ax * nca + ay) * nca + z1;
           const int qb = k0 == 0 ? 0 : cell_start[k0 - 1], qe = cell_start[k1];
-          if (dx == 0 && dy == 0) {
-            for (int q = qb; q < qe; ++q) {
-              const int j = cell_list[q];
-              if (j == i) continue;
-              if ((bits[c0 >> 5] >> (c0 & 31)) & 1u) colc[o++] = (col_t)j;
-              ++c0;
-            }
-          } else {
-            const int cend = c0 + (qe - qb);
-            int c = c0;
-            while (c < cend) {
-              const uint32_t w = bits[c >> 5] >> (c & 31);
-              if (w == 0u) { c += 32 - (c & 31); continue; }
-              c += __ffs(w) - 1;
-              if (c >= cend) break;
-              colc[o++] = (col_t)cell_list[qb + (c - c0)];
-              ++c;
-            }
-            c0 = cend;
+          const int cend = c0 + (qe - qb);
+          int c = c0;
+          while (c < cend) {
+            const uint32_t w = bits[c >> 5] >> (c & 31);
+            if (w == 0u) { c += 32 - (c & 31); continue; }
+            c += __ffs(w) - 1;
+            if (c >= cend) break;
+            const int j = cell_list[qb + (c - c0)];
+            if (j != i) colc[o++] = (col_t)j;
+            ++c;
           }
+          c0 = cend;
         }
       }
       continue;
