@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[33];
   __shared__ double s_min[3];
-  __shared__ int s_flags, s_role_cnt[2], s_tot[2];
+  __shared__ int s_flags, s_role_cnt[2];
   __shared__ int warp_tot[32];
   __shared__ int warp_cnt[2][kCsrWarps];
 
@@ -242,16 +242,18 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const float4 f = pf[i];
     const int r = (int)f.w;
-    int key;
+    int cx, cy, cz;
     if (prefilter) {
-      key = r * NC + (cell_coord_f(f.x, fmin_x) * nca + cell_coord_f(f.y, fmin_y)) * nca + cell_coord_f(f.z, fmin_z);
+      cx = cell_coord_f(f.x, fmin_x); cy = cell_coord_f(f.y, fmin_y); cz = cell_coord_f(f.z, fmin_z);
     } else {
       double x, y, z; int32_t e, rr;
       pv.atom(i, x, y, z, e, rr);
-      key = r * NC + (cell_coord(x, 0) * nca + cell_coord(y, 1)) * nca + cell_coord(z, 2);
+      cx = cell_coord(x, 0); cy = cell_coord(y, 1); cz = cell_coord(z, 2);
     }
-    keys[i] = key;
-    atomicAdd(&cell_start[key], 1);
+    // keys hold (role, cx, cy, cz) packed in 4-bit fields (nca <= 9): the
+    // stencil loops decompose them with shifts instead of divisions
+    keys[i] = (uint16_t)(r << 12 | cx << 8 | cy << 4 | cz);
+    atomicAdd(&cell_start[r * NC + (cx * nca + cy) * nca + cz], 1);
   }
   {
     int run[2] = {0, 0};
@@ -279,7 +281,9 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   }
   block_exclusive_scan(cell_start, 2 * NC, warp_tot);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int slot = atomicAdd(&cell_start[keys[i]], 1);   // becomes the cell end
+    const int kp = keys[i];
+    const int slot = atomicAdd(&cell_start[(kp >> 12) * NC + (((kp >> 8) & 15) * nca + ((kp >> 4) & 15)) * nca +
+                                           (kp & 15)], 1);   // becomes the cell end
     cell_list[slot] = (uint16_t)i;
   }
   __syncthreads();
@@ -315,6 +319,15 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     double d;
     return exact_edge(pv, xi, yi, zi, j, rmax2, t, &d);
   };
+  // same, loading row i's float64 coordinates only inside the band
+  auto decide_i = [&](float d2f, float lo2, float hi2, int i, int j, double t) -> bool {
+    if (d2f > hi2) return false;
+    if (d2f <= lo2) return true;
+    double xi, yi, zi; int32_t e_, r_;
+    pv.atom(i, xi, yi, zi, e_, r_);
+    double d;
+    return exact_edge(pv, xi, yi, zi, j, rmax2, t, &d);
+  };
 
   // ---- non-covalent: bipartite S x L ----
   const int n1 = n - n0;
@@ -334,6 +347,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     int* s_ncnt = reinterpret_cast<int*>(red);   // [<= 64], red is free here
     if (threadIdx.x < 32 * kMaskWords) s_ncnt[threadIdx.x] = 0;
     __syncthreads();
+    int sacc0 = 0, sacc1 = 0;   // lane l: hits of S atoms l and 32 + l in this warp's chunks
     for (int l0 = warp * 32; l0 < nL; l0 += kCsrWarps * 32) {
       const int lj = l0 + lane;
       const bool lv = lj < nL;
@@ -350,9 +364,9 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         else if (d2f <= n_lo2) hit = lv;
         else hit = lv && exact_pair_slow(pv, i, j, rmax2, a.tn);
         const uint32_t b = hit ? 1u : 0u;
-        if (si < 32) m0 |= b << si; else m1 |= b << (si - 32);
         const int c = __popc(__ballot_sync(0xffffffffu, hit));
-        if (lane == 0 && c) atomicAdd(&s_ncnt[si], c);
+        if (si < 32) { m0 |= b << si; sacc0 += lane == si ? c : 0; }
+        else { m1 |= b << (si - 32); sacc1 += lane == si - 32 ? c : 0; }
       }
       if (lv) {
         mask[lj * W] = m0;
@@ -360,6 +374,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         offn[j] = (uint16_t)(__popc(m0) + __popc(m1));
       }
     }
+    if (sacc0) atomicAdd(&s_ncnt[lane], sacc0);
+    if (sacc1) atomicAdd(&s_ncnt[32 + lane], sacc1);
     __syncthreads();
     for (int si = threadIdx.x; si < nS; si += blockDim.x) offn[Slist[si]] = (uint16_t)s_ncnt[si];
   } else {
@@ -384,8 +400,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   // sees every candidate j != i with its running candidate index c. ----
   auto cov_cand = [&](int i, auto&& visit) {
     const int ri = (int)pf[i].w;
-    const int key = keys[i] - ri * NC;
-    const int cz = key % nca, cy = (key / nca) % nca, cx = key / (nca * nca);
+    const int kp = keys[i];
+    const int cz = kp & 15, cy = (kp >> 4) & 15, cx = (kp >> 8) & 15;
     int c = 0;
     for (int dx = -1; dx <= 1; ++dx) {
       const int ax = cx + dx;
@@ -409,8 +425,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
     const float4 fi = pf[i];
     const int ri = (int)fi.w;
-    const int key = keys[i] - ri * NC;
-    const int cz = key % nca, cy = (key / nca) % nca, cx = key / (nca * nca);
+    const int kp = keys[i];
+    const int cz = kp & 15, cy = (kp >> 4) & 15, cx = (kp >> 8) & 15;
     for (int dx = -1; dx <= 1; ++dx) {
       const int ax = cx + dx;
       if (ax < 0 || ax >= nca) continue;
@@ -437,14 +453,13 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   // (same trip counts, broadcast candidate reads)
   for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
     const int i = cell_list[idx];
-    double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
     const float4 fi = pf[i];
     int cnt = 0, c0 = 0;
     bool over = false;
     uint32_t w0 = 0u, w1 = 0u, w2 = 0u;   // hit bits of candidates 0..95
     const int ri = (int)fi.w;
-    const int key = keys[i] - ri * NC;
-    const int cz = key % nca, cy = (key / nca) % nca, cx = key / (nca * nca);
+    const int kp = keys[i];
+    const int cz = kp & 15, cy = (kp >> 4) & 15, cx = (kp >> 8) & 15;
     for (int dx = -1; dx <= 1; ++dx) {
       const int ax = cx + dx;
       if (ax < 0 || ax >= nca) continue;
@@ -464,7 +479,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
             const int j = cell_list[q];
             const float4 fj = pf[j];
             const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
-            const bool hit = decide(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, xi, yi, zi, j, a.tc);
+            const bool hit = decide_i(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, i, j, a.tc);
             rm |= (uint64_t)hit << (q - qb);
           }
         } else {   // crowded column: counted only, the fill re-tests this row
@@ -473,7 +488,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
             const int j = cell_list[q];
             const float4 fj = pf[j];
             const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
-            cnt += decide(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, xi, yi, zi, j, a.tc);
+            cnt += decide_i(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, i, j, a.tc);
           }
         }
         cnt += __popcll(rm);
@@ -593,8 +608,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       // run maps to cell_list[qb + c - c0]; the row's own atom (a candidate
       // that always hits) is not emitted
       const int ri = (int)pf[i].w;
-      const int key = keys[i] - ri * NC;
-      const int cz = key % nca, cy = (key / nca) % nca, cx = key / (nca * nca);
+      const int kp = keys[i];
+      const int cz = kp & 15, cy = (kp >> 4) & 15, cx = (kp >> 8) & 15;
       int c0 = 0;
       for (int dx = -1; dx <= 1; ++dx) {
         const int ax = cx + dx;
