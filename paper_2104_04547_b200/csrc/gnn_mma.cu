@@ -458,12 +458,25 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           const int d = degs[base + row];
           const col_t* c = colv + rows[base + row];
           float sq[4] = {0.f, 0.f, 0.f, 0.f}, sd[2] = {0.f, 0.f};
-          for (int q = g; q < d; q += 32) {
-            int j[4];
+          if (a.ids_padded) {
+            // rows padded to 4 ids (zero row npad): lane group g takes ids
+            // 4g..4g+3 of every 32, one 8-byte load
+            const int e = (d + 3) & ~3;
+            for (int q = 4 * g; q < e; q += 32) {
+              const uint2 v = __ldg(reinterpret_cast<const uint2*>(c + q));
+              const int j[4] = {static_cast<int>(v.x & 0xffffu), static_cast<int>(v.x >> 16),
+                                static_cast<int>(v.y & 0xffffu), static_cast<int>(v.y >> 16)};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) j[u] = q + 8 * u < d ? __ldg(c + q + 8 * u) : npad;
+              for (int u = 0; u < 4; ++u) acc_row(sq, sd, Hc + j[u] * 24, t);
+            }
+          } else {
+            for (int q = g; q < d; q += 32) {
+              int j[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc_row(sq, sd, Hc + j[u] * 24, t);
+              for (int u = 0; u < 4; ++u) j[u] = q + 8 * u < d ? __ldg(c + q + 8 * u) : npad;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) acc_row(sq, sd, Hc + j[u] * 24, t);
+            }
           }
           float s6[6] = {sq[0], sq[1], sq[2], sq[3], sd[0], sd[1]};   // storage order
 #pragma unroll
