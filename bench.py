@@ -469,7 +469,8 @@ def main():
                     "peak": bf16_sus, "unit": "TFLOP/s", "traffic": None}
         elif dom_name == "gnn":
             flop = graph_flop(n_mean, 5152, 9094) * B
-            gk = ("gnn_mma_kernel (GRU message passing on mma.sync, bf16 hi/lo split)" if precision == "bf16"
+            gk = ("gnn_mma_kernel (GRU message passing on mma.sync: fp16 hi/lo activations x fp16 weights, "
+                  "FS_GNN_SPLIT=3: bf16 hi/lo 3-pass)" if precision == "bf16"
                   else "gnn_kernel (GRU message passing, FFMA fp32)")
             roof = {"kernel": gk, "bound": "tensor",
                     "achieved": flop / (avg_ms / 1e3) / 1e12, "peak": bf16_sus, "unit": "TFLOP/s",

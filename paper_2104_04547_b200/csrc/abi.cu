@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "umma_conv.cuh"
 
@@ -103,7 +105,8 @@ struct GnnMmaArgs {
   const int64_t* row_cov; const int32_t* deg_cov; const col_t* col_cov;
   const int64_t* row_ncov; const int32_t* deg_ncov; const col_t* col_ncov;
   const float* we; const float* be; const uint32_t* wfrag[2]; const float* wbias[2];
-  const uint32_t* gfrag; const float* gbias; int k_steps[2]; float* lat; int64_t ld_lat; const int32_t* err;
+  const uint32_t* gfrag; const uint32_t* wfrag16[2]; const uint32_t* gfrag16;
+  const float* gbias; int k_steps[2]; float* lat; int64_t ld_lat; const int32_t* err;
   const int32_t* fact_cnt; int64_t fact_stride; const int32_t* fact_aff; const int32_t* pose_target;
   const char* cache; int64_t cache_stride; int64_t off_hcov, off_f, off_T, off_n;
   float* dump_hcov; float* dump_f; int64_t dump_ld;
@@ -149,6 +152,7 @@ struct fs_model {
   bool umma_ok = false;
   bool gmma_ok = false;  // tensor-core SG-CNN (widths 24 / 128)
   size_t gm_wf[2], gm_wb[2], gm_gf, gm_gb;
+  size_t gm_wf16[2], gm_gf16;   // fp16 weight fragments of the 2-pass SG-CNN
   const float* P(size_t off) const { return blob + off; }
 };
 
@@ -215,6 +219,8 @@ static size_t plan_model(fs_model& m) {
     for (int ph = 0; ph < 2; ++ph) { m.gm_wf[ph] = L.take(gnn_mma_phase_words()); m.gm_wb[ph] = L.take(72); }
     m.gm_gf = L.take(gnn_mma_gather_words());
     m.gm_gb = L.take(256);
+    for (int ph = 0; ph < 2; ++ph) m.gm_wf16[ph] = L.take(gnn_mma_phase_words() / 2);
+    m.gm_gf16 = L.take(gnn_mma_gather_words() / 2);
   }
   size_t bytes = L.n * 4;
   m.umma_ok = umma::supports(d);
@@ -382,6 +388,27 @@ static int pack_model(fs_model& m, const ParamMap& pm, std::vector<float>& h) {
             out_lo[o + 1] = lo[2] | (lo[3] << 16);
           }
     };
+    // fp16 fragments in the layout of the bf16 "hi" set (2-pass SG-CNN)
+    auto frags16 = [&](const std::vector<double>& W, int K, int N, uint32_t* out) {
+      const int KT = K / 16, NT = N / 8;
+      for (int kt = 0; kt < KT; ++kt)
+        for (int nt = 0; nt < NT; ++nt)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int g = lane >> 2, t = lane & 3;
+            const int n = 8 * nt + g;
+            const int ks[4] = {16 * kt + 2 * t, 16 * kt + 2 * t + 1, 16 * kt + 2 * t + 8, 16 * kt + 2 * t + 9};
+            uint32_t hv[4];
+            for (int e = 0; e < 4; ++e) {
+              const __half hb = __float2half_rn((float)W[(size_t)ks[e] * N + n]);
+              uint16_t u;
+              std::memcpy(&u, &hb, 2);
+              hv[e] = u;
+            }
+            const size_t o = ((size_t)(kt * NT + nt) * 32 + lane) * 2;
+            out[o] = hv[0] | (hv[1] << 16);
+            out[o + 1] = hv[2] | (hv[3] << 16);
+          }
+    };
     const char* phases[2] = {"cov", "noncov"};
     const int dg = 24;
     for (int ph = 0; ph < 2; ++ph) {
@@ -413,6 +440,9 @@ static int pack_model(fs_model& m, const ParamMap& pm, std::vector<float>& h) {
       const int zr = 3 * 6 * 64, hh = 3 * 3 * 64;
       frags(Wzr, 48, 48, wf, wf + zr);
       frags(Whh, 48, 24, wf + 2 * zr, wf + 2 * zr + hh);
+      uint32_t* wf16 = reinterpret_cast<uint32_t*>(&h[m.gm_wf16[ph]]);
+      frags16(Wzr, 48, 48, wf16);
+      frags16(Whh, 48, 24, wf16 + zr);
       for (int q = 0; q < 3; ++q)
         for (int k = 0; k < 24; ++k) h[m.gm_wb[ph] + q * 24 + k] = (float)(sc[q] * B[q][k]);
     }
@@ -426,6 +456,7 @@ static int pack_model(fs_model& m, const ParamMap& pm, std::vector<float>& h) {
       }
     uint32_t* gf = reinterpret_cast<uint32_t*>(&h[m.gm_gf]);
     frags(Gm, 32, 256, gf, gf + gnn_mma_gather_words() / 2);
+    frags16(Gm, 32, 256, reinterpret_cast<uint32_t*>(&h[m.gm_gf16]));
     for (int k = 0; k < 128; ++k) {
       h[m.gm_gb + k] = (float)(kNegLog2e * ggb[k]);
       h[m.gm_gb + 128 + k] = (float)(kTwoLog2e * gfb[k]);
@@ -662,11 +693,16 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
       q.wbias[ph] = m.P(m.gm_wb[ph]);
     }
     q.gfrag = reinterpret_cast<const uint32_t*>(m.P(m.gm_gf)); q.gbias = m.P(m.gm_gb);
+    for (int ph = 0; ph < 2; ++ph) q.wfrag16[ph] = reinterpret_cast<const uint32_t*>(m.P(m.gm_wf16[ph]));
+    q.gfrag16 = reinterpret_cast<const uint32_t*>(m.P(m.gm_gf16));
     q.k_steps[0] = m.d.k_cov; q.k_steps[1] = m.d.k_noncov;
     q.lat = g.lat; q.ld_lat = g.ld_lat; q.err = err;
     q.ids_padded = ids_padded ? 1 : 0;
-    // bf16 hi/lo 3-pass (fp32-class, default) or single bf16 pass (FS_GNN_SPLIT=1)
-    static const int split = (getenv("FS_GNN_SPLIT") && atoi(getenv("FS_GNN_SPLIT")) == 1) ? 1 : 3;
+    // FS_GNN_SPLIT (read per call): 2 = fp16 activations hi/lo x fp16
+    // weights, two passes (default); 3 = bf16 hi/lo x hi/lo, three passes
+    // (fp32-class); 1 = one bf16 pass
+    const char* sp_env = getenv("FS_GNN_SPLIT");
+    const int split = sp_env && (atoi(sp_env) == 1 || atoi(sp_env) == 3) ? atoi(sp_env) : 2;
     rc = launch_gnn_mma(q, split, P, max_nodes, st);
   } else {
     rc = launch_gnn(g, m.dpad, P, max_nodes, st);

@@ -12,12 +12,17 @@
 // (t = lane%4) of s, h, z, r, hh and h': the whole GRU update is lane-local
 // and r*h feeds the second GEMM without any data exchange.
 // SPLIT = 3 keeps fp32-class accuracy: x = hi + lo (bf16 each) and
-// A.B ~ Ahi.Bhi + Ahi.Blo + Alo.Bhi (relative error ~2^-16); SPLIT = 1 is a
+// A.B ~ Ahi.Bhi + Ahi.Blo + Alo.Bhi (relative error ~2^-16); SPLIT = 2 splits
+// the activations into fp16 hi + lo (22 significant bits) against fp16
+// weights (2^-12 relative rounding): two passes, half the weight-fragment
+// shared-memory traffic of SPLIT = 3; SPLIT = 1 is a
 // single bf16 pass.  Node states stay fp32 in shared memory.
 // Determinism: every row's sum has a fixed order (CSR order, or for heavy
 // rows 8 CSR-strided partial sums in a fixed tree), fixed reduction trees,
 // fixed pool order -> a pose's latent is bitwise independent of its batch.
 #include <cstdlib>
+
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -32,6 +37,8 @@ struct GnnMmaArgs {
   const uint32_t* wfrag[2];               // per phase, see gnn_mma_phase_words()
   const float* wbias[2];                  // per phase [72] = bz | br | bh
   const uint32_t* gfrag;                  // gather fragments [2 hi/lo][2 kt][32 nt][32][2]
+  const uint32_t* wfrag16[2];             // fp16 phase fragments (SPLIT 2), [zr | hh] in the hi layout
+  const uint32_t* gfrag16;                // fp16 gather fragments (SPLIT 2)
   const float* gbias;                     // [256] = bg | bf
   int k_steps[2];
   float* lat; int64_t ld_lat;             // [P][ld_lat], columns 0..127
@@ -79,6 +86,29 @@ __device__ __forceinline__ void mma_bf16_k8(float (&d)[4], uint32_t a0, uint32_t
       : "r"(a0), "r"(a1), "r"(b0));
 }
 
+template <int SPLIT>
+__device__ __forceinline__ void mma_t(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  if constexpr (SPLIT == 2) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  } else {
+    mma_bf16(d, a, b0, b1);
+  }
+}
+template <int SPLIT>
+__device__ __forceinline__ void mma_t_k8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  if constexpr (SPLIT == 2) {
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a0), "r"(a1), "r"(b0));
+  } else {
+    mma_bf16_k8(d, a0, a1, b0);
+  }
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo_idx, float hi_idx) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo_idx, hi_idx);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -96,9 +126,20 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
 
 // A fragments of a 16x48 tile [left(24) | right(24)] from the lane's values:
 // L[r][c] / R[r][c]: r in {row g, row g+8}, c in {2t,2t+1,8+2t,9+2t,16+2t,17+2t}
+// fp16 hi/lo of a pair: lo = x - fp16(x) rounded to fp16
+__device__ __forceinline__ void split2_f16(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  __half2 h = __floats2half2_rn(x0, x1);
+  float2 hf = __half22float2(h);
+  fadd2(x0, x1, -hf.x, -hf.y);
+  __half2 l = __floats2half2_rn(x0, x1);
+  hi = *reinterpret_cast<uint32_t*>(&h);
+  lo = *reinterpret_cast<uint32_t*>(&l);
+}
+
 template <int SPLIT>
 __device__ __forceinline__ void put_a(uint32_t (&hi)[4], uint32_t (&lo)[4], int q, float x0, float x1) {
   if (SPLIT == 3) split2(x0, x1, hi[q], lo[q]);
+  else if (SPLIT == 2) split2_f16(x0, x1, hi[q], lo[q]);
   else hi[q] = pack_bf16(x0, x1);
 }
 
@@ -132,6 +173,16 @@ __device__ __forceinline__ void mma_bf16_c(float (&d)[4], const uint32_t (&a)[4]
         "f"(c[3]));
 }
 
+__device__ __forceinline__ void mma_f16_c(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
+                                          const float (&c)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%11,%12,%13};"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c[0]), "f"(c[1]), "f"(c[2]),
+        "f"(c[3]));
+}
+
 template <int SPLIT, int NT>
 __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[3][4], const uint32_t (&alo)[3][4],
                                        const uint32_t* __restrict__ fhi, const uint32_t* __restrict__ flo,
@@ -149,8 +200,10 @@ __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[
         const uint2 bl = *reinterpret_cast<const uint2*>(flo + ((kt * NT + nt) * 32 + lane) * 2);
         mma_bf16(D[nt], alo[kt], bh.x, bh.y);
         mma_bf16(D[nt], ahi[kt], bl.x, bl.y);
+      } else if (SPLIT == 2) {
+        mma_t<2>(D[nt], alo[kt], bh.x, bh.y);
       }
-      mma_bf16(D[nt], ahi[kt], bh.x, bh.y);
+      mma_t<SPLIT>(D[nt], ahi[kt], bh.x, bh.y);
     }
 }
 
@@ -325,9 +378,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 
   // GRU update of 16 rows held by the warp (lane: rows g and g+8, columns
   // COLS) from their neighbour sums s and states h; ok[rr] = 0 for padding
+  // SPLIT 1/3: bf16 [zr hi | zr lo | hh hi | hh lo]; SPLIT 2: fp16 [zr | hh]
   const uint32_t* zr_hi = WF;
   const uint32_t* zr_lo = WF + kZrWords;
-  const uint32_t* hh_hi = WF + 2 * kZrWords;
+  const uint32_t* hh_hi = WF + (SPLIT == 2 ? kZrWords : 2 * kZrWords);
   const uint32_t* hh_lo = WF + 2 * kZrWords + kHhWords;
   auto gru16 = [&](const float (&sv)[2][6], const float (&h)[2][6], float (&hn)[2][6], const bool (&ok)[2]) {
     float bz[6], br[6], bh[6];
@@ -397,7 +451,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     }
     // factored covalent phase: only the ligand rows move
     const int prow = FACT && ph == 0 ? nLp : npad;
-    for (int i = threadIdx.x; i < kPhaseWords; i += blockDim.x) WF[i] = a.wfrag[ph][i];
+    if (SPLIT == 2) {
+      for (int i = threadIdx.x; i < kZrWords + kHhWords; i += blockDim.x) WF[i] = a.wfrag16[ph][i];
+    } else {
+      for (int i = threadIdx.x; i < kPhaseWords; i += blockDim.x) WF[i] = a.wfrag[ph][i];
+    }
     for (int i = threadIdx.x; i < 72; i += blockDim.x) WB[i] = a.wbias[ph][i];
     if (threadIdx.x < kBins) hist[threadIdx.x] = 0;
     if (threadIdx.x < 4) CTL[threadIdx.x] = 0;
@@ -609,11 +667,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   for (int j = 0; j < 16; ++j) { acc[j][0] = 0.f; acc[j][1] = 0.f; }
   // gather fragments: stage into the (now free) neighbour-sum buffer when it
   // is large enough, else read them through L1
-  const uint32_t* gsrc = a.gfrag;
+  // SPLIT 2: one fp16 fragment set (the layout of the bf16 "hi" half)
+  const uint32_t* gsrc = SPLIT == 2 ? a.gfrag16 : a.gfrag;
   const float* gb = a.gbias;
   if (hrows * 24 >= kGatherWords + 256) {
     uint32_t* gs = reinterpret_cast<uint32_t*>(Hn);
-    for (int i = threadIdx.x; i < kGatherWords; i += blockDim.x) gs[i] = a.gfrag[i];
+    const int gw = SPLIT == 2 ? kGatherWords / 2 : kGatherWords;
+    for (int i = threadIdx.x; i < gw; i += blockDim.x) gs[i] = gsrc[i];
     float* gbs = reinterpret_cast<float*>(gs + kGatherWords);
     for (int i = threadIdx.x; i < 256; i += blockDim.x) gbs[i] = a.gbias[i];
     gsrc = gs;
@@ -663,6 +723,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           mma_bf16(Dv, ahi[0], bvl.x, bvl.y);
           mma_bf16(Dg, ahi[0], bgh.x, bgh.y);
           mma_bf16(Dv, ahi[0], bvh.x, bvh.y);
+        } else if (SPLIT == 2) {
+          mma_f16_c(Dg, alo[0], bgh.x, bgh.y, Cg);
+          mma_f16_c(Dv, alo[0], bvh.x, bvh.y, Cv);
+          mma_t<2>(Dg, ahi[0], bgh.x, bgh.y);
+          mma_t<2>(Dv, ahi[0], bvh.x, bvh.y);
         } else {
           mma_bf16_c(Dg, ahi[0], bgh.x, bgh.y, Cg);
           mma_bf16_c(Dv, ahi[0], bvh.x, bvh.y, Cv);
@@ -678,9 +743,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           mma_bf16_k8(Dv, alo[1][0], alo[1][1], bvh);
           mma_bf16_k8(Dg, ahi[1][0], ahi[1][1], bgl);
           mma_bf16_k8(Dv, ahi[1][0], ahi[1][1], bvl);
+        } else if (SPLIT == 2) {
+          mma_t_k8<2>(Dg, alo[1][0], alo[1][1], bgh);
+          mma_t_k8<2>(Dv, alo[1][0], alo[1][1], bvh);
         }
-        mma_bf16_k8(Dg, ahi[1][0], ahi[1][1], bgh);
-        mma_bf16_k8(Dv, ahi[1][0], ahi[1][1], bvh);
+        mma_t_k8<SPLIT>(Dg, ahi[1][0], ahi[1][1], bgh);
+        mma_t_k8<SPLIT>(Dv, ahi[1][0], ahi[1][1], bvh);
       }
 #pragma unroll
       {
@@ -793,12 +861,17 @@ int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes
   a.heavy_cap = kMaxHeavy;
   const size_t smem = gnn_mma_smem_bytes(max_nodes);
   const int w = gnn_warps();
+  if (split == 2) {
+    if (!a.wfrag16[0] || !a.wfrag16[1] || !a.gfrag16) return FS_EINVAL;
+    if (a.fact_cnt) return launch_gnn_mma_t<2, true, 20>(a, n_poses, smem, st);
+    return launch_gnn_mma_t<2, false, 20>(a, n_poses, smem, st);
+  }
   if (a.fact_cnt) {
     if (w == 16) return launch_gnn_mma_t<3, true, 16>(a, n_poses, smem, st);
     if (w == 24) return launch_gnn_mma_t<3, true, 24>(a, n_poses, smem, st);
     return launch_gnn_mma_t<3, true, 20>(a, n_poses, smem, st);
   }
-  if (split != 3) return launch_gnn_mma_t<1, false, 20>(a, n_poses, smem, st);
+  if (split == 1) return launch_gnn_mma_t<1, false, 20>(a, n_poses, smem, st);
   if (w == 16) return launch_gnn_mma_t<3, false, 16>(a, n_poses, smem, st);
   if (w == 24) return launch_gnn_mma_t<3, false, 24>(a, n_poses, smem, st);
   return launch_gnn_mma_t<3, false, 20>(a, n_poses, smem, st);

@@ -16,10 +16,18 @@ from tests._cfg import COHERENT, GRAPH, VOXEL  # noqa: E402
 
 @pytest.fixture(scope="module")
 def env():
+    """The fp32-class SG-CNN (FS_GNN_SPLIT=3) for this module: a batch with
+    128-atom ligands exceeds the tensor-core SG-CNN's shared memory on the
+    full path, which then runs the FFMA kernel, so the factored path (which
+    fits) is compared against fp32 arithmetic."""
+    import os
+
     import torch
 
     from paper_2104_04547_b200 import engine as E
     from paper_2104_04547_b200 import models, synth
+    prev = os.environ.get("FS_GNN_SPLIT")
+    os.environ["FS_GNN_SPLIT"] = "3"
     vcfg, gcfg, fcfg = models.VoxelHeadConfig(), models.GraphHeadConfig(), models.table_coherent_fusion_config()
     dm = E.DeviceModel(vcfg, gcfg, fcfg, models.FusionModel(vcfg, gcfg, fcfg, seed=0).all_params())
     if not dm.supports("bf16"):
@@ -33,7 +41,11 @@ def env():
           np.concatenate([[0], np.cumsum([len(p.xyz) for p in pockets])]))
     batch = E.batch_from_arrays(lib.xyz, lib.elem, lib.role, lib.atom_off, pocket=pk, pose_target=lib.target)
     cache = dm.prepare_pockets(batch.pocket_xyz, batch.pocket_elem, batch.pocket_role, batch.pocket_off)
-    return torch, E, synth, dm, pockets, lib, pk, batch, cache
+    yield torch, E, synth, dm, pockets, lib, pk, batch, cache
+    if prev is None:
+        os.environ.pop("FS_GNN_SPLIT", None)
+    else:
+        os.environ["FS_GNN_SPLIT"] = prev
 
 
 def _rel(a, b):
