@@ -481,7 +481,8 @@ def main():
                     "peak": bf16_sus, "unit": "TFLOP/s", "traffic": None}
         # DRAM traffic of the dominant kernel: dram__bytes_read+write per pose
         # from the committed ncu --set full capture, scaled to this launch
-        tr_prefix = {"gnn": "gnn_mma_kernel<3, 0," if precision == "bf16" else None,
+        gsplit = os.environ.get("FS_GNN_SPLIT", "2")
+        tr_prefix = {"gnn": f"gnn_mma_kernel<{gsplit}, 0," if precision == "bf16" else None,
                      "conv1": "conv_umma_kernel<Cfg<16, 8, 32, 5,",
                      "conv2": "conv_umma_kernel<Cfg<16, 32, 32, 3,",
                      "featurize": "graph_csr_kernel<0>"}.get(dom_name)
