@@ -140,6 +140,7 @@ template <int SPLIT>
 __device__ __forceinline__ void put_a(uint32_t (&hi)[4], uint32_t (&lo)[4], int q, float x0, float x1) {
   if (SPLIT == 3) split2(x0, x1, hi[q], lo[q]);
   else if (SPLIT == 2) split2_f16(x0, x1, hi[q], lo[q]);
+  else if (SPLIT == 5) { const __half2 v = __floats2half2_rn(x0, x1); hi[q] = *reinterpret_cast<const uint32_t*>(&v); }
   else hi[q] = pack_bf16(x0, x1);
 }
 
@@ -693,14 +694,18 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         h[rr][c] = hv.x; h[rr][c + 1] = hv.y;
       }
     }
-    // k-tile 0: h[0..15]; k-tile 1: h[16..23] | zero padding
+    // k-tile 0: h[0..15]; k-tile 1: h[16..23] | zero padding.  With the fp16
+    // weights (SPLIT 2) the pool takes h as one fp16 pass (PS 5): its
+    // rounding is per node and the mean over the pose's nodes averages it,
+    // unlike the recurrent GRU inputs
+    constexpr int PS = SPLIT == 2 ? 5 : SPLIT;
     uint32_t ahi[2][4], alo[2][4];
-    put_a<SPLIT>(ahi[0], alo[0], 0, h[0][0], h[0][1]);
-    put_a<SPLIT>(ahi[0], alo[0], 1, h[1][0], h[1][1]);
-    put_a<SPLIT>(ahi[0], alo[0], 2, h[0][2], h[0][3]);
-    put_a<SPLIT>(ahi[0], alo[0], 3, h[1][2], h[1][3]);
-    put_a<SPLIT>(ahi[1], alo[1], 0, h[0][4], h[0][5]);
-    put_a<SPLIT>(ahi[1], alo[1], 1, h[1][4], h[1][5]);
+    put_a<PS>(ahi[0], alo[0], 0, h[0][0], h[0][1]);
+    put_a<PS>(ahi[0], alo[0], 1, h[1][0], h[1][1]);
+    put_a<PS>(ahi[0], alo[0], 2, h[0][2], h[0][3]);
+    put_a<PS>(ahi[0], alo[0], 3, h[1][2], h[1][3]);
+    put_a<PS>(ahi[1], alo[1], 0, h[0][4], h[0][5]);
+    put_a<PS>(ahi[1], alo[1], 1, h[1][4], h[1][5]);
     const bool v0 = valid(tile * 16 + g), v1 = valid(tile * 16 + g + 8);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -724,10 +729,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           mma_bf16(Dg, ahi[0], bgh.x, bgh.y);
           mma_bf16(Dv, ahi[0], bvh.x, bvh.y);
         } else if (SPLIT == 2) {
-          mma_f16_c(Dg, alo[0], bgh.x, bgh.y, Cg);
-          mma_f16_c(Dv, alo[0], bvh.x, bvh.y, Cv);
-          mma_t<2>(Dg, ahi[0], bgh.x, bgh.y);
-          mma_t<2>(Dv, ahi[0], bvh.x, bvh.y);
+          mma_f16_c(Dg, ahi[0], bgh.x, bgh.y, Cg);
+          mma_f16_c(Dv, ahi[0], bvh.x, bvh.y, Cv);
         } else {
           mma_bf16_c(Dg, ahi[0], bgh.x, bgh.y, Cg);
           mma_bf16_c(Dv, ahi[0], bvh.x, bvh.y, Cv);
@@ -743,9 +746,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           mma_bf16_k8(Dv, alo[1][0], alo[1][1], bvh);
           mma_bf16_k8(Dg, ahi[1][0], ahi[1][1], bgl);
           mma_bf16_k8(Dv, ahi[1][0], ahi[1][1], bvl);
-        } else if (SPLIT == 2) {
-          mma_t_k8<2>(Dg, alo[1][0], alo[1][1], bgh);
-          mma_t_k8<2>(Dv, alo[1][0], alo[1][1], bvh);
         }
         mma_t_k8<SPLIT>(Dg, ahi[1][0], ahi[1][1], bgh);
         mma_t_k8<SPLIT>(Dv, ahi[1][0], ahi[1][1], bvh);
