@@ -740,6 +740,7 @@ __device__ __forceinline__ bool fact_decide(const PoseView& pv, float d2f, float
 
 __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_ncnt[kFactMaxLig];
   __shared__ int s_flag;
   __shared__ double s_red[kCsrWarps];
   __shared__ int warp_tot[32];
@@ -776,7 +777,6 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
     const float4 v = make_float4((float)x, (float)y, (float)z, 0.f);
     if (i < np) pf[i] = v; else lf[i - np] = v;
   }
-  for (int i = threadIdx.x; i < np * kFactWords; i += blockDim.x) mask[i] = 0u;
   if (bad) atomicOr(&s_flag, 1);
   for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
   if (lane == 0) s_red[warp] = amax;
@@ -792,23 +792,49 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
   const float n_lo2 = prefilter ? ((float)a.tn - delta) * ((float)a.tn - delta) : -1.0f;
   const float n_hi2 = prefilter ? ((float)a.tn + delta) * ((float)a.tn + delta) : INFINITY;
 
-  // ---- non-covalent (ligand x pocket) bitmasks; ligand-ligand covalent degrees ----
+  // ---- non-covalent (ligand x pocket) bitmasks: lanes over pocket atoms,
+  // loop over the ligand atoms (broadcast reads); each lane builds its pocket
+  // row's mask in registers (no mask atomics), ligand-row counts accumulate
+  // per lane.  Same fp32 operands and order (ligand - pocket) as before. ----
+  for (int i = threadIdx.x; i < kFactMaxLig; i += blockDim.x) s_ncnt[i] = 0;
+  __syncthreads();
+  {
+    int acc[kFactWords] = {0, 0, 0, 0};   // lane l: hits of ligand atoms 32w + l
+    for (int j0 = warp * 32; j0 < np; j0 += kCsrWarps * 32) {
+      const int j = j0 + lane;
+      const bool jv = j < np;
+      const float4 fj = pf[jv ? j : 0];
+      uint32_t m[kFactWords] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int w = 0; w < kFactWords; ++w) {
+        const int s1 = min(nL, 32 * (w + 1));
+        for (int s = 32 * w; s < s1; ++s) {
+          const float4 fi = lf[s];
+          const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+          const float d2f = dx * dx + dy * dy + dz * dz;
+          bool hit;
+          if (d2f > n_hi2) hit = false;
+          else if (d2f <= n_lo2) hit = jv;
+          else hit = jv && exact_pair_slow(pv, np + s, j, rmax2, a.tn);
+          m[w] |= (hit ? 1u : 0u) << (s & 31);
+          const int c = __popc(__ballot_sync(0xffffffffu, hit));
+          acc[w] += lane == (s & 31) ? c : 0;
+        }
+      }
+      if (jv) {
+#pragma unroll
+        for (int w = 0; w < kFactWords; ++w) mask[j * kFactWords + w] = m[w];
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < kFactWords; ++w)
+      if (acc[w]) atomicAdd(&s_ncnt[32 * w + lane], acc[w]);
+  }
+  // ligand-ligand covalent degrees: one warp per ligand atom
   for (int s = warp; s < nL; s += kCsrWarps) {
     double xi, yi, zi; int32_t e_, r_;
     pv.atom(np + s, xi, yi, zi, e_, r_);
     const float4 fi = lf[s];
-    int cn = 0;
-    for (int j0 = 0; j0 < np; j0 += 32) {
-      const int j = j0 + lane;
-      bool hit = false;
-      if (j < np) {
-        const float4 fj = pf[j];
-        const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
-        hit = fact_decide(pv, dx * dx + dy * dy + dz * dz, n_lo2, n_hi2, xi, yi, zi, j, rmax2, a.tn);
-      }
-      cn += __popc(__ballot_sync(0xffffffffu, hit));
-      if (hit) atomicOr(&mask[j * kFactWords + (s >> 5)], 1u << (s & 31));
-    }
     int cc = 0;
     for (int j0 = 0; j0 < nL; j0 += 32) {
       const int j = j0 + lane;
@@ -820,9 +846,10 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
       }
       cc += __popc(__ballot_sync(0xffffffffu, hit));
     }
-    if (lane == 0) { offn[s] = cn; offc[s] = cc; }
+    if (lane == 0) offc[s] = cc;
   }
   __syncthreads();
+  for (int s = threadIdx.x; s < nL; s += blockDim.x) offn[s] = s_ncnt[s];
   for (int j = threadIdx.x; j < np; j += blockDim.x) {
     uint32_t any = 0u;
 #pragma unroll
