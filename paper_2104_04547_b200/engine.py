@@ -5,6 +5,7 @@ through the C-ABI.  Torch provides device memory and the current stream only.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -300,7 +301,11 @@ class DeviceModel:
             N.check(L.fs_model_create(C.byref(self.desc), c_names, c_ptrs, len(names), _ptr(self.blob),
                                       nbytes, _stream(), C.byref(handle)), "fs_model_create")
         self.handle = handle
-        self._ws = None
+        # workspaces are per host thread: the reference runs scorer plugins
+        # concurrently from a thread pool (harness.py:374-376) and a frozen
+        # model must be safe for concurrent prediction; the
+        # packed weight blob is read-only
+        self._tls = threading.local()
 
     def __del__(self):
         try:
@@ -321,10 +326,12 @@ class DeviceModel:
         return int(_g(self.gcfg, "gather_width_noncov"))
 
     def workspace(self, nbytes: int) -> torch.Tensor:
-        if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = None
-            self._ws = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.device)
-        return self._ws
+        ws = getattr(self._tls, "ws", None)
+        if ws is None or ws.numel() < nbytes:
+            self._tls.ws = None
+            ws = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.device)
+            self._tls.ws = ws
+        return ws
 
     # -- scoring --------------------------------------------------------------
     def score_poses(self, batch: PoseBatch, precision="fp32", max_edges_per_pose=40000,

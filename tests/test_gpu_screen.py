@@ -117,3 +117,49 @@ def test_factored_screen_matches_full_screen(setup):
     assert torch.equal(fact["topk_idx"], full["topk_idx"])
     assert torch.equal(fact["best_pose"], full["best_pose"])
     assert torch.equal(fact["topk_compound_idx"], full["topk_compound_idx"])
+
+
+def test_concurrent_scoring_threads_bitwise():
+    """The reference calls scorer plugins concurrently from a thread pool
+    (harness.py:374-376; frozen models are safe for concurrent
+    read-only prediction).  Four host threads, each on its own CUDA stream,
+    score different batches with one DeviceModel: every result equals the
+    sequential one bitwise (per-thread workspaces, read-only weight blob)."""
+    import threading
+
+    import torch
+
+    from paper_2104_04547_b200 import engine as E
+    from paper_2104_04547_b200 import models, synth
+    vcfg, gcfg, fcfg = models.VoxelHeadConfig(), models.GraphHeadConfig(), models.table_coherent_fusion_config()
+    dm = E.DeviceModel(vcfg, gcfg, fcfg, models.FusionModel(vcfg, gcfg, fcfg, seed=0).all_params())
+    pocket = synth.make_pocket(1000, seed=31)
+    pk = (pocket.xyz, pocket.elem, pocket.role, np.array([0, 1000]))
+    batches = []
+    for k in range(4):
+        lib = synth.make_poses(6 + k, poses_per_compound=5, seed=40 + k)
+        batches.append(E.batch_from_arrays(lib.xyz, lib.elem, lib.role, lib.atom_off, pocket=pk,
+                                           pose_target=lib.target))
+    want = [dm.score_poses(b, "bf16")["scores"].cpu().numpy() for b in batches]
+    got = [None] * 4
+    errors = []
+
+    def work(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    out = dm.score_poses(batches[k], "bf16")["scores"]
+                s.synchronize()
+                got[k] = out.cpu().numpy()
+        except Exception as exc:  # noqa: BLE001
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k in range(4):
+        assert np.array_equal(got[k], want[k]), k
