@@ -15,6 +15,7 @@ relative) by default; "bf16" selects the tcgen05 tensor-core Conv3d path
 from __future__ import annotations
 
 import hashlib
+import threading
 from dataclasses import asdict, dataclass, field
 
 import numpy as np
@@ -274,6 +275,17 @@ class FusionModel:
         self.box_size = 16.0
         self._dev = None
         self._dev_key = None
+        self._dev_lock = threading.Lock()   # concurrent scorer threads share one packed model
+
+    def __getstate__(self):   # picklable / deep-copyable: the packed device model is rebuilt lazily
+        st = dict(self.__dict__)
+        st["_dev"], st["_dev_key"] = None, None
+        del st["_dev_lock"]
+        return st
+
+    def __setstate__(self, st):
+        self.__dict__.update(st)
+        self._dev_lock = threading.Lock()
 
     @classmethod
     def from_heads(cls, voxel_params, voxel_cfg, graph_params, graph_cfg, fusion_cfg, seed=0):
@@ -292,11 +304,12 @@ class FusionModel:
                         ("fusion", self.fusion_params))), self.box_size,
                repr(sorted((k, tuple(np.asarray(v["mean"]).ravel()), tuple(np.asarray(v["var"]).ravel()))
                            for k, v in self.bn_state.items())))
-        if self._dev is None or self._dev_key != key:
-            self._dev = DeviceModel(self.voxel_cfg, self.graph_cfg, self.fusion_cfg, self.all_params(),
-                                    self.box_size, bn_state=self.bn_state or None)
-            self._dev_key = key
-        return self._dev
+        with self._dev_lock:
+            if self._dev is None or self._dev_key != key:
+                self._dev = DeviceModel(self.voxel_cfg, self.graph_cfg, self.fusion_cfg, self.all_params(),
+                                        self.box_size, bn_state=self.bn_state or None)
+                self._dev_key = key
+            return self._dev
 
     # -- prediction ---------------------------------------------------------
     def predict_batch(self, items, batch_seed: int = 0):

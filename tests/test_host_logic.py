@@ -153,3 +153,19 @@ def test_validate_item_reason_strings():
                           cx.ComplexGraph(np.zeros((2, 5)), g.covalent_edges, g.noncovalent_edges,
                                           g.covalent_dists, g.noncovalent_dists)))
     assert r.startswith("graph feature width")
+
+
+def test_fusion_model_pickles_and_deep_copies():
+    """Campaign drivers may copy or pickle the model (the packed device model
+    and its lock are rebuilt lazily, never serialised)."""
+    import copy
+    import pickle
+
+    from paper_2104_04547_b200 import models
+    m = models.FusionModel(models.VoxelHeadConfig(), models.GraphHeadConfig(),
+                           models.table_coherent_fusion_config(), seed=0)
+    for m2 in (copy.deepcopy(m), pickle.loads(pickle.dumps(m))):
+        assert m2._dev is None
+        assert m2._dev_lock is not None
+        for k, v in m.all_params().items():
+            assert np.array_equal(v, m2.all_params()[k])
