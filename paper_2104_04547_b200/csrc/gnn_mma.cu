@@ -753,8 +753,22 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
       {
         // rows g (D[0], D[1]) and g+8 (D[2], D[3]), columns 8j+2t, +1
-        sigmoid_pre2(Dg[0], Dg[1]); sigmoid_pre2(Dg[2], Dg[3]);
-        tanh_pre2(Dv[0], Dv[1]); tanh_pre2(Dv[2], Dv[3]);
+        if constexpr (SPLIT == 2) {
+          // one MUFU.TANH per activation (2^-10.7): sigmoid(x) = (1 + tanh(x/2)) / 2
+          // with u = -log2(e) x and v = 2 log2(e) x as staged
+          constexpr float kG = -0.34657359027997264f, kV = 0.34657359027997264f;   // 1/(2 log2 e)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float tg, tv;
+            asm("tanh.approx.f32 %0, %1;" : "=f"(tg) : "f"(Dg[e] * kG));
+            asm("tanh.approx.f32 %0, %1;" : "=f"(tv) : "f"(Dv[e] * kV));
+            Dg[e] = fmaf(0.5f, tg, 0.5f);
+            Dv[e] = tv;
+          }
+        } else {
+          sigmoid_pre2(Dg[0], Dg[1]); sigmoid_pre2(Dg[2], Dg[3]);
+          tanh_pre2(Dv[0], Dv[1]); tanh_pre2(Dv[2], Dv[3]);
+        }
         fmul2(Dg[0], Dg[1], Dv[0], Dv[1]);
         fmul2(Dg[2], Dg[3], Dv[2], Dv[3]);
         const float x00 = v0 ? Dg[0] : 0.f, x01 = v0 ? Dg[1] : 0.f;
