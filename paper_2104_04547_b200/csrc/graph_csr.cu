@@ -475,12 +475,21 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         uint64_t rm = 0ull;
         const int len = qe - qb;
         if (len <= 64) {
+          // branch-free candidate loop: fp32-certain hits and in-band pairs
+          // as bit sets; the (rare) band is settled exactly afterwards
+          uint64_t band = 0ull;
           for (int q = qb; q < qe; ++q) {
             const int j = cell_list[q];
             const float4 fj = pf[j];
             const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
-            const bool hit = decide_i(ddx * ddx + ddy * ddy + ddz * ddz, c_lo2, c_hi2, i, j, a.tc);
-            rm |= (uint64_t)hit << (q - qb);
+            const float d2f = ddx * ddx + ddy * ddy + ddz * ddz;
+            rm |= (uint64_t)(d2f <= c_lo2) << (q - qb);
+            band |= (uint64_t)(d2f > c_lo2 && d2f <= c_hi2) << (q - qb);
+          }
+          while (band) {
+            const int k = __ffsll((long long)band) - 1;
+            band &= band - 1;
+            if (decide_i(c_lo2 + 1.0f, c_lo2, INFINITY, i, cell_list[qb + k], a.tc)) rm |= 1ull << k;
           }
         } else {   // crowded column: counted only, the fill re-tests this row
           over = true;
