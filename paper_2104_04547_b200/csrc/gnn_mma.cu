@@ -378,13 +378,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   }
 
   // GRU update of 16 rows held by the warp (lane: rows g and g+8, columns
-  // COLS) from their neighbour sums s and states h; ok[rr] = 0 for padding
+  // COLS) from their neighbour sums s and states h
   // SPLIT 1/3: bf16 [zr hi | zr lo | hh hi | hh lo]; SPLIT 2: fp16 [zr | hh]
   const uint32_t* zr_hi = WF;
   const uint32_t* zr_lo = WF + kZrWords;
   const uint32_t* hh_hi = WF + (SPLIT == 2 ? kZrWords : 2 * kZrWords);
   const uint32_t* hh_lo = WF + 2 * kZrWords + kHhWords;
-  auto gru16 = [&](const float (&sv)[2][6], const float (&h)[2][6], float (&hn)[2][6], const bool (&ok)[2]) {
+  auto gru16 = [&](const float (&sv)[2][6], const float (&h)[2][6], float (&hn)[2][6]) {
     float bz[6], br[6], bh[6];
 #pragma unroll
     for (int c = 0; c < 6; ++c) { bz[c] = WB[COLS(c)]; br[c] = WB[24 + COLS(c)]; bh[c] = WB[48 + COLS(c)]; }
@@ -427,8 +427,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         tanh_pre2(u0, u1);                                 // hh
         fadd2(u0, u1, -h[rr][c], -h[rr][c + 1]);          // hh - h
         ffma2(u0, u1, z[rr][c], z[rr][c + 1], h[rr][c], h[rr][c + 1]);   // h + z (hh - h)
-        hn[rr][c] = ok[rr] ? u0 : 0.f;
-        hn[rr][c + 1] = ok[rr] ? u1 : 0.f;
+        // padding rows (ok false) evolve too: no CSR row lists them and the
+        // pool masks them, so their values are never read
+        hn[rr][c] = u0;
+        hn[rr][c + 1] = u1;
       }
   };
   auto load_h = [&](int row, float (&h)[6]) {
@@ -621,8 +623,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           float h[2][6], hn[2][6];
           load_h(r0, h[0]);
           load_h(r1, h[1]);
-          const bool ok[2] = {valid(r0), valid(r1)};
-          gru16(sv, h, hn, ok);
+          gru16(sv, h, hn);
           if (r0 < npad) store_hn(r0, hn[0]);
           if (r1 < npad) store_hn(r1, hn[1]);
         } else {
@@ -644,8 +645,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           }
           load_h(r0, h[0]);
           load_h(r1, h[1]);
-          const bool ok[2] = {valid(r0), valid(r1)};
-          gru16(sv, h, hn, ok);
+          gru16(sv, h, hn);
           if (r0 < npad) store_hn(r0, hn[0]);
           if (r1 < npad) store_hn(r1, hn[1]);
         }
@@ -750,7 +750,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         mma_t_k8<SPLIT>(Dg, ahi[1][0], ahi[1][1], bgh);
         mma_t_k8<SPLIT>(Dv, ahi[1][0], ahi[1][1], bvh);
       }
-#pragma unroll
       {
         // rows g (D[0], D[1]) and g+8 (D[2], D[3]), columns 8j+2t, +1
         if constexpr (SPLIT == 2) {
