@@ -263,10 +263,12 @@ __device__ __forceinline__ void tanh_pre2(float& u0, float& u1) {
   sigmoid_pre2(u0, u1);
   ffma2(u0, u1, -2.0f, -2.0f, 1.0f, 1.0f);
 }
-__device__ __forceinline__ void acc_row(float (&q)[4], float (&d)[2], const float* __restrict__ row, int t) {
-  const float* b = row + 6 * t;
-  const float4 v = *reinterpret_cast<const float4*>(b + ((t & 1) << 1));
-  const float2 w = *reinterpret_cast<const float2*>(b + ((t & 1) ? 0 : 4));
+// accumulate neighbour row j from the lane's two per-step bases (H4 = H + 6t
+// + 2(t&1): its 16-byte half, H2: its 8-byte half): one multiply-add each
+__device__ __forceinline__ void acc_row_at(float (&q)[4], float (&d)[2], const float* __restrict__ H4,
+                                           const float* __restrict__ H2, int j) {
+  const float4 v = *reinterpret_cast<const float4*>(H4 + j * 24);
+  const float2 w = *reinterpret_cast<const float2*>(H2 + j * 24);
   fadd2(q[0], q[1], v.x, v.y);
   fadd2(q[2], q[3], v.z, v.w);
   fadd2(d[0], d[1], w.x, w.y);
@@ -507,6 +509,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     const int nitems = nh + nlt + nht;
 
     for (int step = 0; step < a.k_steps[ph]; ++step) {
+      const float* H4 = Hc + 6 * t + ((t & 1) << 1);   // this step's gather bases (acc_row_at)
+      const float* H2 = Hc + 6 * t + ((t & 1) ? 0 : 4);
       // Items, handed out in order by a counter: heavy-row sums (-> HS), then
       // the degree-sorted light tiles (gather + GRU), then the heavy tiles
       // (GRU from HS, after every heavy sum is in).
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
               const int j[4] = {static_cast<int>(v.x & 0xffffu), static_cast<int>(v.x >> 16),
                                 static_cast<int>(v.y & 0xffffu), static_cast<int>(v.y >> 16)};
 #pragma unroll
-              for (int u = 0; u < 4; ++u) acc_row(sq, sd, Hc + j[u] * 24, t);
+              for (int u = 0; u < 4; ++u) acc_row_at(sq, sd, H4, H2, j[u]);
             }
           } else {
             for (int q = g; q < d; q += 32) {
@@ -536,7 +540,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
               for (int u = 0; u < 4; ++u) j[u] = q + 8 * u < d ? __ldg(c + q + 8 * u) : npad;
 #pragma unroll
-              for (int u = 0; u < 4; ++u) acc_row(sq, sd, Hc + j[u] * 24, t);
+              for (int u = 0; u < 4; ++u) acc_row_at(sq, sd, H4, H2, j[u]);
             }
           }
           float s6[6] = {sq[0], sq[1], sq[2], sq[3], sd[0], sd[1]};   // storage order
@@ -587,8 +591,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
               ids4(c1, q, e1, j1); ids4(c1, q + 4, e1, j1 + 4);
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
-                acc_row(sq[0], sd[0], Hc + j0[u] * 24, t);
-                acc_row(sq[1], sd[1], Hc + j1[u] * 24, t);
+                acc_row_at(sq[0], sd[0], H4, H2, j0[u]);
+                acc_row_at(sq[1], sd[1], H4, H2, j1[u]);
               }
             }
             if (q < dm) {
@@ -597,8 +601,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
               ids4(c1, q, e1, j1);
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                acc_row(sq[0], sd[0], Hc + j0[u] * 24, t);
-                acc_row(sq[1], sd[1], Hc + j1[u] * 24, t);
+                acc_row_at(sq[0], sd[0], H4, H2, j0[u]);
+                acc_row_at(sq[1], sd[1], H4, H2, j1[u]);
               }
             }
           } else {
@@ -612,8 +616,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
               for (int u = 0; u < 4; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                acc_row(sq[0], sd[0], Hc + j0[u] * 24, t);
-                acc_row(sq[1], sd[1], Hc + j1[u] * 24, t);
+                acc_row_at(sq[0], sd[0], H4, H2, j0[u]);
+                acc_row_at(sq[1], sd[1], H4, H2, j1[u]);
               }
             }
           }
