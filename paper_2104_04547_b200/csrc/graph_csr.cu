@@ -477,19 +477,24 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         if (len <= 64) {
           // branch-free candidate loop: fp32-certain hits and in-band pairs
           // as bit sets; the (rare) band is settled exactly afterwards
-          uint64_t band = 0ull;
+          bool anyband = false;
           for (int q = qb; q < qe; ++q) {
             const int j = cell_list[q];
             const float4 fj = pf[j];
             const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
             const float d2f = ddx * ddx + ddy * ddy + ddz * ddz;
             rm |= (uint64_t)(d2f <= c_lo2) << (q - qb);
-            band |= (uint64_t)(d2f > c_lo2 && d2f <= c_hi2) << (q - qb);
+            anyband |= d2f > c_lo2 && d2f <= c_hi2;
           }
-          while (band) {
-            const int k = __ffsll((long long)band) - 1;
-            band &= band - 1;
-            if (decide_i(c_lo2 + 1.0f, c_lo2, INFINITY, i, cell_list[qb + k], a.tc)) rm |= 1ull << k;
+          if (anyband) {   // rare: re-walk the column, settle in-band pairs exactly
+            for (int q = qb; q < qe; ++q) {
+              const int j = cell_list[q];
+              const float4 fj = pf[j];
+              const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
+              const float d2f = ddx * ddx + ddy * ddy + ddz * ddz;
+              if (d2f > c_lo2 && d2f <= c_hi2 && decide_i(c_lo2 + 1.0f, c_lo2, INFINITY, i, j, a.tc))
+                rm |= 1ull << (q - qb);
+            }
           }
         } else {   // crowded column: counted only, the fill re-tests this row
           over = true;
