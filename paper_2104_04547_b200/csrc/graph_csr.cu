@@ -475,16 +475,30 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         uint64_t rm = 0ull;
         const int len = qe - qb;
         if (len <= 64) {
-          // branch-free candidate loop: fp32-certain hits and in-band pairs
-          // as bit sets; the (rare) band is settled exactly afterwards
+          // branch-free candidate loop: fp32-certain hits as a bit set (32-bit
+          // for the usual short column), one in-band flag; the (rare) band is
+          // settled exactly afterwards
           bool anyband = false;
-          for (int q = qb; q < qe; ++q) {
-            const int j = cell_list[q];
-            const float4 fj = pf[j];
-            const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
-            const float d2f = ddx * ddx + ddy * ddy + ddz * ddz;
-            rm |= (uint64_t)(d2f <= c_lo2) << (q - qb);
-            anyband |= d2f > c_lo2 && d2f <= c_hi2;
+          if (len <= 32) {
+            uint32_t r32 = 0u;
+            for (int q = qb; q < qe; ++q) {
+              const int j = cell_list[q];
+              const float4 fj = pf[j];
+              const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
+              const float d2f = ddx * ddx + ddy * ddy + ddz * ddz;
+              r32 |= (uint32_t)(d2f <= c_lo2) << (q - qb);
+              anyband |= d2f > c_lo2 && d2f <= c_hi2;
+            }
+            rm = r32;
+          } else {
+            for (int q = qb; q < qe; ++q) {
+              const int j = cell_list[q];
+              const float4 fj = pf[j];
+              const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
+              const float d2f = ddx * ddx + ddy * ddy + ddz * ddz;
+              rm |= (uint64_t)(d2f <= c_lo2) << (q - qb);
+              anyband |= d2f > c_lo2 && d2f <= c_hi2;
+            }
           }
           if (anyband) {   // rare: re-walk the column, settle in-band pairs exactly
             for (int q = qb; q < qe; ++q) {
