@@ -389,7 +389,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   auto gru16 = [&](const float (&sv)[2][6], const float (&h)[2][6], float (&hn)[2][6]) {
     float bz[6], br[6], bh[6];
 #pragma unroll
-    for (int c = 0; c < 6; ++c) { bz[c] = WB[COLS(c)]; br[c] = WB[24 + COLS(c)]; bh[c] = WB[48 + COLS(c)]; }
+    for (int j = 0; j < 3; ++j) {   // columns 8j+2t, 8j+2t+1: one 8-byte load per gate
+      const float2 z2 = *reinterpret_cast<const float2*>(WB + 8 * j + 2 * t);
+      const float2 r2 = *reinterpret_cast<const float2*>(WB + 24 + 8 * j + 2 * t);
+      const float2 h2 = *reinterpret_cast<const float2*>(WB + 48 + 8 * j + 2 * t);
+      bz[2 * j] = z2.x; bz[2 * j + 1] = z2.y; br[2 * j] = r2.x; br[2 * j + 1] = r2.y;
+      bh[2 * j] = h2.x; bh[2 * j + 1] = h2.y;
+    }
     uint32_t ahi[3][4], alo[3][4];
     build_a48<SPLIT>(sv, h, ahi, alo);
     float Dzr[6][4];
