@@ -342,3 +342,37 @@ def test_best_pose_matches_reference_rule(pkg):
         for c in range(50):
             if (c, 0) in want:
                 assert (pid[idx[c]], float(sc[idx[c]])) == want[(c, 0)]
+
+
+@pytest.mark.parametrize("case", ["dense", "oversize"])
+def test_dense_and_oversize_poses_vs_oracle(pkg, case):
+    """Shapes the benchmark never produces: a compressed pocket where nearly
+    every row has >= 32 neighbours (more heavy rows than the SG-CNN's heavy
+    buffer holds, so the overflow rows take the light-tile path; edge lists far
+    above the default capacity), and a pocket larger than the tensor-core
+    SG-CNN's per-CTA node capacity (the bf16 path falls back to the FFMA
+    graph kernel).  Both precisions against the float64 oracle."""
+    cx, E, models, synth = pkg
+    if case == "dense":
+        base = synth.make_pocket(600, seed=31)
+        pocket = synth.Pocket(base.xyz * 0.3, base.elem, base.role, "dense")   # U[-2.4, 2.4)^3
+    else:
+        pocket = synth.make_pocket(2400, seed=32)
+    lib = synth.make_poses(2, poses_per_compound=2, seed=33)
+    vcfg, gcfg, fcfg = VOXEL, GRAPH, COHERENT
+    model = models.FusionModel(models.VoxelHeadConfig(), models.GraphHeadConfig(),
+                               models.table_coherent_fusion_config(), seed=0)
+    dm = model.device_model()
+    b = E.batch_from_arrays(lib.xyz, lib.elem, lib.role, lib.atom_off,
+                            pocket=(pocket.xyz, pocket.elem, pocket.role, np.array([0, len(pocket.xyz)])),
+                            pose_target=lib.target)
+    params = orc.init_params(vcfg, gcfg, fcfg, 0)
+    want = np.array([orc.score_pose(params, (vcfg, gcfg, fcfg), *synth.complex_arrays(pocket, lib, p))["score"]
+                     for p in range(lib.n_poses)])
+    for precision, tol in (("fp32", 1e-3), ("bf16", 3e-2)):
+        if not dm.supports(precision):
+            continue
+        out = dm.score_poses(b, precision)
+        assert not out["err"].cpu().numpy().any()
+        got = out["scores"].cpu().numpy().astype(np.float64)
+        assert _rel(got, want) < tol, (case, precision, got, want)
