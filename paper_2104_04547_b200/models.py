@@ -14,7 +14,6 @@ relative) by default; "bf16" selects the tcgen05 tensor-core Conv3d path
 
 from __future__ import annotations
 
-import hashlib
 import threading
 from dataclasses import asdict, dataclass, field
 
@@ -223,21 +222,25 @@ def late_fusion_predict(p_voxel, p_graph):
 
 def _pack_graphs(graphs):
     """Concatenate node features and lift per-graph i<j edges to global ids
-    (the block-diagonal adjacency of batch_graphs, models.py:233-256)."""
-    counts = np.array([g.n_nodes for g in graphs], dtype=np.int64)
+    (the block-diagonal adjacency of batch_graphs, models.py:233-256).
+    Vectorised: one concatenation per array, offsets added with np.repeat."""
+    feats_l = [np.asarray(g.node_features, dtype=np.float64) for g in graphs]
+    counts = np.array([len(f) for f in feats_l], dtype=np.int64)
     off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-    feats = np.concatenate([np.asarray(g.node_features, dtype=np.float64) for g in graphs]) \
-        if graphs else np.zeros((0, 1))
+    feats = np.concatenate(feats_l) if graphs else np.zeros((0, 1))
 
     def lift(attr):
-        parts = []
-        for g, o in zip(graphs, off[:-1]):
-            e = np.asarray(getattr(g, attr), dtype=np.int64).reshape(-1, 2)
-            if len(e):
-                if e.min() < 0 or e.max() >= g.n_nodes:
-                    raise ValueError(f"{attr} index out of range for a graph of {g.n_nodes} nodes")
-                parts.append(e + o)
-        return np.concatenate(parts) if parts else np.zeros((0, 2), dtype=np.int64)
+        parts = [np.asarray(getattr(g, attr), dtype=np.int64).reshape(-1, 2) for g in graphs]
+        sizes = np.array([len(e) for e in parts], dtype=np.int64)
+        if not sizes.sum():
+            return np.zeros((0, 2), dtype=np.int64)
+        e = np.concatenate(parts)
+        n_of = np.repeat(counts, sizes)
+        bad = (e.min(axis=1) < 0) | (e.max(axis=1) >= n_of)
+        if bad.any():
+            g = int(np.searchsorted(np.cumsum(sizes), int(np.flatnonzero(bad)[0]), side="right"))
+            raise ValueError(f"{attr} index out of range for a graph of {int(counts[g])} nodes")
+        return e + np.repeat(off[:-1], sizes)[:, None]
 
     return feats, off, lift("covalent_edges"), lift("noncovalent_edges")
 
@@ -248,14 +251,45 @@ def _to_dev(a, dtype=None):
     return t.to("cuda", non_blocking=False) if dtype is None else t.to("cuda", dtype=dtype)
 
 
-def _digest(params_sets) -> bytes:
-    h = hashlib.blake2b(digest_size=16)
-    for prefix, ps in params_sets:
-        for k in sorted(ps):
-            a = np.ascontiguousarray(ps[k], dtype=np.float64)
-            h.update(f"{prefix}/{k}{a.shape}".encode())
-            h.update(a.tobytes())
-    return h.digest()
+def _is_grid(x) -> bool:
+    """Duck-typed VoxelGrid: this package's, the reference's
+    (fusionscreen.complexes.VoxelGrid) or any object with ``.occupancy``."""
+    return hasattr(x, "occupancy")
+
+
+def _is_graph(x) -> bool:
+    """Duck-typed ComplexGraph (node features + the two i<j edge lists)."""
+    return all(hasattr(x, a) for a in ("node_features", "covalent_edges", "noncovalent_edges"))
+
+
+def _is_complex(x) -> bool:
+    """Duck-typed SyntheticComplex (positions / elements / roles)."""
+    return all(hasattr(x, a) for a in ("positions", "elements", "roles"))
+
+
+def _expected_shapes(vcfg, gcfg, fcfg) -> dict:
+    """Parameter shapes of init_*_params (models.py:150-218) without drawing."""
+    class _Shape:
+        def uniform(self, lo, hi, size):
+            return np.empty(size, dtype=np.float64)
+    r = _Shape()
+    out = {f"voxel/{k}": v.shape for k, v in init_voxel_params(vcfg, r).items()}
+    out.update({f"graph/{k}": v.shape for k, v in init_graph_params(gcfg, r).items()})
+    out.update({f"fusion/{k}": v.shape for k, v in
+                init_fusion_params(fcfg, gcfg.latent_width, vcfg.latent_width, r).items()})
+    return out
+
+
+def check_param_shapes(vcfg, gcfg, fcfg, flat: dict) -> None:
+    """Every parameter the configs need is present with its init shape (the
+    packer reads raw host pointers, so a mismatch must fail here)."""
+    want = _expected_shapes(vcfg, gcfg, fcfg)
+    for name, shape in want.items():
+        if name not in flat:
+            raise ValueError(f"missing parameter {name!r}")
+        got = np.shape(flat[name])
+        if tuple(got) != tuple(shape):
+            raise ValueError(f"parameter {name!r} has shape {tuple(got)}, expected {tuple(shape)}")
 
 
 class FusionModel:
@@ -275,17 +309,20 @@ class FusionModel:
         self.box_size = 16.0
         self._dev = None
         self._dev_key = None
+        self._version = 0
         self._dev_lock = threading.Lock()   # concurrent scorer threads share one packed model
+        self._tls = threading.local()       # per-thread pinned staging buffers
 
     def __getstate__(self):   # picklable / deep-copyable: the packed device model is rebuilt lazily
         st = dict(self.__dict__)
         st["_dev"], st["_dev_key"] = None, None
-        del st["_dev_lock"]
+        del st["_dev_lock"], st["_tls"]
         return st
 
     def __setstate__(self, st):
         self.__dict__.update(st)
         self._dev_lock = threading.Lock()
+        self._tls = threading.local()
 
     @classmethod
     def from_heads(cls, voxel_params, voxel_cfg, graph_params, graph_cfg, fusion_cfg, seed=0):
@@ -297,27 +334,73 @@ class FusionModel:
     def build_tape(self, *a, **k):
         raise NotImplementedError("autodiff tapes (training) are outside the B200 scoring path")
 
-    # -- device model (packed once; re-packed if parameters change) -----------
+    # -- device model (packed once; re-packed when parameters change) ---------
+    def invalidate(self) -> None:
+        """Drop the packed device weights.  set_params()/load() do this; call
+        it after editing a parameter array in place."""
+        with self._dev_lock:
+            self._version += 1
+            self._dev = None
+
+    def _cache_key(self):
+        # O(#params) identity check, no hashing of the 808k values: a new array
+        # bound to a name, a new dict, set_params() or invalidate() re-packs
+        ids = tuple((pre, id(d), tuple((k, id(v)) for k, v in d.items()))
+                    for pre, d in (("voxel", self.voxel_params), ("graph", self.graph_params),
+                                   ("fusion", self.fusion_params)))
+        bn = tuple((k, id(v.get("mean")), id(v.get("var"))) for k, v in sorted(self.bn_state.items()))
+        return (self._version, ids, bn, self.box_size)
+
     def device_model(self):
         from .engine import DeviceModel
-        key = (_digest((("voxel", self.voxel_params), ("graph", self.graph_params),
-                        ("fusion", self.fusion_params))), self.box_size,
-               repr(sorted((k, tuple(np.asarray(v["mean"]).ravel()), tuple(np.asarray(v["var"]).ravel()))
-                           for k, v in self.bn_state.items())))
+        key = self._cache_key()
         with self._dev_lock:
             if self._dev is None or self._dev_key != key:
-                self._dev = DeviceModel(self.voxel_cfg, self.graph_cfg, self.fusion_cfg, self.all_params(),
+                flat = self.all_params()
+                check_param_shapes(self.voxel_cfg, self.graph_cfg, self.fusion_cfg, flat)
+                self._dev = DeviceModel(self.voxel_cfg, self.graph_cfg, self.fusion_cfg, flat,
                                         self.box_size, bn_state=self.bn_state or None)
                 self._dev_key = key
             return self._dev
 
     # -- prediction ---------------------------------------------------------
+    def _pinned(self, name, numel, dtype):
+        import torch
+        buf = getattr(self._tls, name, None)
+        if buf is None or buf.numel() < numel or buf.dtype != dtype:
+            buf = torch.empty(max(int(numel * 1.25), 1), dtype=dtype).pin_memory()
+            setattr(self._tls, name, buf)
+        return buf
+
+    def _upload(self, name, a):
+        """Host array -> device through a per-thread pinned staging buffer
+        (one DMA; the caller synchronises before the buffer is reused)."""
+        import torch
+        a = np.ascontiguousarray(a)
+        t = torch.from_numpy(a)
+        buf = self._pinned(name, t.numel(), t.dtype)[: t.numel()].view(t.shape)
+        buf.copy_(t)
+        return buf.to("cuda", non_blocking=True)
+
+    def _upload_grids(self, items, valid):
+        import torch
+        shape = (len(valid), self.voxel_cfg.in_channels) + (self.voxel_cfg.grid_extent,) * 3
+        n = int(np.prod(shape))
+        buf = self._pinned("grids", n, torch.float64)[:n].view(shape)
+        host = buf.numpy()
+        for slot, i in enumerate(valid):          # one host copy per grid, straight into pinned memory
+            np.copyto(host[slot], items[i][0].occupancy, casting="unsafe")
+        return buf.to("cuda", non_blocking=True)
+
     def predict_batch(self, items, batch_seed: int = 0):
         """Scores (VoxelGrid, ComplexGraph) pairs (models.py:470-498).
 
         Returns (predictions, errors); malformed items never abort the batch.
-        ``batch_seed`` only seeds dropout in the reference's eval tape, where
-        dropout is the identity, so it does not change results."""
+        Items may be this package's featurizer output, the reference's
+        (fusionscreen.complexes.VoxelGrid / ComplexGraph) or any objects with
+        the same attributes.  ``batch_seed`` only seeds dropout in the
+        reference's eval tape, where dropout is the identity, so it does not
+        change results."""
         preds = [None] * len(items)
         errors = []
         valid = []
@@ -329,11 +412,11 @@ class FusionModel:
                 errors.append((i, reason))
         if not valid:
             return preds, errors
-        grids = np.stack([np.asarray(items[i][0].occupancy, dtype=np.float64) for i in valid])
         feats, off, ce, ne = _pack_graphs([items[i][1] for i in valid])
         dm = self.device_model()
-        out = dm.score_features(len(valid), grids=_to_dev(grids), feats=_to_dev(feats), node_off=_to_dev(off),
-                                cov_edges=_to_dev(ce), ncov_edges=_to_dev(ne), heads=7,
+        out = dm.score_features(len(valid), grids=self._upload_grids(items, valid),
+                                feats=self._upload("feats", feats), node_off=self._upload("off", off),
+                                cov_edges=self._upload("ce", ce), ncov_edges=self._upload("ne", ne), heads=7,
                                 precision=self.precision)
         scores = out["scores"].cpu().numpy().astype(np.float64)
         err = out["err"].cpu().numpy()
@@ -354,26 +437,33 @@ class FusionModel:
         return preds, errors
 
     def _validate_item(self, item):
-        """Host-side structural checks with the reference's reason strings
-        (models.py:511-529); finiteness is checked on device in the same pass
-        that uploads the data."""
+        """The reference's checks, in its order and with its reason strings
+        (models.py:511-529); types are duck-typed so the reference's own
+        featurizer output is accepted unchanged."""
         try:
             grid, graph = item
         except (TypeError, ValueError):
             return "item is not a (VoxelGrid, ComplexGraph) pair"
-        if not isinstance(grid, VoxelGrid) or not isinstance(graph, ComplexGraph):
+        if not _is_grid(grid) or not _is_graph(graph):
             return "item is not a (VoxelGrid, ComplexGraph) pair"
         want = (self.voxel_cfg.in_channels,) + (self.voxel_cfg.grid_extent,) * 3
-        if grid.occupancy.shape != want:
-            return f"voxel grid shape {grid.occupancy.shape} != {want}"
-        if graph.node_features.ndim != 2 or graph.node_features.shape[1] != self.graph_cfg.feature_width:
+        occ = np.asarray(grid.occupancy)
+        if occ.shape != want:
+            return f"voxel grid shape {occ.shape} != {want}"
+        if not np.all(np.isfinite(occ)):
+            return "voxel grid contains non-finite values"
+        nf = np.asarray(graph.node_features)
+        if nf.ndim != 2 or nf.shape[1] != self.graph_cfg.feature_width:
             return (f"graph feature width "
-                    f"{graph.node_features.shape} != {self.graph_cfg.feature_width}")
+                    f"{nf.shape} != {self.graph_cfg.feature_width}")
+        if not np.all(np.isfinite(nf)):
+            return "graph features contain non-finite values"
         return None
 
     def score_complexes(self, complexes):
         """Fused featurize + score of raw complexes on device (the screening
-        path: models.featurize (:638-651) then predict_batch).  Returns
+        path: models.featurize (:638-651) then predict_batch).  Accepts this
+        package's or the reference's SyntheticComplex (duck-typed).  Returns
         (scores float64 [P], err int32 [P])."""
         from .engine import batch_from_complexes
         b = batch_from_complexes(complexes)
@@ -393,21 +483,23 @@ class FusionModel:
             prefix, name = full.split("/", 1)
             target = {"voxel": self.voxel_params, "graph": self.graph_params, "fusion": self.fusion_params}[prefix]
             target[name] = np.array(arr, dtype=np.float64)
+        self.invalidate()
 
-    def save(self, path) -> None:
+    def save(self, path, optimizer=None) -> None:
         meta = {"model": "fusion", "voxel_cfg": asdict(self.voxel_cfg), "graph_cfg": asdict(self.graph_cfg),
                 "fusion_cfg": _fusion_cfg_dict(self.fusion_cfg), "seed": self.seed,
                 "heads_pretrained": self.heads_pretrained}
-        save_checkpoint(path, self.all_params(), meta)
+        save_checkpoint(path, self.all_params(), optimizer, meta)
 
     @classmethod
     def load(cls, path, precision: str = "fp32") -> "FusionModel":
         """Loads reference checkpoints (checkpoint.py:48-71 format) unchanged."""
-        params, meta = load_checkpoint(path)
+        params, _, meta = load_checkpoint(path)
         m = cls(VoxelHeadConfig(**meta["voxel_cfg"]), GraphHeadConfig(**meta["graph_cfg"]),
                 _fusion_cfg_from_dict(meta["fusion_cfg"]), seed=meta.get("seed", 0),
                 heads_pretrained=meta.get("heads_pretrained", False), precision=precision)
         m.set_params(params)
+        check_param_shapes(m.voxel_cfg, m.graph_cfg, m.fusion_cfg, m.all_params())
         return m
 
 
@@ -444,7 +536,7 @@ def _head_model(vcfg=None, gcfg=None, vparams=None, gparams=None, precision="fp3
 
 
 def _stack_grids(grids, cfg):
-    if isinstance(grids, VoxelGrid):
+    if _is_grid(grids):
         grids = [grids]
     vox = np.stack([np.asarray(v.occupancy, dtype=np.float64) for v in grids])
     want = (cfg.in_channels,) + (cfg.grid_extent,) * 3
@@ -472,7 +564,7 @@ def graph_head_forward(params: dict, cfg: GraphHeadConfig, graphs, training: boo
     """Returns (predictions [B], latents [B, gather_width_noncov]) (models.py:604-614)."""
     if training:
         raise NotImplementedError("training-mode forward is outside the scoring path")
-    if isinstance(graphs, ComplexGraph):
+    if _is_graph(graphs):
         graphs = [graphs]
     feats, off, ce, ne = _pack_graphs(graphs)
     dm = _head_model(gcfg=cfg, gparams=params, precision=precision)

@@ -21,7 +21,7 @@ REF = "/root/reference/pkg/src"
 if REF not in sys.path:
     sys.path.insert(0, REF)
 
-from fusionscreen import complexes, models  # noqa: E402
+from fusionscreen import complexes, harness, models  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 BASELINE_GEN = complexes.GenParams(n_protein=(1000, 1000), n_ligand=(64, 64))
@@ -68,6 +68,106 @@ def edge_cases():
                   "edge-clump"))
     del base
     return out
+
+
+def graph_edge_cases():
+    """Complexes that drive every special path of the GPU radius graphs
+    (graph_csr.cu / featurize.cu): threshold-exact and +-1-ulp distances in
+    several directions, a ligand larger than the 64-atom bitmask path, a
+    larger ligand than pocket (smaller role = protein), coordinates beyond the
+    1024 A fp32 prefilter bound, a compressed pocket with > 96 covalent
+    candidates per row, coincident atoms and single-atom / single-role poses."""
+    rng = np.random.default_rng(11)
+    out = []
+
+    def mk(pos, roles, elems, cid):
+        return complexes.SyntheticComplex(cid, np.asarray(pos, dtype=np.float64),
+                                          np.asarray(elems, dtype=np.int64),
+                                          np.asarray(roles, dtype=np.int64), 0.0)
+    # +-1 ulp around both thresholds along axes and diagonals
+    pos, roles = [], []
+    for k, (t, same) in enumerate(((2.24, True), (5.22, False))):
+        for d_i, direc in enumerate(([1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 0], [1, 1, 1], [3, -4, 12])):
+            u = np.asarray(direc, dtype=np.float64) / np.linalg.norm(direc)
+            for j, dist in enumerate((np.nextafter(t, 0), t, np.nextafter(t, 10))):
+                c = np.array([-6.0 + 3.0 * d_i, -6.0 + 4.0 * j, -6.0 + 6.0 * k])
+                pos += [c, c + dist * u]
+                roles += [0, 0 if same else 1]
+    out.append(mk(pos, roles, rng.integers(0, 4, len(pos)), "edge-ulp"))
+    # ligand > 64 atoms (bitmask non-covalent path off), pocket 300
+    p = rng.uniform(-8, 8, (300, 3))
+    lig = np.clip(rng.normal(0, 2.0, (100, 3)), -8, 8)
+    out.append(mk(np.vstack([p, lig]), [0] * 300 + [1] * 100, rng.integers(0, 4, 400), "edge-biglig"))
+    # more ligand than protein atoms (smaller role = protein)
+    p = rng.uniform(-8, 8, (40, 3))
+    lig = np.clip(rng.normal(0, 2.5, (90, 3)), -8, 8)
+    out.append(mk(np.vstack([p, lig]), [0] * 40 + [1] * 90, rng.integers(0, 4, 130), "edge-swap"))
+    # far from the origin: |coords| >= 1024 A (fp32 prefilter disabled)
+    p = rng.uniform(-8, 8, (200, 3)) + 2048.0
+    lig = rng.normal(2048.0, 1.8, (40, 3))
+    out.append(mk(np.vstack([p, lig]), [0] * 200 + [1] * 40, rng.integers(0, 4, 240), "edge-far"))
+    # compressed pocket: 400 atoms in a 5 A cube (> 96 candidates per covalent row)
+    p = rng.uniform(-2.5, 2.5, (400, 3))
+    lig = rng.uniform(-3.0, 3.0, (30, 3))
+    out.append(mk(np.vstack([p, lig]), [0] * 400 + [1] * 30, rng.integers(0, 4, 430), "edge-dense"))
+    # coincident atoms of both roles, a lone atom, a protein-only complex
+    c = np.zeros((8, 3))
+    out.append(mk(c, [0, 1] * 4, [0, 1, 2, 3] * 2, "edge-coincident"))
+    out.append(mk([[1.0, 2.0, 3.0]], [1], [2], "edge-single"))
+    out.append(mk(rng.uniform(-8, 8, (120, 3)), [0] * 120, rng.integers(0, 4, 120), "edge-protein-only"))
+    return out
+
+
+def write_graph_edge_golden():
+    cs = graph_edge_cases()
+    cov_e, cov_d, ncov_e, ncov_d, feats = [], [], [], [], []
+    cov_off, ncov_off = [0], [0]
+    for c in cs:
+        g = complexes.build_graph(c, 2.24, 5.22, 4, 16.0)
+        feats.append(g.node_features)
+        cov_e.append(g.covalent_edges.astype(np.int32).reshape(-1, 2))
+        cov_d.append(g.covalent_dists)
+        ncov_e.append(g.noncovalent_edges.astype(np.int32).reshape(-1, 2))
+        ncov_d.append(g.noncovalent_dists)
+        cov_off.append(cov_off[-1] + len(g.covalent_edges))
+        ncov_off.append(ncov_off[-1] + len(g.noncovalent_edges))
+    np.savez_compressed(
+        os.path.join(HERE, "graph_edge_golden.npz"), **pack_complex(cs),
+        names=np.array([c.complex_id for c in cs]),
+        node_features=np.concatenate(feats),
+        cov_edges=np.concatenate(cov_e), cov_dists=np.concatenate(cov_d),
+        ncov_edges=np.concatenate(ncov_e), ncov_dists=np.concatenate(ncov_d),
+        cov_off=np.asarray(cov_off, dtype=np.int64), ncov_off=np.asarray(ncov_off, dtype=np.int64))
+
+
+def write_campaign_golden():
+    """run_campaign (harness.py:348-424) with the reference ModelScorer over a
+    small featurized library, with record corruption and job failures, so the
+    B200 scorer + campaign driver can be replayed record for record."""
+    import json
+    import tempfile
+    vcfg, gcfg = models.VoxelHeadConfig(), models.GraphHeadConfig()
+    model = models.FusionModel(vcfg, gcfg, models.table_coherent_fusion_config(), seed=0)
+    cs = [complexes.generate_complex(5000 + s) for s in range(30)]
+    items = models.featurize(cs, vcfg, gcfg)
+    lib = [harness.PoseRecord(f"c{i // 3:03d}", "t0" if i % 2 else "t1", i % 3, (it.grid, it.graph))
+           for i, it in enumerate(items)]
+    plan = harness.FaultPlan(record_corruption_rate=0.15, job_failure_rate=0.3, seed=4)
+    with tempfile.TemporaryDirectory() as d:
+        preds, rep = harness.run_campaign(lib, harness.ModelScorer(model), n_jobs=3, plan=plan, out_dir=d,
+                                          parallelism=2, retries=3, ranks_per_job=2, batch_size=4)
+        shards = {}
+        for name in sorted(os.listdir(d)):
+            if name.endswith(".jsonl") or (name.endswith(".json") and name != harness.MANIFEST_NAME):
+                shards[name] = open(os.path.join(d, name)).read()
+        manifest = json.load(open(os.path.join(d, harness.MANIFEST_NAME)))
+    manifest.pop("timings")
+    rows = [(r.compound_id, r.target_id, r.pose_id, r.job_id, r.rank_id) for r in preds]
+    np.savez_compressed(
+        os.path.join(HERE, "campaign_golden.npz"), **pack_complex(cs),
+        pred_rows=np.array(json.dumps(rows)), pred_scores=np.array([r.predicted_pk for r in preds]),
+        corrupted=np.array(json.dumps(rep.corrupted)), manifest=np.array(json.dumps(manifest, sort_keys=True)),
+        files=np.array(json.dumps(shards, sort_keys=True)))
 
 
 def main():
@@ -144,6 +244,8 @@ def main():
     tpreds, _ = tmodel.predict_batch([(it.grid, it.graph) for it in titems])
     np.savez_compressed(os.path.join(HERE, "toy_golden.npz"), **pack_complex(tcs),
                         scores=np.asarray(tpreds))
+    write_graph_edge_golden()
+    write_campaign_golden()
     print("golden vectors written to", HERE)
 
 

@@ -101,3 +101,34 @@ def test_topk_tie_rule():
     assert idx.tolist() == [11, 12, 14]
     best = orc.best_pose(["a", "a", "b"], ["t", "t", "t"], [3, 1, 0], [1.0, 1.0, 2.0])
     assert best[("a", "t")] == (1, 1.0)
+
+
+def _c_radius(z):
+    from oracle import radius_c
+    return radius_c.radius_pairs_batch(z["positions"], z["roles"], z["atom_off"], 2.24, 5.22)
+
+
+def test_c_radius_oracle_matches_reference_bitwise():
+    """oracle/radius_graph.c (the checker the GPU edge tests use at scale) is
+    pinned against the reference's build_graph on every golden complex,
+    including the +-1-ulp, far-from-origin, dense and single-role cases."""
+    for name in ("featurize_golden.npz", "graph_edge_golden.npz"):
+        z = load(name)
+        ce, cd, coff, ne, nd, noff = _c_radius(z)
+        for p in range(len(z["atom_off"]) - 1):
+            for edges, dists, off, key in ((ce, cd, coff, "cov"), (ne, nd, noff, "ncov")):
+                s, e = z[f"{key}_off"][p], z[f"{key}_off"][p + 1]
+                we, wd = orc.canonical_edges(z[f"{key}_edges"][s:e], z[f"{key}_dists"][s:e])
+                assert np.array_equal(edges[off[p]:off[p + 1]], we), (name, p, key)
+                assert np.array_equal(dists[off[p]:off[p + 1]], wd), (name, p, key)
+
+
+def test_c_radius_oracle_matches_numpy_oracle():
+    from oracle import radius_c
+    from paper_2104_04547_b200 import synth
+    pk = synth.make_pocket(1000, seed=0)
+    lib = synth.make_poses(2, 2, seed=9)
+    for p in range(lib.n_poses):
+        pos, _, ro = synth.complex_arrays(pk, lib, p)
+        for a, b in zip(orc.radius_pairs(pos, ro), radius_c.radius_pairs(pos, ro)):
+            assert np.array_equal(a, b)
