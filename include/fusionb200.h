@@ -55,8 +55,22 @@ extern "C" {
 #define FS_MAX_POSE_ATOMS 4096
 
 /* ---- precision of the scoring path ------------------------------------ */
-#define FS_PREC_FP32 0  /* FFMA fp32 everywhere: reference within 1e-3 rel   */
-#define FS_PREC_BF16 1  /* tcgen05 bf16 Conv3d (fp32 accumulate), fp32 rest  */
+/* The precision argument alone fixes every arithmetic choice of a call (no
+ * environment knobs change numerics).
+ *   FS_PREC_FP32  : FFMA fp32 everywhere (the reference within 1e-3 relative;
+ *                   measured ~1e-7).  Slow: the correctness anchor.
+ *   FS_PREC_BF16  : the throughput path.  tcgen05 Conv3d on bf16 operands and
+ *                   bf16 activations (fp32 TMEM accumulation), tcgen05 kind::tf32
+ *                   dense1, SG-CNN GEMMs on mma.sync with fp16 hi/lo activations
+ *                   x fp16 weights (2 passes, fp32 accumulate; transcendentals
+ *                   via ex2.approx / tanh.approx in the pool), fp32 fusion MLP.
+ *                   Stated tolerance vs the reference: see DESIGN.md section 4.
+ *   FS_PREC_MIXED : the 1e-3 path on tensor cores.  Conv3d as FS_PREC_BF16,
+ *                   dense1 FFMA fp32, SG-CNN GEMMs bf16 hi/lo x hi/lo (3 passes,
+ *                   fp32-class), fp32 fusion MLP. */
+#define FS_PREC_FP32  0
+#define FS_PREC_BF16  1
+#define FS_PREC_MIXED 2
 
 /* ---- grid layouts ------------------------------------------------------ */
 #define FS_GRID_NCDHW_F64  0  /* reference VoxelGrid.occupancy [C,G,G,G] f64 */
@@ -119,6 +133,12 @@ long long fs_launch_count(void);
  * conv4, dense, gnn, fusion, end) recorded on the scoring stream at each
  * stage boundary; NULL disables.  Entries may be NULL. */
 int fs_set_stage_events(void** events, int n);
+/* Branch scheduling of fs_score_poses / fs_score_poses_cached on the calling
+ * thread: 0 serial on the caller's stream, 1 radius graph on a side stream,
+ * 2 voxel branch on a high-priority side stream (the default), -1 = the
+ * FS_OVERLAP environment default.  Results are bitwise identical in every
+ * mode; serial mode makes the per-stage events exact per-kernel times. */
+int fs_set_overlap(int mode);
 
 /* ---- weights (FusionModel.__init__/load -> device) ---------------------- */
 /* Replaces FusionModel parameter binding (models.py:263-278, :441-467).
@@ -185,10 +205,37 @@ int fs_graph_edges(const int64_t* node_off, int32_t n_poses,
                    const int64_t* edge_off, int64_t* edges, double* dists,
                    void* stream);
 
+/* Inspection of the SCORING-PATH radius graph (the edge lists north_star
+ * requires bit-exact): runs the graph exactly as the scoring call does --
+ * fs_score_poses's node offsets + fused single-launch CSR kernel, or with
+ * `factored` != 0 fs_score_poses_cached's pocket-factored kernel (ligand-ligand
+ * covalent + ligand-pocket non-covalent edges; pocket-pocket edges live in the
+ * pocket cache) -- then lists every DIRECTED CSR entry the SG-CNN would read:
+ * ent_*[(p * max_edges + k) * 2 + {0,1}] = (i, j), k < n_*[p], pose-local
+ * node ids in the pose's original numbering (pocket atoms, then its own),
+ * with the float64 distance sqrt((dx*dx+dy*dy)+dz*dz) in d_* (nullable).
+ * Replaces nothing in the reference; it exposes what build_graph
+ * (complexes.py:237-246) computes on the scoring path for parity tests.
+ * Workspace: fs_scoring_graph_ws_bytes(P, max_pose_atoms, max_edges,
+ * factored, c_elem).  err[P] as fs_score_poses (FS_ERR_NOT_FACTORED when a
+ * pose cannot be factored). */
+size_t fs_scoring_graph_ws_bytes(int32_t n_poses, int32_t max_pose_atoms, int64_t max_edges, int32_t factored,
+                                 int32_t c_elem);
+int fs_scoring_graph(const fs_pose_batch* b, double cov_thresh, double noncov_thresh, int64_t max_edges,
+                     int32_t factored, int32_t max_pocket_atoms, int32_t c_elem, double box_size, void* ws,
+                     size_t ws_bytes, int32_t* n_cov, int32_t* n_ncov, int32_t* ent_cov, int32_t* ent_ncov,
+                     double* d_cov, double* d_ncov, int32_t* err, void* stream);
+
 /* ---- scoring (FusionModel.predict_batch, models.py:470-498) ------------ */
-/* Workspace for fs_score_poses / fs_score_features. */
+/* Workspace for fs_score_poses / fs_score_poses_cached: max_nodes =
+ * max_poses * (per-pose node bound: the batch's max_pose_atoms, or the
+ * factored slice rows), max_edges = max_poses * the per-pose edge cap. */
 size_t fs_workspace_bytes(const fs_model* m, int32_t max_poses,
                           int64_t max_nodes, int64_t max_edges, int precision);
+/* Workspace for fs_score_features: the batch's total nodes and the larger of
+ * its two i<j edge counts. */
+size_t fs_features_workspace_bytes(const fs_model* m, int32_t n_poses, int64_t n_nodes, int64_t n_edges,
+                                   int precision);
 
 /* Fused featurize + 3D-CNN + SG-CNN + fusion for raw poses (the screening
  * path: models.featurize (:638-651) then predict_batch).  Outputs (nullable
@@ -228,19 +275,22 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses,
  * computes these once per pocket into a cache; fs_score_poses_cached then
  * scores a pose from its ligand atoms, recomputing only ligand nodes and the
  * protein nodes the ligand touches.  Same scores as fs_score_poses to fp32
- * rounding (bf16 precision only).  This is an effective-throughput mode: the
+ * rounding (FS_PREC_BF16 / FS_PREC_MIXED).  This is an effective-throughput mode: the
  * reported algorithmic work per pose is unchanged. */
 size_t fs_pocket_cache_bytes(const fs_model* m, int32_t max_pocket_atoms);
 size_t fs_pocket_prepare_ws_bytes(const fs_model* m, int32_t n_pockets, int32_t max_pocket_atoms);
-/* Pockets as in fs_pose_batch (pocket_xyz/elem/role, pocket_off[n+1]); cache =
+/* precision: FS_PREC_BF16 or FS_PREC_MIXED; a cache is used only with the
+ * precision it was prepared with (the cached pocket node states come from
+ * that precision's SG-CNN).
+ * Pockets as in fs_pose_batch (pocket_xyz/elem/role, pocket_off[n+1]); cache =
  * n_pockets * fs_pocket_cache_bytes(max_pocket_atoms) bytes; err[n_pockets]
  * gets the FS_ERR_* bits of each pocket (a pocket with err != 0 must not be
  * used with the cache). */
-int fs_pocket_prepare(const fs_model* m, const double* pocket_xyz, const int32_t* pocket_elem,
+int fs_pocket_prepare(const fs_model* m, int precision, const double* pocket_xyz, const int32_t* pocket_elem,
                       const int32_t* pocket_role, const int64_t* pocket_off, int32_t n_pockets,
                       int32_t max_pocket_atoms, void* cache, int32_t* err, void* ws,
                       size_t ws_bytes, void* stream);
-/* Like fs_score_poses (bf16 only) for a batch whose pockets are the ones the
+/* Like fs_score_poses (FS_PREC_BF16 / FS_PREC_MIXED) for a batch whose pockets are the ones the
  * cache was prepared from.  Poses that cannot be factored get
  * FS_ERR_NOT_FACTORED (and a NaN score); rescore them with fs_score_poses.
  * Workspace: fs_workspace_bytes(m, P, P * (max_pose_atoms + 32), P * max_edges, bf16). */
@@ -262,7 +312,8 @@ int fs_debug_conv(const fs_model* m, int layer, int32_t n_poses, const void* in,
 /* ---- ranking (top-k merge; tie rule of evaluate.py:67-83) -------------- */
 /* Sorts the concatenation of (a) and (b) by (score desc, index asc) and keeps
  * the first k into (out_scores, out_idx).  NaN scores rank last.  Indices
- * must be < 2^32.  Either input may be empty. */
+ * are full int64 (screens past 2^32 poses keep the lowest-index tie rule).
+ * Either input may be empty. */
 size_t fs_topk_ws_bytes(int64_t n);
 int fs_topk_merge(const float* a_scores, const int64_t* a_idx, int64_t na,
                   const float* b_scores, const int64_t* b_idx, int64_t nb,

@@ -18,23 +18,24 @@ FS_OK, FS_EINVAL, FS_ECAPACITY, FS_ECUDA, FS_ENOTSUP = 0, -1, -2, -3, -4
 FS_ERR_ROLE, FS_ERR_NAN, FS_ERR_NONFINITE, FS_ERR_EDGE_CAP, FS_ERR_TOO_LARGE = 1, 2, 4, 8, 16
 FS_ERR_GRID_NONFINITE, FS_ERR_FEAT_NONFINITE, FS_ERR_NOT_FACTORED = 32, 64, 128
 FS_MAX_POSE_ATOMS = 4096
-FS_PREC_FP32, FS_PREC_BF16 = 0, 1
+FS_PREC_FP32, FS_PREC_BF16, FS_PREC_MIXED = 0, 1, 2
 FS_GRID_NCDHW_F64, FS_GRID_NDHWC_F32, FS_GRID_NDHWC_BF16 = 0, 1, 2
 FS_MODE_LATE, FS_MODE_MID, FS_MODE_COHERENT = 0, 1, 2
 
 STAGES = ("featurize", "conv1", "conv2", "conv3", "conv4", "dense", "gnn", "fusion", "end")
-PRECISIONS = {"fp32": FS_PREC_FP32, "bf16": FS_PREC_BF16}
+PRECISIONS = {"fp32": FS_PREC_FP32, "bf16": FS_PREC_BF16, "mixed": FS_PREC_MIXED}
 
 # every symbol include/fusionb200.h declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "fs_strerror", "fs_version", "fs_last_cuda_error", "fs_launch_count", "fs_set_stage_events",
+    "fs_strerror", "fs_version", "fs_last_cuda_error", "fs_launch_count", "fs_set_stage_events", "fs_set_overlap",
     "fs_weights_bytes", "fs_model_create",
     "fs_model_destroy", "fs_model_supports", "fs_node_offsets", "fs_node_offsets_ws_bytes",
     "fs_voxelize", "fs_node_features", "fs_graph_count", "fs_graph_rows", "fs_graph_rows_ws_bytes",
-    "fs_graph_fill", "fs_graph_edge_counts", "fs_graph_edges", "fs_workspace_bytes",
+    "fs_graph_fill", "fs_graph_edge_counts", "fs_graph_edges", "fs_workspace_bytes", "fs_features_workspace_bytes",
     "fs_score_poses", "fs_score_features", "fs_debug_conv", "fs_topk_ws_bytes", "fs_topk_merge",
     "fs_best_pose", "fs_best_pose_update", "fs_best_pose_decode",
     "fs_pocket_cache_bytes", "fs_pocket_prepare_ws_bytes", "fs_pocket_prepare", "fs_score_poses_cached",
+    "fs_scoring_graph_ws_bytes", "fs_scoring_graph",
 )
 
 
@@ -86,6 +87,7 @@ def _sig(lib):
         "fs_last_cuda_error": (C.c_char_p, []),
         "fs_launch_count": (C.c_longlong, []),
         "fs_set_stage_events": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
+        "fs_set_overlap": (C.c_int, [C.c_int]),
         "fs_weights_bytes": (_SZ, [md]),
         "fs_model_create": (C.c_int, [md, C.POINTER(C.c_char_p), C.POINTER(C.c_void_p), C.c_int,
                                       _P, _SZ, _P, C.POINTER(C.c_void_p)]),
@@ -102,10 +104,14 @@ def _sig(lib):
         "fs_graph_edge_counts": (C.c_int, [_P, _I32, _P, _P, _P, _P, _SZ, _P]),
         "fs_graph_edges": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P, _P]),
         "fs_workspace_bytes": (_SZ, [_P, _I32, _I64, _I64, C.c_int]),
+        "fs_features_workspace_bytes": (_SZ, [_P, _I32, _I64, _I64, C.c_int]),
+        "fs_scoring_graph_ws_bytes": (_SZ, [_I32, _I32, _I64, _I32, _I32]),
+        "fs_scoring_graph": (C.c_int, [sp, _D, _D, _I64, _I32, _I32, _I32, _D, _P, _SZ, _P, _P, _P, _P, _P, _P,
+                                       _P, _P]),
         "fs_score_poses": (C.c_int, [_P, C.c_int, sp, _I64, _P, _SZ, _P, _P, _P, _P, _P, _P, _P]),
         "fs_pocket_cache_bytes": (_SZ, [_P, _I32]),
         "fs_pocket_prepare_ws_bytes": (_SZ, [_P, _I32, _I32]),
-        "fs_pocket_prepare": (C.c_int, [_P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
+        "fs_pocket_prepare": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
         "fs_score_poses_cached": (C.c_int, [_P, C.c_int, sp, _P, _I32, _I64, _P, _SZ, _P, _P, _P, _P, _P, _P,
                                             _P]),
         "fs_score_features": (C.c_int, [_P, C.c_int, _I32, _P, _P, _P, _I64, _P, _I64, _P, _I64,

@@ -47,7 +47,8 @@ void mark_stage(int stage, cudaStream_t st) {
 }
 
 // ---- launchers defined in the other translation units ----------------------
-int launch_node_offsets(const fs_pose_batch& b, int64_t* node_off, void* ws, size_t ws_bytes, cudaStream_t st);
+int launch_node_offsets(const fs_pose_batch& b, int64_t* node_off, void* ws, size_t ws_bytes, cudaStream_t st,
+                        int64_t clamp = 0);
 int launch_voxelize(const fs_pose_batch& b, int g, int c_elem, double box, int layout, void* out, int32_t* err, cudaStream_t st);
 int launch_node_features(const fs_pose_batch& b, const int64_t* node_off, int c_elem, double box, void* out, bool f64, cudaStream_t st);
 int launch_graph_count(const fs_pose_batch& b, const int64_t* node_off, double tc, double tn, int32_t* deg_cov, int32_t* deg_ncov, int32_t* err, cudaStream_t st);
@@ -63,6 +64,11 @@ int launch_graph_fact(const fs_pose_batch& b, double tc, double tn, double box, 
                       int max_pocket, int32_t* cnt, int32_t* aff, float* feats, int64_t* row_cov, int32_t* deg_cov,
                       col_t* col_cov, int64_t* row_ncov, int32_t* deg_ncov, col_t* col_ncov, int32_t* err,
                       cudaStream_t st);
+int launch_csr_entries(const fs_pose_batch& b, const int64_t* node_off, const int32_t* fact_cnt, const int32_t* aff,
+                       int64_t S, int64_t cap, int max_rows, const int64_t* row_cov, const int32_t* deg_cov,
+                       const col_t* col_cov, const int64_t* row_ncov, const int32_t* deg_ncov, const col_t* col_ncov,
+                       int64_t cap_out, int32_t* n_cov, int32_t* n_ncov, int32_t* ent_cov, int32_t* ent_ncov,
+                       double* d_cov, double* d_ncov, const int32_t* err, cudaStream_t st);
 bool conv1_fact_supported(int g, int k, int cin, int cout);
 int launch_conv1_fact(const fs_pose_batch& b, const char* cache, int64_t cache_stride, int64_t off_pp,
                       int64_t off_ppact, int64_t off_wl, int c_elem, double box, __nv_bfloat16* out, cudaStream_t st);
@@ -504,16 +510,18 @@ struct WsPlan {
   size_t take(size_t bytes) { size_t o = total; total = align_up(total + bytes, 256); return o; }
 };
 
-static WsPlan plan_ws(const fs_model& m, int64_t P, int64_t N, int64_t E, int prec) {
+// pose_nodes: upper bound on one pose's nodes (sizes the FFMA SG-CNN's global
+// state fallback, needed only for poses too large for its shared memory)
+static WsPlan plan_ws(const fs_model& m, int64_t P, int64_t N, int64_t E, int prec, int64_t pose_nodes) {
   WsPlan w;
   const int64_t G3 = (int64_t)m.G * m.G * m.G, H3 = G3 / 8, Q3 = G3 / 64;
   w.node_off = w.take(8 * (P + 1));
   w.deg_cov = w.take(4 * N); w.deg_ncov = w.take(4 * N);
   w.row_cov = w.take(8 * (N + 1)); w.row_ncov = w.take(8 * (N + 1));
-  w.col_cov = w.take(4 * E); w.col_ncov = w.take(4 * E);
+  w.col_cov = w.take(sizeof(col_t) * E); w.col_ncov = w.take(sizeof(col_t) * E);
   w.node_pose = w.take(4 * N); w.cursor = w.take(8 * (N + 1));
   w.feats = w.take(4 * N * m.F);
-  if (prec == FS_PREC_BF16) {
+  if (prec != FS_PREC_FP32) {   // tcgen05 conv chain (bf16 / mixed)
     w.grid = w.take(2 * P * G3 * m.cin);
     w.umma = w.take(umma::workspace_bytes(m.d, P));
     w.a1 = w.a2 = w.p1 = w.a3 = w.a4 = 0;
@@ -531,9 +539,10 @@ static WsPlan plan_ws(const fs_model& m, int64_t P, int64_t N, int64_t E, int pr
   w.hb0 = w.take(4 * P * m.fd); w.hb1 = w.take(4 * P * m.fd);
   w.g1 = w.take(4 * P * m.w1); w.g2 = w.take(4 * P * m.w2);
   w.pv = w.take(4 * P); w.pg = w.take(4 * P);
-  int max_nodes = (int)(P > 0 ? (N + P - 1) / P : 0);
-  (void)max_nodes;
-  w.state = w.take((size_t)2 * 4 * N * m.dpad);   // GNN fallback state (unused when smem fits)
+  // FFMA SG-CNN's global node-state fallback: only for poses too large for
+  // its shared-memory state
+  const int pn = (int)(pose_nodes < FS_MAX_POSE_ATOMS ? pose_nodes : FS_MAX_POSE_ATOMS);
+  w.state = w.take(gnn_needs_global_state(m.dpad, pn) ? (size_t)2 * 4 * N * m.dpad : 0);
   w.scan = w.take(scan_ws_bytes(N > P ? N : P) + 1024);
   w.fact_cnt = w.take(8 * P);
   w.fact_aff = w.take(4 * N);
@@ -554,19 +563,24 @@ struct SideStream {
   int mode = 1;
 };
 
+// per host thread; -1 = the FS_OVERLAP environment default (scheduling only:
+// results are bitwise identical in every mode)
+static thread_local int g_overlap_mode = -1;
+
 static SideStream* side_stream() {
   // default 2: the tensor-bound conv chain leaves issue slots and shared
   // memory for one radius-graph CTA per SM (measured 43.7 -> 42.8 ms/step)
-  static const int mode = getenv("FS_OVERLAP") ? atoi(getenv("FS_OVERLAP")) : 2;
+  static const int env_mode = getenv("FS_OVERLAP") ? atoi(getenv("FS_OVERLAP")) : 2;
+  const int mode = g_overlap_mode >= 0 ? g_overlap_mode : env_mode;
   if (mode != 1 && mode != 2) return nullptr;
   static thread_local std::map<int, SideStream> streams;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   SideStream& ss = streams[dev];
+  ss.mode = mode;
   if (!ss.s) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    ss.mode = mode;
     if (cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, mode == 2 ? hi : lo) != cudaSuccess ||
         cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
@@ -647,8 +661,7 @@ static int voxel_tail(const fs_model& m, int P, char* ws, const WsPlan& w, bool 
   DenseArgs a{};
   a.x = (float*)(ws + w.p2); a.ldx = m.flat; a.w = m.P(m.d1w); a.b = m.P(m.d1b);
   a.y = (float*)(ws + w.d1); a.ldy = m.dn; a.m = P; a.k = m.flat; a.n = m.dn; a.act = FS_ACT_RELU;
-  static const bool force_ffma = getenv("FS_DENSE_FFMA") != nullptr;
-  int rc = tc && !force_ffma && umma::dense_tf32_ok(m.flat, m.dn)
+  int rc = tc && umma::dense_tf32_ok(m.flat, m.dn)
                ? umma::dense_tf32(a.x, P, m.flat, m.P(m.d1t), m.dn, a.b, a.y, st)
                : launch_dense(a, st);
   if (rc) return rc;
@@ -680,8 +693,7 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
   g.state = (float*)(ws + w.state); g.lat = (float*)(ws + w.lat); g.ld_lat = m.LW; g.err = err;
   mark_stage(ST_GNN, st);
   int rc;
-  static const bool force_ffma = getenv("FS_GNN_FFMA") != nullptr;
-  if (extra || (precision == FS_PREC_BF16 && m.gmma_ok && !force_ffma && gnn_mma_fits(max_nodes))) {
+  if (extra || (precision != FS_PREC_FP32 && m.gmma_ok && gnn_mma_fits(max_nodes))) {
     GnnMmaArgs q{};
     if (extra) q = *extra;   // factored-mode / dump fields
     q.feats = g.feats; q.F = g.F; q.node_off = g.node_off;
@@ -698,12 +710,10 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
     q.k_steps[0] = m.d.k_cov; q.k_steps[1] = m.d.k_noncov;
     q.lat = g.lat; q.ld_lat = g.ld_lat; q.err = err;
     q.ids_padded = ids_padded ? 1 : 0;
-    // FS_GNN_SPLIT (read per call): 2 = fp16 activations hi/lo x fp16
-    // weights, two passes (default); 3 = bf16 hi/lo x hi/lo, three passes
-    // (fp32-class); 1 = one bf16 pass
-    const char* sp_env = getenv("FS_GNN_SPLIT");
-    const int split = sp_env && (atoi(sp_env) == 1 || atoi(sp_env) == 3) ? atoi(sp_env) : 2;
-    rc = launch_gnn_mma(q, split, P, max_nodes, st);
+    // GEMM operand split, fixed by the precision argument: FS_PREC_BF16 =
+    // fp16 activations hi/lo x fp16 weights, two passes; FS_PREC_MIXED = bf16
+    // hi/lo x hi/lo, three passes (fp32-class)
+    rc = launch_gnn_mma(q, precision == FS_PREC_MIXED ? 3 : 2, P, max_nodes, st);
   } else {
     rc = launch_gnn(g, m.dpad, P, max_nodes, st);
   }
@@ -803,6 +813,12 @@ int fs_set_stage_events(void** events, int n) {
 
 const char* fs_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
 
+int fs_set_overlap(int mode) {
+  if (mode < -1 || mode > 2) return FS_EINVAL;
+  g_overlap_mode = mode;
+  return FS_OK;
+}
+
 size_t fs_weights_bytes(const fs_model_desc* desc) {
   if (!desc || validate_desc(*desc)) return 0;
   fs_model m;
@@ -837,7 +853,7 @@ int fs_model_destroy(fs_model* m) { delete m; return FS_OK; }
 int fs_model_supports(const fs_model* m, int precision) {
   if (!m) return 0;
   if (precision == FS_PREC_FP32) return 1;
-  if (precision == FS_PREC_BF16) return m->umma_ok ? 1 : 0;
+  if (precision == FS_PREC_BF16 || precision == FS_PREC_MIXED) return m->umma_ok ? 1 : 0;
   return 0;
 }
 
@@ -896,7 +912,14 @@ int fs_graph_edges(const int64_t* node_off, int32_t n_poses, const int64_t* row_
 
 size_t fs_workspace_bytes(const fs_model* m, int32_t max_poses, int64_t max_nodes, int64_t max_edges, int precision) {
   if (!m || max_poses < 0 || max_nodes < 0 || max_edges < 0) return 0;
-  return plan_ws(*m, max_poses, max_nodes, max_edges, precision).total + 256;
+  const int64_t pose_nodes = max_poses > 0 ? (max_nodes + max_poses - 1) / max_poses : 0;
+  return plan_ws(*m, max_poses, max_nodes, max_edges, precision, pose_nodes).total + 256;
+}
+
+size_t fs_features_workspace_bytes(const fs_model* m, int32_t n_poses, int64_t n_nodes, int64_t n_edges,
+                                   int precision) {
+  if (!m || n_poses < 0 || n_nodes < 0 || n_edges < 0) return 0;
+  return plan_ws(*m, n_poses, n_nodes, 2 * n_edges, precision, n_nodes).total + 256;
 }
 
 int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int64_t max_edges, void* ws,
@@ -910,7 +933,7 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   const int max_atoms = b->max_pose_atoms > 0 ? b->max_pose_atoms : FS_MAX_POSE_ATOMS;
   const int64_t N = (int64_t)P * max_atoms;
   if (max_edges <= 0) return FS_EINVAL;
-  WsPlan w = plan_ws(*m, P, N, (int64_t)P * max_edges, precision);
+  WsPlan w = plan_ws(*m, P, N, (int64_t)P * max_edges, precision, max_atoms);
   if (w.total > ws_bytes) return FS_ECAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
   char* W = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
@@ -919,7 +942,10 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   int rc;
   mark_stage(ST_FEATURIZE, st);
   FS_CUDA_CHECK(cudaMemsetAsync(err, 0, 4 * (size_t)P, st));
-  if ((rc = launch_node_offsets(*b, node_off, W + w.scan, scan_ws_bytes(N > P ? N : P) + 1024, st))) return rc;
+  // oversize poses are clamped to max_atoms rows (and flagged by the graph
+  // kernel), so node_off[P] <= N = P * max_atoms always holds
+  if ((rc = launch_node_offsets(*b, node_off, W + w.scan, scan_ws_bytes(N > P ? N : P) + 1024, st, max_atoms)))
+    return rc;
   const fs_model_desc& d = m->d;
   const bool late = d.fusion_mode == FS_MODE_LATE;
   // featurize (models.py:638-651): radius graph + node features in one fused
@@ -933,7 +959,7 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   };
   auto voxel_branch = [&](cudaStream_t vs) {
     int r;
-    if (precision == FS_PREC_BF16) {
+    if (precision != FS_PREC_FP32) {
       if ((r = launch_voxelize(*b, d.grid_extent, m->cgrid, d.box_size, FS_GRID_NDHWC_BF16, W + w.grid, err, vs)))
         return r;
       if ((r = umma::voxel_convs(d, (const char*)m->blob + m->umma_off, m->P(m->c1b), m->P(m->c2b), m->P(m->c3b),
@@ -945,6 +971,7 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
         return r;
       if ((r = voxel_head_fp32(*m, P, W, w, vs))) return r;
     }
+    // dense1: tcgen05 tf32 on the bf16 path, FFMA fp32 on the mixed (1e-3) path
     return voxel_tail(*m, P, W, w, late || pred_v, vs, precision == FS_PREC_BF16);
   };
   // FS_OVERLAP=0: serial; 1: graph branch on a side stream; 2 (default):
@@ -976,6 +1003,12 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
 }
 
 // ---- pocket-invariant factoring ----------------------------
+// node rows of one pose's compact factored slice: nc = nLp + nA <= max_atoms + 15
+static int64_t fact_slice_rows(int max_atoms) {
+  const int64_t S = (int64_t)((max_atoms + 15 + 15) & ~15);
+  return S > gnn_mma_max_nodes() ? gnn_mma_max_nodes() : S;
+}
+
 // covalent CSR capacity of a pocket-only pose (directed entries)
 static int64_t pocket_edge_cap(int max_pocket) { return (int64_t)64 * max_pocket + 1024; }
 
@@ -994,16 +1027,18 @@ static size_t prep_extra_bytes(const fs_model& m, int n, int mp) {
 size_t fs_pocket_prepare_ws_bytes(const fs_model* m, int32_t n_pockets, int32_t max_pocket_atoms) {
   if (!m || n_pockets < 0 || !factoring_ok(*m, max_pocket_atoms)) return 0;
   const int64_t N = (int64_t)n_pockets * max_pocket_atoms;
-  return plan_ws(*m, n_pockets, N, n_pockets * pocket_edge_cap(max_pocket_atoms), FS_PREC_FP32).total +
+  return plan_ws(*m, n_pockets, N, n_pockets * pocket_edge_cap(max_pocket_atoms), FS_PREC_FP32,
+                 max_pocket_atoms).total +
          prep_extra_bytes(*m, n_pockets, max_pocket_atoms) + 512;
 }
 
-int fs_pocket_prepare(const fs_model* m, const double* pocket_xyz, const int32_t* pocket_elem,
+int fs_pocket_prepare(const fs_model* m, int precision, const double* pocket_xyz, const int32_t* pocket_elem,
                       const int32_t* pocket_role, const int64_t* pocket_off, int32_t n_pockets,
                       int32_t max_pocket_atoms, void* cache, int32_t* err, void* ws, size_t ws_bytes,
                       void* stream) {
   if (!m || !pocket_xyz || !pocket_elem || !pocket_role || !pocket_off || !cache || !err || !ws) return FS_EINVAL;
-  if (!factoring_ok(*m, max_pocket_atoms)) return FS_ENOTSUP;
+  if ((precision != FS_PREC_BF16 && precision != FS_PREC_MIXED) || !factoring_ok(*m, max_pocket_atoms))
+    return FS_ENOTSUP;
   const int n = n_pockets, mp = max_pocket_atoms;
   if (n <= 0) return FS_OK;
   if (ws_bytes < fs_pocket_prepare_ws_bytes(m, n, mp)) return FS_ECAPACITY;
@@ -1012,7 +1047,7 @@ int fs_pocket_prepare(const fs_model* m, const double* pocket_xyz, const int32_t
   const PocketCacheLayout L = cache_layout(*m, mp);
   const int64_t cap = pocket_edge_cap(mp);
   // fp32 plan: the pocket grid is voxelized as fp32 for the FFMA conv1
-  WsPlan w = plan_ws(*m, n, (int64_t)n * mp, n * cap, FS_PREC_FP32);
+  WsPlan w = plan_ws(*m, n, (int64_t)n * mp, n * cap, FS_PREC_FP32, mp);
   char* W = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   char* X = W + w.total;   // prep-only buffers
   int64_t* atom_off = (int64_t*)X; X += align_up(8 * (size_t)(n + 1), 256);
@@ -1041,7 +1076,7 @@ int fs_pocket_prepare(const fs_model* m, const double* pocket_xyz, const int32_t
   // states and the per-node pool terms
   GnnMmaArgs x{};
   x.dump_hcov = dump_h; x.dump_f = dump_f; x.dump_ld = mp;
-  if ((rc = graph_head(*m, n, mp, W, w, err, false, FS_PREC_BF16, st, &x))) return rc;
+  if ((rc = graph_head(*m, n, mp, W, w, err, false, precision, st, &x))) return rc;
   char* C = (char*)cache;
   FS_CUDA_CHECK(cudaMemcpy2DAsync(C + L.off_hcov, L.bytes, dump_h, (size_t)4 * mp * 24, (size_t)4 * mp * 24, n,
                                   cudaMemcpyDeviceToDevice, st));
@@ -1065,16 +1100,16 @@ int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch*
                           int32_t max_pocket_atoms, int64_t max_edges, void* ws, size_t ws_bytes, float* scores,
                           float* lat_v, float* lat_g, float* pred_v, float* pred_g, int32_t* err, void* stream) {
   if (!m || !b || !cache || !ws || !scores || !err || max_edges <= 0) return FS_EINVAL;
-  if (precision != FS_PREC_BF16 || !factoring_ok(*m, max_pocket_atoms)) return FS_ENOTSUP;
+  if ((precision != FS_PREC_BF16 && precision != FS_PREC_MIXED) || !factoring_ok(*m, max_pocket_atoms))
+    return FS_ENOTSUP;
   const int P = b->n_poses;
   if (P <= 0) return FS_OK;
   const int max_atoms = b->max_pose_atoms > 0 ? b->max_pose_atoms : FS_MAX_POSE_ATOMS;
   // compact node slice per pose; poses whose touched set does not fit the
   // tensor-core SG-CNN's shared memory are flagged FS_ERR_NOT_FACTORED
-  int64_t S = (int64_t)((max_atoms + 15 + 15) & ~15);   // nc = nLp + nA <= max_atoms + 15
-  if (S > gnn_mma_max_nodes()) S = gnn_mma_max_nodes();
+  const int64_t S = fact_slice_rows(max_atoms);
   const int64_t N = (int64_t)P * S;
-  WsPlan w = plan_ws(*m, P, N, (int64_t)P * max_edges, FS_PREC_BF16);
+  WsPlan w = plan_ws(*m, P, N, (int64_t)P * max_edges, precision, S);
   char* W = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   if ((size_t)(W - (char*)ws) + w.total > ws_bytes) return FS_ECAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1106,13 +1141,13 @@ int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch*
   if ((rc = umma::voxel_convs_from2(d, (const char*)m->blob + m->umma_off, m->P(m->c2b), m->P(m->c3b), m->P(m->c4b),
                                     P, W + w.umma, (float*)(W + w.p2), st)))
     return rc;
-  if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st, true))) return rc;
+  if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st, precision == FS_PREC_BF16))) return rc;
   if (ss) FS_CUDA_CHECK(cudaStreamWaitEvent(st, ss->join, 0));
   GnnMmaArgs x{};
   x.fact_cnt = cnt; x.fact_stride = S; x.fact_aff = aff; x.pose_target = b->pose_target;
   x.cache = (const char*)cache; x.cache_stride = L.bytes;
   x.off_hcov = L.off_hcov; x.off_f = L.off_f; x.off_T = L.off_T; x.off_n = L.off_n;
-  if ((rc = graph_head(*m, P, (int)S, W, w, err, late || pred_g, FS_PREC_BF16, st, &x))) return rc;
+  if ((rc = graph_head(*m, P, (int)S, W, w, err, late || pred_g, precision, st, &x))) return rc;
   if (!late && (rc = fusion_head(*m, P, W, w, scores, st))) return rc;
   if ((rc = launch_finalize(P, d.fusion_mode, (float*)(W + w.pv), (float*)(W + w.pg), scores, err, st))) return rc;
   rc = copy_outputs(*m, P, W, w, lat_v, lat_g, pred_v, pred_g, st);
@@ -1137,14 +1172,14 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const d
   if (need_g && (!feats || !node_off)) return FS_EINVAL;
   if (want_f && !scores) return FS_EINVAL;
   const int64_t E = 2 * (n_cov > n_ncov ? n_cov : n_ncov);
-  WsPlan w = plan_ws(*m, P, n_nodes, E, precision);
+  WsPlan w = plan_ws(*m, P, n_nodes, E, precision, n_nodes);
   char* W = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   if ((size_t)(W - (char*)ws) + w.total > ws_bytes) return FS_ECAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
   FS_CUDA_CHECK(cudaMemsetAsync(err, 0, 4 * (size_t)P, st));
   if (need_v) {
-    if (precision == FS_PREC_BF16) {
+    if (precision != FS_PREC_FP32) {
       if ((rc = launch_grid_convert(grids, W + w.grid, P, m->cin, m->G, true, err, st))) return rc;
       if ((rc = umma::voxel_convs(d, (const char*)m->blob + m->umma_off, m->P(m->c1b), m->P(m->c2b),
                                   m->P(m->c3b), m->P(m->c4b), P, (const __nv_bfloat16*)(W + w.grid),
@@ -1192,6 +1227,77 @@ int fs_debug_conv(const fs_model* m, int layer, int32_t n_poses, const void* in,
   if (layer < 1 || layer > 4) return FS_EINVAL;
   return umma::debug_layer(m->d, (const char*)m->blob + m->umma_off, bias[layer], nullptr, layer, n_poses, in,
                            residual, out, (cudaStream_t)stream);
+}
+
+// ---- inspection of the scoring-path radius graph ---------------------------
+struct GraphHookPlan {
+  size_t total = 0, node_off, scan, row_c, row_n, deg_c, deg_n, col_c, col_n, feats, cnt, aff;
+  int64_t N, S;
+  size_t take(size_t bytes) { size_t o = total; total = align_up(total + bytes, 256); return o; }
+};
+
+static GraphHookPlan graph_hook_plan(int64_t P, int max_atoms, int64_t max_edges, int factored, int c_elem) {
+  GraphHookPlan g;
+  g.S = factored ? fact_slice_rows(max_atoms) : max_atoms;
+  g.N = P * g.S;
+  g.node_off = g.take(8 * (P + 1));
+  g.scan = g.take(scan_ws_bytes(g.N > P ? g.N : P) + 1024);
+  g.row_c = g.take(8 * (g.N + 1)); g.row_n = g.take(8 * (g.N + 1));
+  g.deg_c = g.take(4 * g.N); g.deg_n = g.take(4 * g.N);
+  g.col_c = g.take(sizeof(col_t) * P * max_edges); g.col_n = g.take(sizeof(col_t) * P * max_edges);
+  g.feats = g.take(4 * g.N * (c_elem + 4));
+  g.cnt = g.take(8 * P); g.aff = g.take(4 * g.N);
+  return g;
+}
+
+size_t fs_scoring_graph_ws_bytes(int32_t n_poses, int32_t max_pose_atoms, int64_t max_edges, int32_t factored,
+                                 int32_t c_elem) {
+  if (n_poses < 0 || max_edges <= 0 || c_elem < 1) return 0;
+  const int max_atoms = max_pose_atoms > 0 ? max_pose_atoms : FS_MAX_POSE_ATOMS;
+  return graph_hook_plan(n_poses, max_atoms, max_edges, factored, c_elem).total + 256;
+}
+
+int fs_scoring_graph(const fs_pose_batch* b, double cov_thresh, double noncov_thresh, int64_t max_edges,
+                     int32_t factored, int32_t max_pocket_atoms, int32_t c_elem, double box_size, void* ws,
+                     size_t ws_bytes, int32_t* n_cov, int32_t* n_ncov, int32_t* ent_cov, int32_t* ent_ncov,
+                     double* d_cov, double* d_ncov, int32_t* err, void* stream) {
+  if (!b || !ws || !n_cov || !n_ncov || !ent_cov || !ent_ncov || !err || max_edges <= 0 || c_elem < 1)
+    return FS_EINVAL;
+  const int P = b->n_poses;
+  if (P <= 0) return FS_OK;
+  const int max_atoms = b->max_pose_atoms > 0 ? b->max_pose_atoms : FS_MAX_POSE_ATOMS;
+  const GraphHookPlan g = graph_hook_plan(P, max_atoms, max_edges, factored, c_elem);
+  char* W = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  if ((size_t)(W - (char*)ws) + g.total > ws_bytes) return FS_ECAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  FS_CUDA_CHECK(cudaMemsetAsync(err, 0, 4 * (size_t)P, st));
+  int64_t* node_off = (int64_t*)(W + g.node_off);
+  int32_t* cnt = nullptr; int32_t* aff = nullptr;
+  if (factored) {
+    // exactly fs_score_poses_cached's graph launch
+    if (max_pocket_atoms <= 0 || max_pocket_atoms > FS_MAX_POSE_ATOMS) return FS_EINVAL;
+    cnt = (int32_t*)(W + g.cnt); aff = (int32_t*)(W + g.aff);
+    if ((rc = launch_graph_fact(*b, cov_thresh, noncov_thresh, box_size, c_elem, g.S, max_edges, max_pocket_atoms,
+                                cnt, aff, (float*)(W + g.feats), (int64_t*)(W + g.row_c), (int32_t*)(W + g.deg_c),
+                                (col_t*)(W + g.col_c), (int64_t*)(W + g.row_n), (int32_t*)(W + g.deg_n),
+                                (col_t*)(W + g.col_n), err, st)))
+      return rc;
+  } else {
+    // exactly fs_score_poses's node offsets + graph launch
+    if ((rc = launch_node_offsets(*b, node_off, W + g.scan, scan_ws_bytes(g.N > P ? g.N : P) + 1024, st,
+                                  max_atoms)))
+      return rc;
+    if ((rc = launch_graph_csr(*b, node_off, cov_thresh, noncov_thresh, (int64_t*)(W + g.row_c),
+                               (int32_t*)(W + g.deg_c), (col_t*)(W + g.col_c), nullptr, (int64_t*)(W + g.row_n),
+                               (int32_t*)(W + g.deg_n), (col_t*)(W + g.col_n), nullptr, max_edges, err, st,
+                               (float*)(W + g.feats), c_elem, box_size)))
+      return rc;
+  }
+  return launch_csr_entries(*b, node_off, cnt, aff, g.S, max_edges, (int)g.S, (int64_t*)(W + g.row_c),
+                            (int32_t*)(W + g.deg_c), (col_t*)(W + g.col_c), (int64_t*)(W + g.row_n),
+                            (int32_t*)(W + g.deg_n), (col_t*)(W + g.col_n), max_edges, n_cov, n_ncov, ent_cov,
+                            ent_ncov, d_cov, d_ncov, err, st);
 }
 
 size_t fs_topk_ws_bytes(int64_t n) { return topk_ws_bytes(n); }

@@ -11,13 +11,16 @@ namespace fs {
 // ---------------------------------------------------------------------------
 // node offsets
 // ---------------------------------------------------------------------------
-__global__ void pose_node_counts_kernel(fs_pose_batch b, int64_t* counts) {
+// clamp > 0: a pose above `clamp` nodes (flagged FS_ERR_TOO_LARGE by the graph
+// kernels) occupies only `clamp` node rows, so one oversize pose can neither
+// push the others past a workspace sized P * clamp nor be written past it
+__global__ void pose_node_counts_kernel(fs_pose_batch b, int64_t* counts, int64_t clamp) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= b.n_poses) return;
   int t = b.pose_target ? b.pose_target[p] : -1;
   int64_t n = b.atom_off[p + 1] - b.atom_off[p];
   if (t >= 0) n += b.pocket_off[t + 1] - b.pocket_off[t];
-  counts[p] = n;
+  counts[p] = clamp > 0 && n > clamp ? clamp : n;
 }
 
 // ---------------------------------------------------------------------------
@@ -540,9 +543,9 @@ int exclusive_scan_i64(int64_t* inout, int64_t n_plus_1, void* ws, size_t ws_byt
 }
 
 int launch_node_offsets(const fs_pose_batch& b, int64_t* node_off, void* ws, size_t ws_bytes,
-                        cudaStream_t st) {
+                        cudaStream_t st, int64_t clamp) {
   if (b.n_poses <= 0) return cuda_status(cudaMemsetAsync(node_off, 0, sizeof(int64_t), st));
-  pose_node_counts_kernel<<<(int)cdiv(b.n_poses, 256), 256, 0, st>>>(b, node_off);
+  pose_node_counts_kernel<<<(int)cdiv(b.n_poses, 256), 256, 0, st>>>(b, node_off, clamp);
   FS_LAUNCH_CHECK();
   FS_CUDA_CHECK(cudaMemsetAsync(node_off + b.n_poses, 0, sizeof(int64_t), st));
   return exclusive_scan_i64(node_off, b.n_poses + 1, ws, ws_bytes, st);

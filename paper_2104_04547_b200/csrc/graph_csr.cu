@@ -157,7 +157,10 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
 
   auto fail = [&](int flags) {
     if (threadIdx.x == 0) atomicOr(&a.err[p], flags);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    // an oversize pose owns only smem_atoms node rows (launch_node_offsets
+    // clamps its count), so empty rows are written for those alone
+    const int nr = min(n, a.smem_atoms);
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
       a.deg_cov[base + i] = 0; a.deg_ncov[base + i] = 0;
       a.row_cov[base + i] = cbase; a.row_ncov[base + i] = cbase;
     }
@@ -1008,6 +1011,101 @@ int launch_graph_fact(const fs_pose_batch& b, double tc, double tn, double box, 
   if (smem > 227 * 1024) return FS_ECAPACITY;
   FS_CUDA_CHECK(cudaFuncSetAttribute(graph_fact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   graph_fact_kernel<<<b.n_poses, kCsrThreads, smem, st>>>(a);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
+// ===========================================================================
+// Inspection of the scoring-path graphs (fs_scoring_graph): every DIRECTED
+// CSR entry (i, j) that graph_csr_kernel / graph_fact_kernel left for the
+// SG-CNN, mapped back to the pose's original node numbering (pocket atoms,
+// then its own atoms), with the float64 distance of the pair recomputed by
+// the reference's formula (the scoring kernels never store distances).
+// Padding entries (rows are padded to 4 ids) are not listed.
+// ===========================================================================
+struct CsrEntriesArgs {
+  fs_pose_batch b;
+  const int64_t* node_off;                          // full mode
+  const int32_t* fact_cnt; const int32_t* aff;      // factored mode (null: full)
+  int64_t S, cap, cap_out;
+  const int64_t* row[2]; const int32_t* deg[2]; const col_t* col[2];
+  int32_t* n_out[2]; int32_t* ent[2]; double* dist[2];
+  const int32_t* err;
+};
+
+__global__ void __launch_bounds__(256) csr_entries_kernel(CsrEntriesArgs a) {
+  extern __shared__ int s_off[];      // [rows + 1]
+  __shared__ int warp_tot[32];
+  const int p = blockIdx.x;
+  const PoseView pv = pose_view(a.b, p);
+  const bool fact = a.fact_cnt != nullptr;
+  const int np = (int)pv.np_;
+  int rows, nL = 0, nLp = 0;
+  int64_t nb;
+  if (fact) {
+    nL = a.fact_cnt[2 * p];
+    nLp = (nL + 15) & ~15;
+    rows = nLp + a.fact_cnt[2 * p + 1];
+    nb = (int64_t)p * a.S;
+  } else {
+    nb = a.node_off[p];
+    rows = (int)(a.node_off[p + 1] - nb);
+  }
+  if (a.err[p]) {
+    if (threadIdx.x < 2) a.n_out[threadIdx.x][p] = 0;
+    return;
+  }
+  // compact factored row -> original node id (ligand rows, zero pad rows, touched pocket atoms)
+  auto node_id = [&](int r) -> int {
+    if (!fact) return r;
+    return r < nL ? np + r : (r >= nLp ? a.aff[nb + r] : -1);
+  };
+  for (int t = 0; t < 2; ++t) {
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) s_off[r] = a.deg[t][nb + r];
+    block_exclusive_scan(s_off, rows, warp_tot);
+    const int64_t cb = (int64_t)p * a.cap, ob = (int64_t)p * a.cap_out;
+    const int total = s_off[rows];
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+      const int d = a.deg[t][nb + r];
+      if (!d) continue;
+      const int i = node_id(r);
+      double xi, yi, zi; int32_t e_, r_;
+      pv.atom(i, xi, yi, zi, e_, r_);
+      const int64_t s = a.row[t][nb + r] - cb;
+      for (int k = 0; k < d; ++k) {
+        const int j = node_id(a.col[t][cb + s + k]);
+        const int64_t o = ob + s_off[r] + k;
+        if (s_off[r] + k >= a.cap_out) break;
+        a.ent[t][2 * o] = i;
+        a.ent[t][2 * o + 1] = j;
+        if (a.dist[t]) {
+          double xj, yj, zj;
+          pv.atom(j, xj, yj, zj, e_, r_);
+          a.dist[t][o] = __dsqrt_rn(dist2_exact(xi - xj, yi - yj, zi - zj));
+        }
+      }
+    }
+    if (threadIdx.x == 0) a.n_out[t][p] = total;
+    __syncthreads();
+  }
+}
+
+int launch_csr_entries(const fs_pose_batch& b, const int64_t* node_off, const int32_t* fact_cnt, const int32_t* aff,
+                       int64_t S, int64_t cap, int max_rows, const int64_t* row_cov, const int32_t* deg_cov,
+                       const col_t* col_cov, const int64_t* row_ncov, const int32_t* deg_ncov, const col_t* col_ncov,
+                       int64_t cap_out, int32_t* n_cov, int32_t* n_ncov, int32_t* ent_cov, int32_t* ent_ncov,
+                       double* d_cov, double* d_ncov, const int32_t* err, cudaStream_t st) {
+  if (b.n_poses <= 0) return FS_OK;
+  CsrEntriesArgs a;
+  a.b = b; a.node_off = node_off; a.fact_cnt = fact_cnt; a.aff = aff; a.S = S;
+  // the scoring kernels round their slice capacity down to 4 entries
+  a.cap = cap & ~static_cast<int64_t>(3); a.cap_out = cap_out;
+  a.row[0] = row_cov; a.row[1] = row_ncov; a.deg[0] = deg_cov; a.deg[1] = deg_ncov;
+  a.col[0] = col_cov; a.col[1] = col_ncov; a.n_out[0] = n_cov; a.n_out[1] = n_ncov;
+  a.ent[0] = ent_cov; a.ent[1] = ent_ncov; a.dist[0] = d_cov; a.dist[1] = d_ncov; a.err = err;
+  const size_t smem = (size_t)(max_rows + 2) * 4;
+  FS_CUDA_CHECK(cudaFuncSetAttribute(csr_entries_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  csr_entries_kernel<<<b.n_poses, 256, smem, st>>>(a);
   FS_LAUNCH_CHECK();
   return FS_OK;
 }

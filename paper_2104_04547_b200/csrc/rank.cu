@@ -26,28 +26,40 @@ __device__ __forceinline__ float score_from_bits(uint32_t k) {
   return __uint_as_float(u);
 }
 
+// Two stable radix passes give the order (score desc, index asc) over the full
+// 64-bit pose index: sort by index, then stably by the 32-bit score key.
+__device__ __forceinline__ uint64_t index_key(int64_t i) {   // signed -> unsigned order
+  return static_cast<uint64_t>(i) ^ 0x8000000000000000ull;
+}
+
 __global__ void topk_keys_kernel(const float* as, const int64_t* ai, int64_t na, const float* bs,
-                                 const int64_t* bi, int64_t nb, uint64_t* keys) {
+                                 const int64_t* bi, int64_t nb, uint64_t* idx_keys, uint32_t* score_keys) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= na + nb) return;
   float s; int64_t i;
   if (t < na) { s = as[t]; i = ai[t]; } else { s = bs[t - na]; i = bi[t - na]; }
-  keys[t] = ((uint64_t)score_desc_bits(s) << 32) | (uint64_t)(uint32_t)i;
+  idx_keys[t] = index_key(i);
+  score_keys[t] = score_desc_bits(s);
 }
 
-__global__ void topk_decode_kernel(const uint64_t* keys, int64_t k, float* os, int64_t* oi) {
+__global__ void topk_decode_kernel(const uint32_t* score_keys, const uint64_t* idx_keys, int64_t k, float* os,
+                                   int64_t* oi) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= k) return;
-  uint64_t key = keys[t];
-  os[t] = score_from_bits((uint32_t)(key >> 32));
-  oi[t] = (int64_t)(uint32_t)key;
+  os[t] = score_from_bits(score_keys[t]);
+  oi[t] = static_cast<int64_t>(idx_keys[t] ^ 0x8000000000000000ull);
 }
 
-size_t topk_ws_bytes(int64_t n) {
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, tmp, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n);
-  return tmp + 2 * (size_t)n * 8 + 512;
+static size_t topk_tmp_bytes(int64_t n) {
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int)n);
+  cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint64_t*)nullptr,
+                                  (uint64_t*)nullptr, (int)n);
+  return t1 > t2 ? t1 : t2;
 }
+
+size_t topk_ws_bytes(int64_t n) { return topk_tmp_bytes(n) + 2 * (size_t)n * (8 + 4) + 1024; }
 
 int launch_topk_merge(const float* as, const int64_t* ai, int64_t na, const float* bs,
                       const int64_t* bi, int64_t nb, int k, float* os, int64_t* oi, void* ws,
@@ -56,17 +68,19 @@ int launch_topk_merge(const float* as, const int64_t* ai, int64_t na, const floa
   if (k < 0) return FS_EINVAL;
   if (n == 0 || k == 0) return FS_OK;
   if ((size_t)topk_ws_bytes(n) > ws_bytes) return FS_ECAPACITY;
-  char* w = (char*)ws;
-  uint64_t* keys_in = (uint64_t*)w;
-  uint64_t* keys_out = keys_in + n;
-  void* tmp = (void*)(((uintptr_t)(keys_out + n) + 255) & ~(uintptr_t)255);
-  size_t tmp_bytes = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys_in, keys_out, (int)n, 0, 64, st);
-  topk_keys_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(as, ai, na, bs, bi, nb, keys_in);
+  uint64_t* ik0 = (uint64_t*)ws;
+  uint64_t* ik1 = ik0 + n;
+  uint32_t* sk0 = (uint32_t*)(ik1 + n);
+  uint32_t* sk1 = sk0 + n;
+  void* tmp = (void*)(((uintptr_t)(sk1 + n) + 255) & ~(uintptr_t)255);
+  size_t tmp_bytes = topk_tmp_bytes(n);
+  topk_keys_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(as, ai, na, bs, bi, nb, ik0, sk0);
   FS_LAUNCH_CHECK();
-  FS_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys_in, keys_out, (int)n, 0, 64, st));
+  // pass 1: by pose index (all 64 bits); pass 2: stably by score key
+  FS_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ik0, ik1, sk0, sk1, (int)n, 0, 64, st));
+  FS_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, sk1, sk0, ik1, ik0, (int)n, 0, 32, st));
   const int64_t kk = k < n ? k : n;
-  topk_decode_kernel<<<(unsigned)cdiv(kk, 256), 256, 0, st>>>(keys_out, kk, os, oi);
+  topk_decode_kernel<<<(unsigned)cdiv(kk, 256), 256, 0, st>>>(sk0, ik0, kk, os, oi);
   FS_LAUNCH_CHECK();
   return FS_OK;
 }

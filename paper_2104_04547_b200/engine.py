@@ -231,6 +231,34 @@ def edge_lists(g: DeviceGraph, which="cov"):
     return edges[:e], (None if dists is None else dists[:e]), edge_off
 
 
+def scoring_graph_entries(batch: PoseBatch, cov_thresh=2.24, noncov_thresh=5.22, max_edges=32768,
+                          factored=False, max_pocket_atoms=0, c_elem=4, box_size=16.0, with_dists=True):
+    """The radius graph exactly as the scoring path builds it (fs_scoring_graph):
+    dict(n_cov [P], n_ncov [P], ent_cov [P, max_edges, 2], ent_ncov, d_cov
+    [P, max_edges], d_ncov, err [P]) -- directed CSR entries per pose in the
+    pose's original node numbering; only the first n_*[p] of each are set."""
+    L = N.lib()
+    dev = batch.device
+    P = batch.n_poses
+    nbytes = L.fs_scoring_graph_ws_bytes(P, batch.max_pose_atoms, max_edges, int(bool(factored)), c_elem)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    out = {"n_cov": torch.zeros(P, dtype=torch.int32, device=dev),
+           "n_ncov": torch.zeros(P, dtype=torch.int32, device=dev),
+           "ent_cov": torch.empty((P, max_edges, 2), dtype=torch.int32, device=dev),
+           "ent_ncov": torch.empty((P, max_edges, 2), dtype=torch.int32, device=dev),
+           "err": torch.empty(P, dtype=torch.int32, device=dev)}
+    if with_dists:
+        out["d_cov"] = torch.empty((P, max_edges), dtype=torch.float64, device=dev)
+        out["d_ncov"] = torch.empty((P, max_edges), dtype=torch.float64, device=dev)
+    s = batch.cstruct()
+    N.check(L.fs_scoring_graph(C.byref(s), cov_thresh, noncov_thresh, max_edges, int(bool(factored)),
+                               int(max_pocket_atoms), c_elem, float(box_size), _ptr(ws), ws.numel(),
+                               _ptr(out["n_cov"]), _ptr(out["n_ncov"]), _ptr(out["ent_cov"]), _ptr(out["ent_ncov"]),
+                               _ptr(out.get("d_cov")), _ptr(out.get("d_ncov")), _ptr(out["err"]), _stream()),
+            "fs_scoring_graph")
+    return out
+
+
 def node_features(batch: PoseBatch, node_off, c_elem=4, box_size=16.0):
     L = N.lib()
     n = int(node_off[-1].item())
@@ -370,9 +398,13 @@ class DeviceModel:
             cap *= 2
 
     # ---- pocket-invariant factoring ----
-    def prepare_pockets(self, pocket_xyz, pocket_elem, pocket_role, pocket_off):
+    def prepare_pockets(self, pocket_xyz, pocket_elem, pocket_role, pocket_off, precision="bf16"):
         """Build the pocket cache (fs_pocket_prepare) for the given device
-        pocket arrays (fs_pose_batch layout).  Returns a PocketCache."""
+        pocket arrays (fs_pose_batch layout) at `precision` ("bf16" or
+        "mixed"; the cache scores only at that precision).  Returns a
+        PocketCache."""
+        if precision not in ("bf16", "mixed"):
+            raise ValueError(f"pocket factoring runs at bf16 or mixed precision, not {precision!r}")
         L = N.lib()
         off_h = pocket_off.cpu().numpy()
         n = len(off_h) - 1
@@ -383,20 +415,22 @@ class DeviceModel:
         cache = torch.empty(max(n, 1) * stride, dtype=torch.uint8, device=self.device)
         err = torch.zeros(max(n, 1), dtype=torch.int32, device=self.device)
         ws = self.workspace(L.fs_pocket_prepare_ws_bytes(self.handle, n, mp))
-        N.check(L.fs_pocket_prepare(self.handle, _ptr(pocket_xyz), _ptr(pocket_elem), _ptr(pocket_role),
+        N.check(L.fs_pocket_prepare(self.handle, N.PRECISIONS[precision], _ptr(pocket_xyz), _ptr(pocket_elem), _ptr(pocket_role),
                                     _ptr(pocket_off), n, mp, _ptr(cache), _ptr(err), _ptr(ws), ws.numel(),
                                     _stream()), "fs_pocket_prepare")
         bad = err[:n].cpu().numpy()
         if bad.any():
             raise ValueError(f"pocket preparation failed (err bits {bad.tolist()})")
-        return PocketCache(cache, err, n, mp, stride)
+        return PocketCache(cache, err, n, mp, stride, precision)
 
     def score_poses_cached(self, batch: PoseBatch, cache: "PocketCache", max_edges_per_pose=32768,
                            outputs=("scores",), rescore=True):
-        """fs_score_poses_cached (bf16): scores from ligand atoms + the pocket
-        cache.  Poses flagged FS_ERR_NOT_FACTORED (or EDGE_CAP) are re-scored
-        through the full path when `rescore` (needs a host read of err)."""
+        """fs_score_poses_cached at the cache's precision: scores from ligand
+        atoms + the pocket cache.  Poses flagged FS_ERR_NOT_FACTORED (or
+        EDGE_CAP) are re-scored through the full path when `rescore` (needs a
+        host read of err)."""
         L = N.lib()
+        prec = N.PRECISIONS[cache.precision]
         P = batch.n_poses
         dev = self.device
         out = {"scores": torch.empty(P, dtype=torch.float32, device=dev),
@@ -407,10 +441,10 @@ class DeviceModel:
                 out[k] = torch.empty(shape, dtype=torch.float32, device=dev)
         cap = int(max_edges_per_pose)
         S = (batch.max_pose_atoms + 15) // 16 * 16 + 32
-        nbytes = L.fs_workspace_bytes(self.handle, P, P * S, max(1, P) * cap, N.PRECISIONS["bf16"])
+        nbytes = L.fs_workspace_bytes(self.handle, P, P * S, max(1, P) * cap, prec)
         ws = self.workspace(nbytes)
         s = batch.cstruct()
-        N.check(L.fs_score_poses_cached(self.handle, N.PRECISIONS["bf16"], C.byref(s), _ptr(cache.buf),
+        N.check(L.fs_score_poses_cached(self.handle, prec, C.byref(s), _ptr(cache.buf),
                                         cache.max_pocket_atoms, cap, _ptr(ws), ws.numel(), _ptr(out["scores"]),
                                         _ptr(out.get("lat_v")), _ptr(out.get("lat_g")), _ptr(out.get("pred_v")),
                                         _ptr(out.get("pred_g")), _ptr(out["err"]), _stream()),
@@ -418,7 +452,7 @@ class DeviceModel:
         if rescore:
             redo = ((out["err"] & (N.FS_ERR_NOT_FACTORED | N.FS_ERR_EDGE_CAP)) != 0).nonzero().flatten()
             if redo.numel():
-                full = self.score_poses(batch, "bf16", max_edges_per_pose, outputs)
+                full = self.score_poses(batch, cache.precision, max_edges_per_pose, outputs)
                 for k, v in out.items():
                     v[redo] = full[k][redo]
         return out
@@ -434,8 +468,7 @@ class DeviceModel:
         ce = cov_edges if cov_edges is not None else torch.empty((0, 2), dtype=torch.int64, device=dev)
         ne = ncov_edges if ncov_edges is not None else torch.empty((0, 2), dtype=torch.int64, device=dev)
         nc, nn = int(ce.shape[0]), int(ne.shape[0])
-        E = 2 * max(nc, nn)
-        nbytes = L.fs_workspace_bytes(self.handle, P, n_nodes, E, prec)
+        nbytes = L.fs_features_workspace_bytes(self.handle, P, n_nodes, max(nc, nn), prec)
         ws = self.workspace(nbytes)
         out = {"err": torch.empty(P, dtype=torch.int32, device=dev),
                "scores": torch.empty(P, dtype=torch.float32, device=dev),
@@ -494,6 +527,7 @@ class PocketCache:
     n_pockets: int
     max_pocket_atoms: int
     stride: int
+    precision: str = "bf16"
 
 
 class BestPoseAccumulator:

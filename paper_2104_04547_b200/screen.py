@@ -113,14 +113,14 @@ class Screen:
     """Scores a DeviceLibrary batch by batch with a running device top-k.
 
     ``pocket_cache`` (DeviceModel.prepare_pockets of the library's pockets)
-    switches to the pocket-factored scorer (SURVEY.md 8f-4, bf16): same
+    switches to the pocket-factored scorer (SURVEY.md 8f-4, bf16/mixed): same
     scores to fp32 rounding; non-factorable poses come back flagged
     FS_ERR_NOT_FACTORED (rescore them with a plain Screen)."""
 
     def __init__(self, model: E.DeviceModel, precision="bf16", batch_size=8192, k=100,
                  max_edges_per_pose=32768, pocket_cache=None):
-        if pocket_cache is not None and precision != "bf16":
-            raise ValueError("the pocket-factored scorer is bf16 only")
+        if pocket_cache is not None and precision != pocket_cache.precision:
+            raise ValueError(f"pocket cache prepared at {pocket_cache.precision!r}, screen runs {precision!r}")
         self.model = model
         self.precision = precision
         self.B = batch_size
@@ -181,21 +181,28 @@ def compound_topk(acc: E.BestPoseAccumulator, k):
             "topk_compound_idx": ci}
 
 
-def merge_topk_across_ranks(top_s, top_i, k, group=None, merge=None):
+def merge_topk_across_ranks(top_s, top_i, k, group=None, merge=None, device=None):
     """All-gather every rank's top-k (NCCL over NVLink) and merge on device.
-    Ranks holding fewer than k entries pad with NaN (ranked last).  `merge`
-    defaults to the device kernel fs_topk_merge (tests pass a CPU rule)."""
+    Ranks holding fewer than k entries -- or none (an empty shard: ``top_s``
+    None) -- pad with NaN scores (ranked last) and the largest index, so every
+    rank joins the collective.  `merge` defaults to the device kernel
+    fs_topk_merge (tests pass a CPU rule)."""
     import torch.distributed as dist
     merge = merge or (lambda s, i, kk: E.topk_merge(s, i, None, None, kk))
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return top_s, top_i
+    if device is None:
+        device = top_s.device if top_s is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
     ws = dist.get_world_size(group)
-    pad_s = torch.full((k,), float("nan"), dtype=torch.float32, device=top_s.device)
-    pad_i = torch.full((k,), np.iinfo(np.int32).max, dtype=torch.int64, device=top_s.device)
-    pad_s[: top_s.numel()] = top_s
-    pad_i[: top_i.numel()] = top_i
-    gs = torch.empty(ws * k, dtype=torch.float32, device=top_s.device)
-    gi = torch.empty(ws * k, dtype=torch.int64, device=top_s.device)
+    pad_s = torch.full((k,), float("nan"), dtype=torch.float32, device=device)
+    pad_i = torch.full((k,), np.iinfo(np.int64).max, dtype=torch.int64, device=device)
+    if top_s is not None and top_s.numel():
+        pad_s[: top_s.numel()] = top_s
+        pad_i[: top_i.numel()] = top_i
+    gs = torch.empty(ws * k, dtype=torch.float32, device=device)
+    gi = torch.empty(ws * k, dtype=torch.int64, device=device)
     dist.all_gather_into_tensor(gs, pad_s, group=group)
     dist.all_gather_into_tensor(gi, pad_i, group=group)
+    # fewer than k entries over all ranks leave trailing pads (NaN, int64 max)
     return merge(gs, gi, k)

@@ -16,22 +16,18 @@ from tests._cfg import COHERENT, GRAPH, VOXEL  # noqa: E402
 
 @pytest.fixture(scope="module")
 def env():
-    """The fp32-class SG-CNN (FS_GNN_SPLIT=3) for this module: a batch with
+    """The mixed precision (fp32-class SG-CNN) for this module: a batch with
     128-atom ligands exceeds the tensor-core SG-CNN's shared memory on the
     full path, which then runs the FFMA kernel, so the factored path (which
-    fits) is compared against fp32 arithmetic."""
-    import os
-
+    fits) is compared against fp32-class arithmetic."""
     import torch
 
     from paper_2104_04547_b200 import engine as E
     from paper_2104_04547_b200 import models, synth
-    prev = os.environ.get("FS_GNN_SPLIT")
-    os.environ["FS_GNN_SPLIT"] = "3"
     vcfg, gcfg, fcfg = models.VoxelHeadConfig(), models.GraphHeadConfig(), models.table_coherent_fusion_config()
     dm = E.DeviceModel(vcfg, gcfg, fcfg, models.FusionModel(vcfg, gcfg, fcfg, seed=0).all_params())
-    if not dm.supports("bf16"):
-        pytest.skip("bf16 path unsupported")
+    if not dm.supports("mixed"):
+        pytest.skip("tensor-core path unsupported")
     pockets = [synth.make_pocket(1000, seed=41, name="a"), synth.make_pocket(420, seed=42, name="b")]
     lib = synth.concat([synth.make_poses(9, 5, seed=43, target=0),
                         synth.make_poses(6, 4, seed=44, target=1, ligand_atoms=(3, 100)),
@@ -40,12 +36,9 @@ def env():
           np.concatenate([p.role for p in pockets]),
           np.concatenate([[0], np.cumsum([len(p.xyz) for p in pockets])]))
     batch = E.batch_from_arrays(lib.xyz, lib.elem, lib.role, lib.atom_off, pocket=pk, pose_target=lib.target)
-    cache = dm.prepare_pockets(batch.pocket_xyz, batch.pocket_elem, batch.pocket_role, batch.pocket_off)
+    cache = dm.prepare_pockets(batch.pocket_xyz, batch.pocket_elem, batch.pocket_role, batch.pocket_off,
+                               precision="mixed")
     yield torch, E, synth, dm, pockets, lib, pk, batch, cache
-    if prev is None:
-        os.environ.pop("FS_GNN_SPLIT", None)
-    else:
-        os.environ["FS_GNN_SPLIT"] = prev
 
 
 def _rel(a, b):
@@ -56,7 +49,7 @@ def _rel(a, b):
 def test_factored_equals_full_path(env):
     torch, E, synth, dm, pockets, lib, pk, batch, cache = env
     outs = ("scores", "lat_v", "lat_g")
-    full = dm.score_poses(batch, "bf16", 1 << 17, outs, retry=False)
+    full = dm.score_poses(batch, "mixed", 1 << 17, outs, retry=False)
     fact = dm.score_poses_cached(batch, cache, 1 << 17, outs, rescore=False)
     assert int(full["err"].abs().sum()) == 0
     assert int(fact["err"].abs().sum()) == 0
@@ -107,7 +100,7 @@ def test_non_factorable_poses_are_flagged_and_rescored(env):
     assert err[2] & 128 and err[6] & 128
     assert not err[[0, 1, 3, 4, 5]].any()
     fixed = dm.score_poses_cached(b, cache)
-    full = dm.score_poses(b, "bf16")
+    full = dm.score_poses(b, "mixed")
     assert not fixed["err"].cpu().numpy().any()
     s_fixed, s_full = fixed["scores"].cpu().numpy(), full["scores"].cpu().numpy()
     assert s_fixed[2] == s_full[2] and s_fixed[6] == s_full[6]

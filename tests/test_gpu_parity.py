@@ -294,6 +294,42 @@ def test_model_scorer_plugin(pkg):
         scorer([harness.PoseRecord("c0", "t0", 0, None)])
 
 
+def test_foreign_payload_classes(pkg):
+    """Payload classes from another package (here: bare classes with the
+    reference's attribute names, as fusionscreen.complexes defines them) go
+    through predict_batch and ModelScorer unchanged (duck typing; the drop-in
+    contract of harness.py:224-234)."""
+    cx, E, models, synth = pkg
+    from paper_2104_04547_b200 import harness
+    z = load("model_golden.npz")
+    vcfg, gcfg = models.VoxelHeadConfig(), models.GraphHeadConfig()
+    model = models.FusionModel(vcfg, gcfg, models.table_coherent_fusion_config(), seed=0)
+    cs, items = _reference_items(z, cx, models, vcfg, gcfg)
+
+    class Grid:                     # fusionscreen.complexes.VoxelGrid's fields
+        def __init__(self, occ):
+            self.occupancy = occ
+
+    class Graph:                    # fusionscreen.complexes.ComplexGraph's fields
+        def __init__(self, g):
+            for k in ("node_features", "covalent_edges", "noncovalent_edges", "covalent_dists",
+                      "noncovalent_dists"):
+                setattr(self, k, np.array(getattr(g, k)))
+
+    class Complex:                  # fusionscreen.complexes.SyntheticComplex's fields
+        def __init__(self, c):
+            self.complex_id, self.label_pk = c.complex_id, 0.0
+            self.positions, self.elements, self.roles = c.positions, c.elements, c.roles
+
+    pairs = [(Grid(it.grid.occupancy.copy()), Graph(it.graph)) for it in items]
+    preds, errors = model.predict_batch(pairs)
+    assert errors == [] and _rel(preds, z["scores"]) < 1e-3
+    scorer = harness.ModelScorer(model)
+    assert scorer([harness.PoseRecord(f"c{i}", "t", 0, pr) for i, pr in enumerate(pairs)]) == preds
+    raw = scorer([harness.PoseRecord(f"c{i}", "t", 0, Complex(c)) for i, c in enumerate(cs)])
+    assert _rel(raw, z["scores"]) < 1e-3
+
+
 def test_edge_capacity_overflow_retries(pkg):
     cx, E, models, synth = pkg
     z = load("model_golden.npz")

@@ -157,32 +157,31 @@ def test_bf16_batch_invariance_bitwise(setup):
         assert np.array_equal(got, whole[s:e])
 
 
-@pytest.mark.parametrize("split,tol", [("3", 1e-4), ("2", 5e-3)])
-def test_tensorcore_gnn_matches_ffma_gnn(setup, monkeypatch, split, tol):
+@pytest.mark.parametrize("precision,tol", [("mixed", 1e-4), ("bf16", 5e-3)])
+def test_tensorcore_gnn_matches_ffma_gnn(setup, precision, tol):
     """mma.sync SG-CNN vs the FFMA fp32 kernel on the same graphs (|lat| ~ 0.1).
-    FS_GNN_SPLIT=3 (bf16 hi/lo x hi/lo, fp32-class): latent_g within 1e-4
-    absolute; 2 (default: fp16 activations hi/lo x fp16 weights): the fp16
-    weight rounding (2^-12) is a fixed perturbation of the model, stated
+    "mixed" (bf16 hi/lo x hi/lo, 3 passes, fp32-class): latent_g within 1e-4
+    absolute; "bf16" (fp16 activations hi/lo x fp16 weights, 2 passes): the
+    fp16 weight rounding (2^-12) is a fixed perturbation of the model, stated
     tolerance 5e-3 (measured ~1.6e-3)."""
     torch, N, m, dm = setup
     from paper_2104_04547_b200 import engine as E
     from paper_2104_04547_b200 import synth
-    monkeypatch.setenv("FS_GNN_SPLIT", split)
     pocket = synth.make_pocket(1000, seed=9)
     lib = synth.make_poses(40, poses_per_compound=10, seed=10).slice(0, 397)
     b = E.batch_from_arrays(lib.xyz, lib.elem, lib.role, lib.atom_off,
                             pocket=(pocket.xyz, pocket.elem, pocket.role, np.array([0, 1000])),
                             pose_target=lib.target)
     g32 = dm.score_poses(b, "fp32", outputs=("lat_g",))["lat_g"]
-    g16 = dm.score_poses(b, "bf16", outputs=("lat_g",))["lat_g"]
+    g16 = dm.score_poses(b, precision, outputs=("lat_g",))["lat_g"]
     torch.cuda.synchronize()
     diff = float((g32 - g16).abs().max())
-    print(f"tensor-core GNN (split {split}) vs FFMA GNN: max |dlat_g| = {diff:.3e}")
+    print(f"tensor-core GNN ({precision}) vs FFMA GNN: max |dlat_g| = {diff:.3e}")
     assert diff < tol
 
 
 def test_factored_equals_full_path_default_split(setup):
-    """Default (FS_GNN_SPLIT=2) SG-CNN on both paths: ligands <= 64 atoms keep
+    """bf16-precision SG-CNN on both paths: ligands <= 64 atoms keep
     the full path on the tensor-core SG-CNN, so the pocket-factored scores
     differ only by fp32 summation order."""
     torch, N, m, dm = setup
