@@ -426,16 +426,16 @@ def config_legs(dm, E, N, dev, precision):
         # edge lists are pose-local: lift them to global node ids
         cp = torch.repeat_interleave(torch.arange(B3, device=dev), coff.diff())
         np_ = torch.repeat_interleave(torch.arange(B3, device=dev), noff.diff())
-        inputs.append((grids, feats, no, ce + no[cp][:, None], ne + no[np_][:, None]))
+        inputs.append((grids, feats, no, ce + no[cp][:, None], ne + no[np_][:, None], int(no.diff().max().item())))
     for prec, n_batches in (("bf16", 391), ("fp32", 100)):
         for head, name in ((1, "voxel"), (2, "graph")):
             def once(i):
-                grids, feats, no, ce, ne = inputs[i % n_inputs]
+                grids, feats, no, ce, ne, mpn = inputs[i % n_inputs]
                 if head == 1:
-                    dm.score_features(B3, grids=grids, heads=1, precision=prec)
+                    dm.score_features(B3, grids=grids, heads=1, precision=prec, max_pose_nodes=0)
                 else:
                     dm.score_features(B3, feats=feats, node_off=no, cov_edges=ce, ncov_edges=ne, heads=2,
-                                      precision=prec)
+                                      precision=prec, max_pose_nodes=mpn)
             once(0)
             torch.cuda.synchronize()
             e0, e1 = ev(), ev()
@@ -558,7 +558,7 @@ def main():
         # per-compound best pose (all on device)
         for a in range(s, e, BMAX):
             b = min(e, a + BMAX)
-            out = dm.score_poses(dlib.batch(a, b), precision, 32768, retry=False)
+            out = score_call(lambda x, y: dm.score_poses(dlib.batch(x, y), precision, 32768, retry=False), a, b)
             top = E.topk_merge(top[0], top[1], out["scores"], dlib.pidx[a:b], TOPK)
             acc.update(dlib.compound[a:b], dlib.pose_id[a:b], out["scores"])
         return out, top
@@ -578,10 +578,20 @@ def main():
     torch.cuda.synchronize()
     assert int(out["err"].abs().sum().item()) == 0, "pose errors in warm-up batch"
 
-    stage_events = [[torch.cuda.Event(enable_timing=True) for _ in N.STAGES] for _ in range(K)]
-    for evs in stage_events:          # torch creates CUDA events lazily: force creation
+    # one set of stage events per fs_score_poses call (a step is one or more calls)
+    calls = [(a, min(e, a + BMAX)) for s, e in bounds for a in range(s, e, BMAX)]
+    stage_events = {c: [torch.cuda.Event(enable_timing=True) for _ in N.STAGES] for c in calls}
+    for evs in stage_events.values():   # torch creates CUDA events lazily: force creation
         for e in evs:
             e.record()
+    ev_ptrs = {c: (E.C.c_void_p * len(evs))(*[E.C.c_void_p(e.cuda_event) for e in evs])
+               for c, evs in stage_events.items()}
+
+    def score_call(scoref, a, b):
+        L.fs_set_stage_events(ev_ptrs[(a, b)], len(N.STAGES))
+        out = scoref(a, b)
+        L.fs_set_stage_events(None, 0)
+        return out
 
     def run_steps(stepf):
         top = (None, None)
@@ -589,12 +599,8 @@ def main():
         errs = []
         for i in range(K):
             flush.zero_()                                  # L2 flush between steps
-            evs = stage_events[i]
-            arr = (E.C.c_void_p * len(evs))(*[E.C.c_void_p(e.cuda_event) for e in evs])
-            L.fs_set_stage_events(arr, len(evs))
             s, e = bounds[i]
             out, top = stepf(s, e, top, acc)
-            L.fs_set_stage_events(None, 0)
             errs.append(out["err"])
         return top, acc, errs
 
@@ -617,10 +623,10 @@ def main():
             torch.cuda.synchronize()
             return None
 
-    def stage_sum():
+    def stage_sum(only=None):
         tot = np.zeros(len(N.STAGES) - 1)
-        for i in range(K):
-            evs = stage_events[i]
+        for c in (only or calls):
+            evs = stage_events[c]
             for j in range(len(N.STAGES) - 1):
                 tot[j] += evs[j].elapsed_time(evs[j + 1])
         return tot
@@ -667,21 +673,14 @@ def main():
     L.fs_set_overlap(0)
     top_s = (None, None)
     acc_s = E.BestPoseAccumulator(n_comp, c0, device=dev)
-    serial = np.zeros(len(N.STAGES) - 1)
-    n_serial = min(K, 3)
-    for i in range(n_serial):
-        evs = stage_events[i]
-        arr = (E.C.c_void_p * len(evs))(*[E.C.c_void_p(e.cuda_event) for e in evs])
+    serial_calls = [c for c in calls if c[1] > c[0]][:3]
+    for a, b in serial_calls:
         flush.zero_()
-        L.fs_set_stage_events(arr, len(evs))
-        s, e = bounds[i]
-        _, top_s = step(s, e, top_s, acc_s)
-        L.fs_set_stage_events(None, 0)
+        _, top_s = step(a, b, top_s, acc_s)
         torch.cuda.synchronize()
-        for j in range(len(N.STAGES) - 1):
-            serial[j] += evs[j].elapsed_time(evs[j + 1])
+    serial = stage_sum(serial_calls)
     L.fs_set_overlap(-1)
-    serial_poses = sum(bounds[i][1] - bounds[i][0] for i in range(n_serial))
+    serial_poses = sum(b - a for a, b in serial_calls)
 
     # ---- end to end: packed library file (memory-mapped) -> pinned double
     # buffer -> H2D on a copy stream overlapping the previous batch's scoring;
@@ -738,7 +737,8 @@ def main():
         def fstep(s, e, top, acc):
             for a in range(s, e, BMAX):
                 b = min(e, a + BMAX)
-                out = dm.score_poses_cached(dlib.batch(a, b), cache, 32768, rescore=False)
+                out = score_call(lambda x, y: dm.score_poses_cached(dlib.batch(x, y), cache, 32768, rescore=False),
+                                 a, b)
                 top = E.topk_merge(top[0], top[1], out["scores"], dlib.pidx[a:b], TOPK)
                 acc.update(dlib.compound[a:b], dlib.pose_id[a:b], out["scores"])
             return out, top
@@ -831,16 +831,16 @@ def main():
                 kern[nm]["ms_per_16384_poses"] = round(per_pose_ms[j] * 16384, 4)
         dom = int(np.argmax(serial))
         dom_name = names[dom]
-        avg_ms = stage_ms[dom] / K
+        ms_per_pose_timed = stage_ms[dom] / n_rank          # the timed run's own stage events
         gk = {"bf16": "gnn_mma_kernel<2> (GRU message passing on mma.sync: fp16 hi/lo activations x fp16 weights)",
               "mixed": "gnn_mma_kernel<3> (GRU message passing on mma.sync: bf16 hi/lo x hi/lo, 3 passes)",
               "fp32": "gnn_kernel (GRU message passing, FFMA fp32)"}[precision]
         if dom_name == "gnn":
-            roof = {"kernel": gk, "bound": "tensor", "achieved": gflop * B / (avg_ms / 1e3) / 1e12,
+            roof = {"kernel": gk, "bound": "tensor", "achieved": gflop / (ms_per_pose_timed / 1e3) / 1e12,
                     "peak": bf16_sus, "unit": "TFLOP/s", "traffic": None}
         elif dom_name in CONV_FLOP:
             roof = {"kernel": f"{dom_name} conv_umma_kernel", "bound": "tensor",
-                    "achieved": CONV_FLOP[dom_name] * B / (avg_ms / 1e3) / 1e12, "peak": bf16_sus,
+                    "achieved": CONV_FLOP[dom_name] / (ms_per_pose_timed / 1e3) / 1e12, "peak": bf16_sus,
                     "unit": "TFLOP/s", "traffic": None}
         else:
             roof = dict(kern.get(dom_name, {"bound": "tensor", "achieved": 0.0, "peak": bf16_sus, "unit": "TFLOP/s"}))
@@ -851,8 +851,8 @@ def main():
             key = {"gnn": "gnn", "conv1": "conv1", "conv2": "conv2", "featurize": "graph_csr"}.get(dom_name)
             ent = tr.get(f"{key}_{precision}") or tr.get(key)
             if ent:
-                roof["traffic"] = ent["bytes_per_pose"] * B
-                roof["traffic_unit"] = "bytes per launch"
+                roof["traffic"] = ent["bytes_per_pose"] * min(B, BMAX)
+                roof["traffic_unit"] = f"bytes per launch ({min(B, BMAX)} poses)"
                 roof["traffic_source"] = ("profiles/r02/ncu_traffic.json: ncu --set full dram__bytes_read.sum + "
                                           "dram__bytes_write.sum, per pose, scaled to this launch")
                 if "onchip" in ent:

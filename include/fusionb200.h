@@ -234,8 +234,8 @@ size_t fs_workspace_bytes(const fs_model* m, int32_t max_poses,
                           int64_t max_nodes, int64_t max_edges, int precision);
 /* Workspace for fs_score_features: the batch's total nodes and the larger of
  * its two i<j edge counts. */
-size_t fs_features_workspace_bytes(const fs_model* m, int32_t n_poses, int64_t n_nodes, int64_t n_edges,
-                                   int precision);
+size_t fs_features_workspace_bytes(const fs_model* m, int32_t n_poses, int64_t n_nodes, int32_t max_pose_nodes,
+                                   int64_t n_edges, int precision);
 
 /* Fused featurize + 3D-CNN + SG-CNN + fusion for raw poses (the screening
  * path: models.featurize (:638-651) then predict_batch).  Outputs (nullable
@@ -252,12 +252,14 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b,
 /* Pre-featurized batch: the drop-in predict_batch / voxel_head_forward /
  * graph_head_forward path.  grids: float64 [P,C,G,G,G] (VoxelGrid layout,
  * nullable when only the graph head is wanted); feats: float64
- * [N, c_elem+4]; node_off [P+1]; edges given as i<j pairs with GLOBAL node
+ * [N, c_elem+4]; node_off [P+1]; max_pose_nodes = the largest pose's node
+ * count (sizes the SG-CNN's on-chip node state; poses above it get
+ * FS_ERR_TOO_LARGE; <= 0: unknown, worst case assumed); edges given as i<j pairs with GLOBAL node
  * ids (int64 [E,2]) per edge type.  heads: bit0 voxel head, bit1 graph head,
  * bit2 fusion. */
 int fs_score_features(const fs_model* m, int precision, int32_t n_poses,
                       const double* grids, const double* feats,
-                      const int64_t* node_off, int64_t n_nodes,
+                      const int64_t* node_off, int64_t n_nodes, int32_t max_pose_nodes,
                       const int64_t* cov_edges, int64_t n_cov,
                       const int64_t* ncov_edges, int64_t n_ncov, int32_t heads,
                       void* ws, size_t ws_bytes, float* scores, float* lat_v,

@@ -104,7 +104,7 @@ def _sig(lib):
         "fs_graph_edge_counts": (C.c_int, [_P, _I32, _P, _P, _P, _P, _SZ, _P]),
         "fs_graph_edges": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P, _P]),
         "fs_workspace_bytes": (_SZ, [_P, _I32, _I64, _I64, C.c_int]),
-        "fs_features_workspace_bytes": (_SZ, [_P, _I32, _I64, _I64, C.c_int]),
+        "fs_features_workspace_bytes": (_SZ, [_P, _I32, _I64, _I32, _I64, C.c_int]),
         "fs_scoring_graph_ws_bytes": (_SZ, [_I32, _I32, _I64, _I32, _I32]),
         "fs_scoring_graph": (C.c_int, [sp, _D, _D, _I64, _I32, _I32, _I32, _D, _P, _SZ, _P, _P, _P, _P, _P, _P,
                                        _P, _P]),
@@ -114,7 +114,7 @@ def _sig(lib):
         "fs_pocket_prepare": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _SZ, _P]),
         "fs_score_poses_cached": (C.c_int, [_P, C.c_int, sp, _P, _I32, _I64, _P, _SZ, _P, _P, _P, _P, _P, _P,
                                             _P]),
-        "fs_score_features": (C.c_int, [_P, C.c_int, _I32, _P, _P, _P, _I64, _P, _I64, _P, _I64,
+        "fs_score_features": (C.c_int, [_P, C.c_int, _I32, _P, _P, _P, _I64, _I32, _P, _I64, _P, _I64,
                                         _I32, _P, _SZ, _P, _P, _P, _P, _P, _P, _P]),
         "fs_debug_conv": (C.c_int, [_P, C.c_int, _I32, _P, _P, _P, _P]),
         "fs_topk_ws_bytes": (_SZ, [_I64]),

@@ -96,6 +96,7 @@ int launch_dense(const DenseArgs& a, cudaStream_t st);
 int launch_finalize(int n, int mode, const float* pv, const float* pg, float* scores, const int32_t* err, cudaStream_t st);
 int launch_grid_convert(const double* in, void* out, int n_poses, int c, int g, bool bf16, int32_t* err, cudaStream_t st);
 int launch_f64_to_f32(const double* in, float* out, int64_t n, int row, const int32_t* node_pose, int32_t* err, cudaStream_t st);
+int launch_pose_bound(const int64_t* node_off, int n_poses, int64_t bound, int32_t* err, cudaStream_t st);
 
 struct GnnArgs {
   const float* feats; int F; const int64_t* node_off;
@@ -916,10 +917,12 @@ size_t fs_workspace_bytes(const fs_model* m, int32_t max_poses, int64_t max_node
   return plan_ws(*m, max_poses, max_nodes, max_edges, precision, pose_nodes).total + 256;
 }
 
-size_t fs_features_workspace_bytes(const fs_model* m, int32_t n_poses, int64_t n_nodes, int64_t n_edges,
-                                   int precision) {
+size_t fs_features_workspace_bytes(const fs_model* m, int32_t n_poses, int64_t n_nodes, int32_t max_pose_nodes,
+                                   int64_t n_edges, int precision) {
   if (!m || n_poses < 0 || n_nodes < 0 || n_edges < 0) return 0;
-  return plan_ws(*m, n_poses, n_nodes, 2 * n_edges, precision, n_nodes).total + 256;
+  const int64_t bound = max_pose_nodes > 0 ? (max_pose_nodes < n_nodes ? max_pose_nodes : n_nodes)
+                                           : (n_nodes < FS_MAX_POSE_ATOMS ? n_nodes : FS_MAX_POSE_ATOMS);
+  return plan_ws(*m, n_poses, n_nodes, 2 * n_edges, precision, bound).total + 256;
 }
 
 int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int64_t max_edges, void* ws,
@@ -1156,7 +1159,7 @@ int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch*
 }
 
 int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const double* grids,
-                      const double* feats, const int64_t* node_off, int64_t n_nodes,
+                      const double* feats, const int64_t* node_off, int64_t n_nodes, int32_t max_pose_nodes,
                       const int64_t* cov_edges, int64_t n_cov, const int64_t* ncov_edges, int64_t n_ncov,
                       int32_t heads, void* ws, size_t ws_bytes, float* scores, float* lat_v, float* lat_g,
                       float* pred_v, float* pred_g, int32_t* err, void* stream) {
@@ -1172,7 +1175,10 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const d
   if (need_g && (!feats || !node_off)) return FS_EINVAL;
   if (want_f && !scores) return FS_EINVAL;
   const int64_t E = 2 * (n_cov > n_ncov ? n_cov : n_ncov);
-  WsPlan w = plan_ws(*m, P, n_nodes, E, precision, n_nodes);
+  // per-pose node bound: the caller's (checked on device), else the worst case
+  const int64_t bound = max_pose_nodes > 0 ? (max_pose_nodes < n_nodes ? max_pose_nodes : n_nodes)
+                                           : (n_nodes < FS_MAX_POSE_ATOMS ? n_nodes : FS_MAX_POSE_ATOMS);
+  WsPlan w = plan_ws(*m, P, n_nodes, E, precision, bound);
   char* W = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   if ((size_t)(W - (char*)ws) + w.total > ws_bytes) return FS_ECAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1206,10 +1212,12 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const d
                                     scan_b, st)))
       return rc;
     if ((rc = launch_f64_to_f32(feats, (float*)(W + w.feats), n_nodes * m->F, m->F, node_pose, err, st))) return rc;
-    // max nodes per pose bounds the GNN's shared-memory state; the host
-    // passes it implicitly via n_nodes (worst case: one pose holds them all)
-    int max_nodes = (int)(n_nodes < FS_MAX_POSE_ATOMS ? n_nodes : FS_MAX_POSE_ATOMS);
-    if ((rc = graph_head(*m, P, max_nodes, W, w, err, late || pred_g, precision, st, nullptr, false))) return rc;
+    // the per-pose node bound sizes the SG-CNN's shared-memory node state (and
+    // picks the tensor-core kernel when it fits); poses above it are flagged
+    if ((rc = launch_pose_bound(noff, P, bound, err, st))) return rc;
+    if ((rc = graph_head(*m, P, (int)(bound < FS_MAX_POSE_ATOMS ? bound : FS_MAX_POSE_ATOMS), W, w, err,
+                         late || pred_g, precision, st, nullptr, false)))
+      return rc;
   }
   if (want_f) {
     if (!late && (rc = fusion_head(*m, P, W, w, scores, st))) return rc;

@@ -246,6 +246,20 @@ __global__ void f64_to_f32_kernel(const double* in, float* out, int64_t n, int r
   out[t] = (float)v;
 }
 
+// poses above the caller's per-pose node bound are flagged (the SG-CNN sizes
+// its shared-memory node state by that bound and skips flagged poses)
+__global__ void pose_bound_kernel(const int64_t* node_off, int n_poses, int64_t bound, int32_t* err) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n_poses && node_off[p + 1] - node_off[p] > bound) atomicOr(&err[p], FS_ERR_TOO_LARGE);
+}
+
+int launch_pose_bound(const int64_t* node_off, int n_poses, int64_t bound, int32_t* err, cudaStream_t st) {
+  if (n_poses <= 0) return FS_OK;
+  pose_bound_kernel<<<(unsigned)cdiv(n_poses, 256), 256, 0, st>>>(node_off, n_poses, bound, err);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
 int launch_f64_to_f32(const double* in, float* out, int64_t n, int row, const int32_t* node_pose,
                       int32_t* err, cudaStream_t st) {
   if (n <= 0) return FS_OK;

@@ -123,15 +123,45 @@ def batch_from_arrays(positions, elements, roles, atom_off, device=None,
                      max_pose_atoms=max(maxn, 1), n_nodes=int(nodes.sum()), **kw)
 
 
+_STAGE = threading.local()
+
+
+def _pinned(name, numel, dtype):
+    """Per-thread pinned host staging buffer (grown on demand)."""
+    buf = getattr(_STAGE, name, None)
+    if buf is None or buf.numel() < numel:
+        buf = torch.empty(max(int(numel * 1.25), 1024), dtype=dtype).pin_memory()
+        setattr(_STAGE, name, buf)
+    return buf
+
+
 def batch_from_complexes(complexes, device=None) -> PoseBatch:
-    """SyntheticComplex-like objects (positions/elements/roles) -> PoseBatch."""
-    pos = [np.asarray(c.positions, dtype=np.float64).reshape(-1, 3) for c in complexes]
-    off = np.cumsum([0] + [len(p) for p in pos]).astype(np.int64)
-    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt)  # noqa: E731
-    return batch_from_arrays(np.concatenate(pos) if pos else np.zeros((0, 3)),
-                             cat([np.asarray(c.elements).reshape(-1) for c in complexes], np.int64),
-                             cat([np.asarray(c.roles).reshape(-1) for c in complexes], np.int64),
-                             off, device)
+    """SyntheticComplex-like objects (positions/elements/roles) -> PoseBatch.
+
+    Each complex is copied once, straight into per-thread pinned staging
+    buffers (float64 xyz, int32 element/role; integers outside int32 are
+    clipped, which keeps the reference's element clipping and leaves an
+    invalid role invalid), then uploaded with one asynchronous DMA per array.
+    The staging buffers are reused by the thread's next call, which the
+    caller orders after this batch's scores are read back."""
+    dev = _require_cuda(device)
+    counts = np.fromiter((len(c.positions) for c in complexes), dtype=np.int64, count=len(complexes))
+    off = np.zeros(len(complexes) + 1, dtype=np.int64)
+    np.cumsum(counts, out=off[1:])
+    A = int(off[-1])
+    h_xyz = _pinned("xyz", 3 * A, torch.float64)[: 3 * A]
+    h_el = _pinned("elem", A, torch.int32)[:A]
+    h_ro = _pinned("role", A, torch.int32)[:A]
+    x, e_, r_ = h_xyz.numpy().reshape(-1, 3), h_el.numpy(), h_ro.numpy()
+    lo, hi = np.iinfo(np.int32).min, np.iinfo(np.int32).max
+    for c, a, b in zip(complexes, off[:-1], off[1:]):
+        x[a:b] = c.positions
+        np.clip(c.elements, lo, hi, out=e_[a:b], casting="unsafe")
+        np.clip(c.roles, lo, hi, out=r_[a:b], casting="unsafe")
+    maxn = int(counts.max()) if len(counts) else 1
+    return PoseBatch(atom_xyz=h_xyz.to(dev, non_blocking=True).view(-1, 3),
+                     atom_elem=h_el.to(dev, non_blocking=True), atom_role=h_ro.to(dev, non_blocking=True),
+                     atom_off=torch.from_numpy(off).to(dev), max_pose_atoms=max(maxn, 1), n_nodes=A)
 
 
 def node_offsets(batch: PoseBatch) -> torch.Tensor:
@@ -458,8 +488,13 @@ class DeviceModel:
         return out
 
     def score_features(self, n_poses, grids=None, feats=None, node_off=None, cov_edges=None,
-                       ncov_edges=None, heads=7, precision="fp32"):
-        """Pre-featurized batch (drop-in predict_batch / head forwards)."""
+                       ncov_edges=None, heads=7, precision="fp32", max_pose_nodes=None):
+        """Pre-featurized batch (drop-in predict_batch / head forwards).
+        ``max_pose_nodes``: the largest pose's node count (read from node_off
+        when not given)."""
+        if max_pose_nodes is None:
+            max_pose_nodes = int((node_off[1:] - node_off[:-1]).max().item()) if node_off is not None and \
+                node_off.numel() > 1 else 0
         L = N.lib()
         prec = N.PRECISIONS[precision]
         dev = self.device
@@ -468,7 +503,7 @@ class DeviceModel:
         ce = cov_edges if cov_edges is not None else torch.empty((0, 2), dtype=torch.int64, device=dev)
         ne = ncov_edges if ncov_edges is not None else torch.empty((0, 2), dtype=torch.int64, device=dev)
         nc, nn = int(ce.shape[0]), int(ne.shape[0])
-        nbytes = L.fs_features_workspace_bytes(self.handle, P, n_nodes, max(nc, nn), prec)
+        nbytes = L.fs_features_workspace_bytes(self.handle, P, n_nodes, int(max_pose_nodes), max(nc, nn), prec)
         ws = self.workspace(nbytes)
         out = {"err": torch.empty(P, dtype=torch.int32, device=dev),
                "scores": torch.empty(P, dtype=torch.float32, device=dev),
@@ -479,6 +514,7 @@ class DeviceModel:
         ce_p = ce if nc else torch.empty(2, dtype=torch.int64, device=dev)
         ne_p = ne if nn else torch.empty(2, dtype=torch.int64, device=dev)
         N.check(L.fs_score_features(self.handle, prec, P, _ptr(grids), _ptr(feats), _ptr(node_off), n_nodes,
+                                    int(max_pose_nodes),
                                     _ptr(ce_p), nc, _ptr(ne_p), nn, heads, _ptr(ws), ws.numel(),
                                     _ptr(out["scores"]), _ptr(out["lat_v"]), _ptr(out["lat_g"]),
                                     _ptr(out["pred_v"]), _ptr(out["pred_g"]), _ptr(out["err"]), _stream()),

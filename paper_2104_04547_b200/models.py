@@ -236,7 +236,7 @@ def _pack_graphs(graphs):
             return np.zeros((0, 2), dtype=np.int64)
         e = np.concatenate(parts)
         n_of = np.repeat(counts, sizes)
-        bad = (e.min(axis=1) < 0) | (e.max(axis=1) >= n_of)
+        bad = (np.minimum(e[:, 0], e[:, 1]) < 0) | (np.maximum(e[:, 0], e[:, 1]) >= n_of)
         if bad.any():
             g = int(np.searchsorted(np.cumsum(sizes), int(np.flatnonzero(bad)[0]), side="right"))
             raise ValueError(f"{attr} index out of range for a graph of {int(counts[g])} nodes")
@@ -372,16 +372,6 @@ class FusionModel:
             setattr(self._tls, name, buf)
         return buf
 
-    def _upload(self, name, a):
-        """Host array -> device through a per-thread pinned staging buffer
-        (one DMA; the caller synchronises before the buffer is reused)."""
-        import torch
-        a = np.ascontiguousarray(a)
-        t = torch.from_numpy(a)
-        buf = self._pinned(name, t.numel(), t.dtype)[: t.numel()].view(t.shape)
-        buf.copy_(t)
-        return buf.to("cuda", non_blocking=True)
-
     def _upload_grids(self, items, valid):
         import torch
         shape = (len(valid), self.voxel_cfg.in_channels) + (self.voxel_cfg.grid_extent,) * 3
@@ -391,6 +381,44 @@ class FusionModel:
         for slot, i in enumerate(valid):          # one host copy per grid, straight into pinned memory
             np.copyto(host[slot], items[i][0].occupancy, casting="unsafe")
         return buf.to("cuda", non_blocking=True)
+
+    def _upload_graphs(self, graphs):
+        """Node features and both edge lists of a batch, each graph copied once
+        into pinned staging buffers and uploaded; the block-diagonal lift to
+        global node ids (batch_graphs, models.py:233-256) runs on the device.
+        Returns (feats, node_off, cov_edges, ncov_edges, host node_off)."""
+        import torch
+        G = len(graphs)
+        feats_l = [np.asarray(g.node_features) for g in graphs]
+        ce_l = [np.asarray(g.covalent_edges).reshape(-1, 2) for g in graphs]
+        ne_l = [np.asarray(g.noncovalent_edges).reshape(-1, 2) for g in graphs]
+        counts = np.fromiter((len(f) for f in feats_l), dtype=np.int64, count=G)
+        off = np.zeros(G + 1, dtype=np.int64)
+        np.cumsum(counts, out=off[1:])
+        F = self.graph_cfg.feature_width
+        out = [None, None, None]
+        for slot, (name, parts, width, dt) in enumerate((("feats", feats_l, F, torch.float64),
+                                                         ("ce", ce_l, 2, torch.int64), ("ne", ne_l, 2, torch.int64))):
+            sizes = np.fromiter((len(x) for x in parts), dtype=np.int64, count=G)
+            rows = int(sizes.sum())
+            buf = self._pinned(name, max(rows, 1) * width, dt)[: rows * width]
+            host = buf.numpy().reshape(rows, width)
+            r = 0
+            for k, x in enumerate(parts):
+                n = len(x)
+                if n:
+                    if slot and (x.min() < 0 or x.max() >= counts[k]):
+                        attr = "covalent_edges" if slot == 1 else "noncovalent_edges"
+                        raise ValueError(f"{attr} index out of range for a graph of {int(counts[k])} nodes")
+                    host[r:r + n] = x
+                r += n
+            dev = buf.to("cuda", non_blocking=True).view(rows, width)
+            if slot and rows:          # pose-local -> global node ids on device
+                base = torch.from_numpy(off[:-1]).to("cuda", non_blocking=True)
+                rep = torch.from_numpy(sizes).to("cuda", non_blocking=True)
+                dev = dev + torch.repeat_interleave(base, rep, output_size=rows)[:, None]
+            out[slot] = dev if rows else torch.zeros((0, width), dtype=dt, device="cuda")
+        return out[0], torch.from_numpy(off).to("cuda", non_blocking=True), out[1], out[2], off
 
     def predict_batch(self, items, batch_seed: int = 0):
         """Scores (VoxelGrid, ComplexGraph) pairs (models.py:470-498).
@@ -412,12 +440,11 @@ class FusionModel:
                 errors.append((i, reason))
         if not valid:
             return preds, errors
-        feats, off, ce, ne = _pack_graphs([items[i][1] for i in valid])
+        feats, node_off, ce, ne, off = self._upload_graphs([items[i][1] for i in valid])
         dm = self.device_model()
-        out = dm.score_features(len(valid), grids=self._upload_grids(items, valid),
-                                feats=self._upload("feats", feats), node_off=self._upload("off", off),
-                                cov_edges=self._upload("ce", ce), ncov_edges=self._upload("ne", ne), heads=7,
-                                precision=self.precision)
+        out = dm.score_features(len(valid), grids=self._upload_grids(items, valid), feats=feats, node_off=node_off,
+                                cov_edges=ce, ncov_edges=ne, heads=7, precision=self.precision,
+                                max_pose_nodes=int(np.diff(off).max()))
         scores = out["scores"].cpu().numpy().astype(np.float64)
         err = out["err"].cpu().numpy()
         from . import _native as N
@@ -569,7 +596,8 @@ def graph_head_forward(params: dict, cfg: GraphHeadConfig, graphs, training: boo
     feats, off, ce, ne = _pack_graphs(graphs)
     dm = _head_model(gcfg=cfg, gparams=params, precision=precision)
     out = dm.score_features(len(graphs), feats=_to_dev(feats), node_off=_to_dev(off), cov_edges=_to_dev(ce),
-                            ncov_edges=_to_dev(ne), heads=2, precision=precision)
+                            ncov_edges=_to_dev(ne), heads=2, precision=precision,
+                            max_pose_nodes=int(np.diff(off).max()) if len(off) > 1 else 0)
     if int(out["err"].abs().sum().item()):
         raise GraphError("non-finite values in array")
     return (out["pred_g"].cpu().numpy().astype(np.float64),
