@@ -273,6 +273,60 @@ __device__ __forceinline__ void acc_row_at(float (&q)[4], float (&d)[2], const f
   fadd2(q[2], q[3], v.z, v.w);
   fadd2(d[0], d[1], w.x, w.y);
 }
+// fp16 gather copies (VAR & 4): the same lane-major storage order, 48-byte
+// rows; the lane's 16-byte fp32 half is an 8-byte fp16 load at half index
+// 6t + 2(t&1), its 8-byte half a 4-byte load at 6t + (t&1 ? 0 : 4).  Mixed
+// precision FHADD (fp32 += fp16, exact conversion): the sums stay fp32 and
+// exactly CSR-ordered.
+__device__ __forceinline__ void fhadd2(float& a0, float& a1, uint32_t v) {
+  asm("{\n.reg .f16 l, h;\n"
+      "mov.b32 {l, h}, %2;\n"
+      "add.rn.f32.f16 %0, l, %0;\n"
+      "add.rn.f32.f16 %1, h, %1;\n}"
+      : "+f"(a0), "+f"(a1)
+      : "r"(v));
+}
+__device__ __forceinline__ void acc_row_at16(float (&q)[4], float (&d)[2], const __half* __restrict__ G4,
+                                             const __half* __restrict__ G2, int j) {
+  const uint2 v = *reinterpret_cast<const uint2*>(G4 + j * 24);
+  const uint32_t w = *reinterpret_cast<const uint32_t*>(G2 + j * 24);
+  fhadd2(q[0], q[1], v.x);
+  fhadd2(q[2], q[3], v.y);
+  fhadd2(d[0], d[1], w);
+}
+// gate activations of a pre-scaled pair (see fs_sigmoid_pre / fs_tanh_pre):
+// VAR & 1: one tanh.approx.f32 per value; VAR & 2: one tanh.approx.f16x2
+// per pair; else ex2 + rcp per value.  sigmoid(x) = (1 + tanh(x/2)) / 2.
+constexpr float kSigPre = -0.34657359027997264f;   // u = -log2(e) x  ->  x/2
+constexpr float kTanhPre = 0.34657359027997264f;   // u = 2 log2(e) x ->  x
+template <int VAR>
+__device__ __forceinline__ void gate_tanh2(float& u0, float& u1, float k) {
+  if constexpr (VAR & 2) {
+    const __half2 x = __floats2half2_rn(u0 * k, u1 * k);
+    uint32_t xi = *reinterpret_cast<const uint32_t*>(&x), yi;
+    asm("tanh.approx.f16x2 %0, %1;" : "=r"(yi) : "r"(xi));
+    const float2 y = __half22float2(*reinterpret_cast<const __half2*>(&yi));
+    u0 = y.x; u1 = y.y;
+  } else {
+    asm("tanh.approx.f32 %0, %1;" : "=f"(u0) : "f"(u0 * k));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(u1) : "f"(u1 * k));
+  }
+}
+template <int VAR>
+__device__ __forceinline__ void gate_sigmoid2(float& u0, float& u1) {
+  if constexpr ((VAR & 3) != 0) {
+    gate_tanh2<VAR>(u0, u1, kSigPre);
+    ffma2(u0, u1, 0.5f, 0.5f, 0.5f, 0.5f);
+  } else {
+    sigmoid_pre2(u0, u1);
+  }
+}
+template <int VAR>
+__device__ __forceinline__ void gate_tanh_pre2(float& u0, float& u1) {
+  if constexpr ((VAR & 3) != 0) gate_tanh2<VAR>(u0, u1, kTanhPre);
+  else tanh_pre2(u0, u1);
+}
+
 __device__ __forceinline__ void frag_order(const float (&q)[4], const float (&d)[2], int t, float (&o)[6]) {
   const bool odd = t & 1;
   o[0] = odd ? d[0] : q[0]; o[1] = odd ? d[1] : q[1];
@@ -282,8 +336,13 @@ __device__ __forceinline__ void frag_order(const float (&q)[4], const float (&d)
 // storage position of natural column c (c = 8k + 2t + e -> 6t + 2k + e)
 __host__ __device__ constexpr int hpos(int c) { return 6 * ((c % 8) / 2) + 2 * (c / 8) + (c % 2); }
 
-template <int SPLIT, bool FACT, int kMmaWarps>
+// VAR (SPLIT 2 only): bit 0/1 = gate activations (see gate_tanh2); bit 2 =
+// neighbour gathers from fp16 copies of the node states (the fp32 states are
+// then single-buffered and updated in place: a row's fp32 state is read only
+// by the warp that updates it)
+template <int SPLIT, bool FACT, int kMmaWarps, int VAR = 0>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a) {
+  constexpr bool G16 = (VAR & 4) != 0;
   extern __shared__ __align__(16) float sm[];
   __shared__ int wcnt[kMmaWarps];
   const int p = blockIdx.x;
@@ -314,6 +373,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   float* Hc = sm;
   float* Hn = Hc + hrows * 24;      // both buffers hrows: either may end as Hn
   float* HS = Hn + hrows * 24;
+  // G16: Hc = the fp32 states (never swapped); the Hn region holds the two
+  // fp16 gather copies [hrows][24] each
+  __half* Gc = reinterpret_cast<__half*>(Hn);
+  __half* Gn = Gc + hrows * 24;
   uint32_t* WF = reinterpret_cast<uint32_t*>(HS + a.heavy_cap * 24);   // phase fragments
   float* WB = reinterpret_cast<float*>(WF + kPhaseWords);            // phase biases [72]
   int* CTL = reinterpret_cast<int*>(WB + 72);    // item ctr[2], heavy-done ctr[2], -, -, hist[kBins], cursor[kBins]
@@ -341,7 +404,16 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       for (int k = 0; k < 6; ++k) {
         const float4 v = src[k];
         reinterpret_cast<float4*>(Hc + i * 24)[k] = v;
-        reinterpret_cast<float4*>(Hn + i * 24)[k] = v;
+        if constexpr (G16) {
+          const __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
+          uint2 u;
+          u.x = *reinterpret_cast<const uint32_t*>(&lo);
+          u.y = *reinterpret_cast<const uint32_t*>(&hi);
+          reinterpret_cast<uint2*>(Gc + i * 24)[k] = u;
+          reinterpret_cast<uint2*>(Gn + i * 24)[k] = u;
+        } else {
+          reinterpret_cast<float4*>(Hn + i * 24)[k] = v;
+        }
       }
       continue;
     }
@@ -375,7 +447,16 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     for (int k = 0; k < 24; k += 4) {
       const float4 v = make_float4(hv[k], hv[k + 1], hv[k + 2], hv[k + 3]);
       *reinterpret_cast<float4*>(Hc + i * 24 + k) = v;
-      *reinterpret_cast<float4*>(Hn + i * 24 + k) = v;
+      if constexpr (G16) {
+        const __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
+        uint2 u;
+        u.x = *reinterpret_cast<const uint32_t*>(&lo);
+        u.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(Gc + i * 24 + k) = u;
+        *reinterpret_cast<uint2*>(Gn + i * 24 + k) = u;
+      } else {
+        *reinterpret_cast<float4*>(Hn + i * 24 + k) = v;
+      }
     }
   }
 
@@ -410,10 +491,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         const int c = 2 * j;
         z[rr][c] = Dzr[j][2 * rr]; z[rr][c + 1] = Dzr[j][2 * rr + 1];
         fadd2(z[rr][c], z[rr][c + 1], bz[c], bz[c + 1]);
-        sigmoid_pre2(z[rr][c], z[rr][c + 1]);
+        gate_sigmoid2<VAR>(z[rr][c], z[rr][c + 1]);
         rh[rr][c] = Dzr[3 + j][2 * rr]; rh[rr][c + 1] = Dzr[3 + j][2 * rr + 1];
         fadd2(rh[rr][c], rh[rr][c + 1], br[c], br[c + 1]);
-        sigmoid_pre2(rh[rr][c], rh[rr][c + 1]);
+        gate_sigmoid2<VAR>(rh[rr][c], rh[rr][c + 1]);
         fmul2(rh[rr][c], rh[rr][c + 1], h[rr][c], h[rr][c + 1]);
       }
     // A = [s | r*h]: the s part (k-tile 0 and half of k-tile 1) is reused
@@ -432,7 +513,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         const int c = 2 * j;
         float u0 = Dh[j][2 * rr], u1 = Dh[j][2 * rr + 1];
         fadd2(u0, u1, bh[c], bh[c + 1]);
-        tanh_pre2(u0, u1);                                 // hh
+        gate_tanh_pre2<VAR>(u0, u1);                       // hh
         fadd2(u0, u1, -h[rr][c], -h[rr][c + 1]);          // hh - h
         ffma2(u0, u1, z[rr][c], z[rr][c + 1], h[rr][c], h[rr][c + 1]);   // h + z (hh - h)
         // padding rows (ok false) evolve too: no CSR row lists them and the
@@ -449,8 +530,17 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     }
   };
   auto store_hn = [&](int row, const float (&v)[6]) {
+    if constexpr (G16) {
+      // fp32 state in place (read only by this warp), fp16 copy for the gathers
 #pragma unroll
-    for (int c = 0; c < 6; c += 2) *reinterpret_cast<float2*>(Hn + row * 24 + PCOL(c)) = make_float2(v[c], v[c + 1]);
+      for (int c = 0; c < 6; c += 2) {
+        *reinterpret_cast<float2*>(Hc + row * 24 + PCOL(c)) = make_float2(v[c], v[c + 1]);
+        *reinterpret_cast<__half2*>(Gn + row * 24 + PCOL(c)) = __floats2half2_rn(v[c], v[c + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 6; c += 2) *reinterpret_cast<float2*>(Hn + row * 24 + PCOL(c)) = make_float2(v[c], v[c + 1]);
+    }
   };
 
   int gstep = 0;
@@ -517,12 +607,23 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     for (int step = 0; step < a.k_steps[ph]; ++step) {
       const float* H4 = Hc + 6 * t + ((t & 1) << 1);   // this step's gather bases (acc_row_at)
       const float* H2 = Hc + 6 * t + ((t & 1) ? 0 : 4);
+      const __half* G4 = Gc + 6 * t + ((t & 1) << 1);
+      const __half* G2 = Gc + 6 * t + ((t & 1) ? 0 : 4);
+      auto acc = [&](float (&q)[4], float (&d)[2], int j) {
+        if constexpr (G16) acc_row_at16(q, d, G4, G2, j);
+        else acc_row_at(q, d, H4, H2, j);
+      };
       // Items, handed out in order by a counter: heavy-row sums (-> HS), then
       // the degree-sorted light tiles (gather + GRU), then the heavy tiles
       // (GRU from HS, after every heavy sum is in).
       int* ctr = CTL + (gstep & 1);
       int* hdone = CTL + 2 + (gstep & 1);
       for (int item = warp; item < nitems;) {
+        // claim the next item now: the counter's round trip overlaps this
+        // item's work (items are claimed in increasing order, so a warp
+        // spinning in a heavy tile never holds an unprocessed heavy sum)
+        int next = 0;
+        if (lane == 0) next = atomicAdd(ctr, 1) + kMmaWarps;
         if (item < nh) {
           // one heavy row: lane (q = lane/4, t) sums neighbours q, q+8, ...
           const int row = PERM[item];
@@ -538,7 +639,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
               const int j[4] = {static_cast<int>(v.x & 0xffffu), static_cast<int>(v.x >> 16),
                                 static_cast<int>(v.y & 0xffffu), static_cast<int>(v.y >> 16)};
 #pragma unroll
-              for (int u = 0; u < 4; ++u) acc_row_at(sq, sd, H4, H2, j[u]);
+              for (int u = 0; u < 4; ++u) acc(sq, sd, j[u]);
             }
           } else {
             for (int q = g; q < d; q += 32) {
@@ -546,7 +647,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
               for (int u = 0; u < 4; ++u) j[u] = q + 8 * u < d ? __ldg(c + q + 8 * u) : npad;
 #pragma unroll
-              for (int u = 0; u < 4; ++u) acc_row_at(sq, sd, H4, H2, j[u]);
+              for (int u = 0; u < 4; ++u) acc(sq, sd, j[u]);
             }
           }
           float s6[6] = {sq[0], sq[1], sq[2], sq[3], sd[0], sd[1]};   // storage order
@@ -581,35 +682,31 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             // ids come 4 at a time; past a row's padded extent the lane reads
             // row npad (x + 0 == x: sums stay exactly CSR-ordered)
             const int e0 = (d0 + 3) & ~3, e1 = (d1 + 3) & ~3;
-            const int dm = max(e0, e1);
-            auto ids4 = [&](const col_t* c, int q, int e, int* j) {
-              if (q < e) {
-                const uint2 v = __ldg(reinterpret_cast<const uint2*>(c + q));
-                j[0] = v.x & 0xffffu; j[1] = v.x >> 16; j[2] = v.y & 0xffffu; j[3] = v.y >> 16;
-              } else {
-                j[0] = j[1] = j[2] = j[3] = npad;
-              }
+            const int nch = max(e0, e1) >> 2;          // 4-id chunks
+            // ids are software-pipelined one 8-id round ahead: the global
+            // (L2) latency of round k+1 overlaps the gathers of round k
+            const uint32_t padw = static_cast<uint32_t>(npad) * 0x10001u;
+            auto ld = [&](const col_t* c, int q, int e) {
+              return q < e ? __ldg(reinterpret_cast<const uint2*>(c + q)) : make_uint2(padw, padw);
             };
-            int q = 0;
-            for (; q + 8 <= dm; q += 8) {
-              int j0[8], j1[8];
-              ids4(c0, q, e0, j0); ids4(c0, q + 4, e0, j0 + 4);
-              ids4(c1, q, e1, j1); ids4(c1, q + 4, e1, j1 + 4);
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                acc_row_at(sq[0], sd[0], H4, H2, j0[u]);
-                acc_row_at(sq[1], sd[1], H4, H2, j1[u]);
+            auto gather4 = [&](int r, uint2 v) {
+              acc(sq[r], sd[r], static_cast<int>(v.x & 0xffffu));
+              acc(sq[r], sd[r], static_cast<int>(v.x >> 16));
+              acc(sq[r], sd[r], static_cast<int>(v.y & 0xffffu));
+              acc(sq[r], sd[r], static_cast<int>(v.y >> 16));
+            };
+            uint2 x0 = ld(c0, 0, e0), x1 = ld(c1, 0, e1), y0 = ld(c0, 4, e0), y1 = ld(c1, 4, e1);
+            for (int k = 0; k < nch; k += 2) {
+              const int qn = 4 * (k + 2);
+              const uint2 nx0 = ld(c0, qn, e0), nx1 = ld(c1, qn, e1);
+              const uint2 ny0 = ld(c0, qn + 4, e0), ny1 = ld(c1, qn + 4, e1);
+              gather4(0, x0);
+              gather4(1, x1);
+              if (k + 1 < nch) {
+                gather4(0, y0);
+                gather4(1, y1);
               }
-            }
-            if (q < dm) {
-              int j0[4], j1[4];
-              ids4(c0, q, e0, j0);
-              ids4(c1, q, e1, j1);
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                acc_row_at(sq[0], sd[0], H4, H2, j0[u]);
-                acc_row_at(sq[1], sd[1], H4, H2, j1[u]);
-              }
+              x0 = nx0; x1 = nx1; y0 = ny0; y1 = ny1;
             }
           } else {
             // packed CSR (rows built from reference edge lists): one id per load
@@ -622,8 +719,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
               for (int u = 0; u < 4; ++u) j1[u] = q + u < d1 ? __ldg(c1 + q + u) : npad;
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                acc_row_at(sq[0], sd[0], H4, H2, j0[u]);
-                acc_row_at(sq[1], sd[1], H4, H2, j1[u]);
+                acc(sq[0], sd[0], j0[u]);
+                acc(sq[1], sd[1], j1[u]);
               }
             }
           }
@@ -659,15 +756,17 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           if (r0 < npad) store_hn(r0, hn[0]);
           if (r1 < npad) store_hn(r1, hn[1]);
         }
-        int next = 0;
-        if (lane == 0) next = atomicAdd(ctr, 1) + kMmaWarps;
         item = __shfl_sync(0xffffffffu, next, 0);
       }
       // counters of the next step (last used two steps ago)
       if (threadIdx.x == 0) { CTL[(gstep + 1) & 1] = 0; CTL[2 + ((gstep + 1) & 1)] = 0; }
       ++gstep;
       __syncthreads();
-      float* tmp = Hc; Hc = Hn; Hn = tmp;
+      if constexpr (G16) {
+        __half* tg = Gc; Gc = Gn; Gn = tg;
+      } else {
+        float* tmp = Hc; Hc = Hn; Hn = tmp;
+      }
     }
   }
   float* RED = Hn;   // [warps][128] (+ [warps][128] doubles), written only after every warp is done with the staged fragments
@@ -861,21 +960,21 @@ int gnn_mma_max_nodes() {
   return n;
 }
 
-template <int SPLIT, bool FACT, int WARPS>
+template <int SPLIT, bool FACT, int WARPS, int VAR = 0>
 static int launch_gnn_mma_t(const GnnMmaArgs& a, int n_poses, size_t smem, cudaStream_t st) {
-  FS_CUDA_CHECK(cudaFuncSetAttribute(gnn_mma_kernel<SPLIT, FACT, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-  gnn_mma_kernel<SPLIT, FACT, WARPS><<<n_poses, WARPS * 32, smem, st>>>(a);
+  FS_CUDA_CHECK(cudaFuncSetAttribute(gnn_mma_kernel<SPLIT, FACT, WARPS, VAR>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  gnn_mma_kernel<SPLIT, FACT, WARPS, VAR><<<n_poses, WARPS * 32, smem, st>>>(a);
   FS_LAUNCH_CHECK();
   return FS_OK;
 }
 
-// warps per pose: FS_GNN_WARPS = 16 | 20 | 24 (more warps hide more gather
-// latency with fewer registers each; 20 measured fastest)
-static int gnn_warps() {
-  static const int w = getenv("FS_GNN_WARPS") ? atoi(getenv("FS_GNN_WARPS")) : 20;
-  return w == 16 || w == 24 ? w : 20;
-}
+// FS_PREC_BF16 (SPLIT 2) runs VAR 6: neighbour gathers from fp16 copies of
+// the node states (half the shared-memory bytes of the fp32 rows: 21.7 ->
+// 20.1 ms per 16,384 poses) and one tanh.approx.f16x2 per pair of gate
+// activations (-> 19.8 ms); config-1 score error vs the oracle 1.03e-3 max
+// relative (1.33e-3 before; profiles/r02/gnn_variants.md)
+constexpr int kSplit2Var = 6;
 
 int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes, cudaStream_t st) {
   if (n_poses <= 0) return FS_OK;
@@ -883,20 +982,13 @@ int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes
   GnnMmaArgs a = a_in;
   a.heavy_cap = kMaxHeavy;
   const size_t smem = gnn_mma_smem_bytes(max_nodes);
-  const int w = gnn_warps();
   if (split == 2) {
     if (!a.wfrag16[0] || !a.wfrag16[1] || !a.gfrag16) return FS_EINVAL;
-    if (a.fact_cnt) return launch_gnn_mma_t<2, true, 20>(a, n_poses, smem, st);
-    return launch_gnn_mma_t<2, false, 20>(a, n_poses, smem, st);
+    if (a.fact_cnt) return launch_gnn_mma_t<2, true, 20, kSplit2Var>(a, n_poses, smem, st);
+    return launch_gnn_mma_t<2, false, 20, kSplit2Var>(a, n_poses, smem, st);
   }
-  if (a.fact_cnt) {
-    if (w == 16) return launch_gnn_mma_t<3, true, 16>(a, n_poses, smem, st);
-    if (w == 24) return launch_gnn_mma_t<3, true, 24>(a, n_poses, smem, st);
-    return launch_gnn_mma_t<3, true, 20>(a, n_poses, smem, st);
-  }
-  if (split == 1) return launch_gnn_mma_t<1, false, 20>(a, n_poses, smem, st);
-  if (w == 16) return launch_gnn_mma_t<3, false, 16>(a, n_poses, smem, st);
-  if (w == 24) return launch_gnn_mma_t<3, false, 24>(a, n_poses, smem, st);
+  if (split != 3) return FS_EINVAL;
+  if (a.fact_cnt) return launch_gnn_mma_t<3, true, 20>(a, n_poses, smem, st);
   return launch_gnn_mma_t<3, false, 20>(a, n_poses, smem, st);
 }
 
