@@ -13,13 +13,14 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libfusionb200.so")
+_BOUNDS = bool(os.environ.get("FS_BOUNDS"))     # device-side index checks: a separate debug library
+BUILD = os.path.join(HERE, "_build_bounds" if _BOUNDS else "_build")
+LIB = os.path.join(HERE, "libfusionb200_bounds.so" if _BOUNDS else "libfusionb200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", INCLUDE, "-I", CSRC]
-if os.environ.get("FS_BOUNDS"):            # device-side index checks (debug builds only)
+if _BOUNDS:
     FLAGS.append("-DFS_BOUNDS")
 
 

@@ -22,7 +22,13 @@
 namespace fs {
 
 static thread_local std::string g_last_cuda_error;
-void set_cuda_error(cudaError_t e) { g_last_cuda_error = cudaGetErrorString(e); }
+void set_cuda_error(cudaError_t e, const char* file, int line) {
+  g_last_cuda_error = cudaGetErrorString(e);
+  if (file) {
+    const char* base = strrchr(file, '/');
+    g_last_cuda_error += std::string(" at ") + (base ? base + 1 : file) + ":" + std::to_string(line);
+  }
+}
 
 static std::atomic<long long> g_launches{0};
 void count_launch(const char* file, int line) {

@@ -10,13 +10,14 @@
 
 namespace fs {
 
-// Record the last CUDA error per host thread (reported by fs_last_cuda_error).
-void set_cuda_error(cudaError_t e);
+// Record the last CUDA error per host thread (reported by fs_last_cuda_error),
+// with the library source site that saw it.
+void set_cuda_error(cudaError_t e, const char* file = nullptr, int line = 0);
 
 #define FS_CUDA_CHECK(expr)                                   \
   do {                                                        \
     cudaError_t _e = (expr);                                  \
-    if (_e != cudaSuccess) { ::fs::set_cuda_error(_e); return FS_ECUDA; } \
+    if (_e != cudaSuccess) { ::fs::set_cuda_error(_e, __FILE__, __LINE__); return FS_ECUDA; } \
   } while (0)
 
 // Pose-local neighbour ids of the scoring-path CSR (FS_MAX_POSE_ATOMS < 2^16):

@@ -530,6 +530,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     }
   };
   auto store_hn = [&](int row, const float (&v)[6]) {
+    FS_DCHECK(row >= 0 && row < npad, "gnn state row", row, npad);
     if constexpr (G16) {
       // fp32 state in place (read only by this warp), fp16 copy for the gathers
 #pragma unroll
@@ -610,6 +611,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       const __half* G4 = Gc + 6 * t + ((t & 1) << 1);
       const __half* G2 = Gc + 6 * t + ((t & 1) ? 0 : 4);
       auto acc = [&](float (&q)[4], float (&d)[2], int j) {
+        FS_DCHECK(j >= 0 && j <= npad, "gnn gather row", j, npad);
         if constexpr (G16) acc_row_at16(q, d, G4, G2, j);
         else acc_row_at(q, d, H4, H2, j);
       };
@@ -660,6 +662,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             s6[k] = v;
           }
           if (g == 0) {
+            FS_DCHECK(item < a.heavy_cap, "gnn heavy slot", item, a.heavy_cap);
             float* b = HS + item * 24 + 6 * t;
             *reinterpret_cast<float4*>(b + ((t & 1) << 1)) = make_float4(s6[0], s6[1], s6[2], s6[3]);
             *reinterpret_cast<float2*>(b + ((t & 1) ? 0 : 4)) = make_float2(s6[4], s6[5]);

@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     const int kp = keys[i];
     const int slot = atomicAdd(&cell_start[(kp >> 12) * NC + (((kp >> 8) & 15) * nca + ((kp >> 4) & 15)) * nca +
                                            (kp & 15)], 1);   // becomes the cell end
+    FS_DCHECK(slot < n, "graph cell slot", slot, n);
     cell_list[slot] = (uint16_t)i;
   }
   __syncthreads();
@@ -574,6 +575,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         if (hit) {
           const int o = w + __popc(m & ((1u << lane) - 1u));
           const int j = Llist[lj];
+          FS_DCHECK(o < a.cap, "graph ncov S fill", o, a.cap);
           coln[o] = j;
           if (DIST) { double d; exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
         }
@@ -590,6 +592,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
           const int b = __ffs(bits) - 1;
           bits &= bits - 1;
           const int j = Slist[32 * w + b];
+          FS_DCHECK(o < a.cap, "graph ncov L fill", o, a.cap);
           coln[o] = j;
           if (DIST) { double d; exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
           ++o;
@@ -659,6 +662,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
             c += __ffs(w) - 1;
             if (c >= cend) break;
             const int j = cell_list[qb + (c - c0)];
+            FS_DCHECK(o < a.cap, "graph cov fill", o, a.cap);
             if (j != i) colc[o++] = (col_t)j;
             ++c;
           }

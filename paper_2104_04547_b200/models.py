@@ -420,8 +420,32 @@ class FusionModel:
             out[slot] = dev if rows else torch.zeros((0, width), dtype=dt, device="cuda")
         return out[0], torch.from_numpy(off).to("cuda", non_blocking=True), out[1], out[2], off
 
+    def _thread_stream(self):
+        """Each host thread scores on its own CUDA stream, so the reference's
+        campaign driver -- which calls the scorer plugin from a thread pool
+        (harness.py:374-376) -- overlaps its batches on the GPU; the packed
+        weights are read-only, workspaces and staging buffers are per thread."""
+        import torch
+        st = getattr(self._tls, "stream", None)
+        if st is None or st.device.index != torch.cuda.current_device():
+            st = torch.cuda.Stream()
+            self._tls.stream = st
+        return torch.cuda.stream(st)
+
     def predict_batch(self, items, batch_seed: int = 0):
         """Scores (VoxelGrid, ComplexGraph) pairs (models.py:470-498).
+
+        Returns (predictions, errors); malformed items never abort the batch.
+        Items may be this package's featurizer output, the reference's
+        (fusionscreen.complexes.VoxelGrid / ComplexGraph) or any objects with
+        the same attributes.  ``batch_seed`` only seeds dropout in the
+        reference's eval tape, where dropout is the identity, so it does not
+        change results."""
+        with self._thread_stream():
+            return self._predict_batch(items)
+
+    def _predict_batch(self, items):
+        """predict_batch on the calling thread's stream.
 
         Returns (predictions, errors); malformed items never abort the batch.
         Items may be this package's featurizer output, the reference's
@@ -493,9 +517,11 @@ class FusionModel:
         package's or the reference's SyntheticComplex (duck-typed).  Returns
         (scores float64 [P], err int32 [P])."""
         from .engine import batch_from_complexes
-        b = batch_from_complexes(complexes)
-        out = self.device_model().score_poses(b, self.precision)
-        return out["scores"].cpu().numpy().astype(np.float64), out["err"].cpu().numpy()
+        dm = self.device_model()
+        with self._thread_stream():
+            b = batch_from_complexes(complexes)
+            out = dm.score_poses(b, self.precision)
+            return out["scores"].cpu().numpy().astype(np.float64), out["err"].cpu().numpy()
 
     # -- parameter bookkeeping (models.py:532-568) -----------------------------
     def all_params(self) -> dict:
