@@ -332,7 +332,7 @@ def plugin_legs(model_prec, dev):
         atoms = sum(len(c.positions) for c in complexes[:bs])
         out[f"model_scorer_raw_b{bs}"] = {
             "value": rate, "unit": "poses/s", "poses": n,
-            "h2d_bytes_per_call": int(atoms * (24 + 4 + 4) + (bs + 1) * 8), "d2h_bytes_per_call": 8 * bs + 4 * bs,
+            "h2d_bytes_per_call": int(atoms * (24 + 8 + 8) + (bs + 1) * 8), "d2h_bytes_per_call": 4 * bs + 4 * bs,
             "source": "harness.ModelScorer(list[PoseRecord]) with SyntheticComplex payloads (host numpy "
                       "vstack([pocket, ligand])), featurized on device in the call; wall clock incl. host work"}
     # the caller the reference actually uses: run_campaign drives the plugin

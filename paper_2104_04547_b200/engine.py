@@ -139,28 +139,31 @@ def batch_from_complexes(complexes, device=None) -> PoseBatch:
     """SyntheticComplex-like objects (positions/elements/roles) -> PoseBatch.
 
     Each complex is copied once, straight into per-thread pinned staging
-    buffers (float64 xyz, int32 element/role; integers outside int32 are
-    clipped, which keeps the reference's element clipping and leaves an
-    invalid role invalid), then uploaded with one asynchronous DMA per array.
-    The staging buffers are reused by the thread's next call, which the
-    caller orders after this batch's scores are read back."""
+    buffers (float64 xyz; elements and roles as int64, a plain copy of the
+    reference's integer arrays), uploaded with one asynchronous DMA per
+    array, and narrowed to int32 on the device with values clipped to the
+    int32 range (which keeps the reference's element clipping and leaves an
+    invalid role invalid).  The staging buffers are reused by the thread's
+    next call, which the caller orders after this batch's scores are read
+    back."""
     dev = _require_cuda(device)
     counts = np.fromiter((len(c.positions) for c in complexes), dtype=np.int64, count=len(complexes))
     off = np.zeros(len(complexes) + 1, dtype=np.int64)
     np.cumsum(counts, out=off[1:])
     A = int(off[-1])
     h_xyz = _pinned("xyz", 3 * A, torch.float64)[: 3 * A]
-    h_el = _pinned("elem", A, torch.int32)[:A]
-    h_ro = _pinned("role", A, torch.int32)[:A]
+    h_el = _pinned("elem", A, torch.int64)[:A]
+    h_ro = _pinned("role", A, torch.int64)[:A]
     x, e_, r_ = h_xyz.numpy().reshape(-1, 3), h_el.numpy(), h_ro.numpy()
-    lo, hi = np.iinfo(np.int32).min, np.iinfo(np.int32).max
     for c, a, b in zip(complexes, off[:-1], off[1:]):
         x[a:b] = c.positions
-        np.clip(c.elements, lo, hi, out=e_[a:b], casting="unsafe")
-        np.clip(c.roles, lo, hi, out=r_[a:b], casting="unsafe")
+        e_[a:b] = c.elements
+        r_[a:b] = c.roles
+    lo, hi = np.iinfo(np.int32).min, np.iinfo(np.int32).max
+    d_el = h_el.to(dev, non_blocking=True).clamp_(lo, hi).to(torch.int32)
+    d_ro = h_ro.to(dev, non_blocking=True).clamp_(lo, hi).to(torch.int32)
     maxn = int(counts.max()) if len(counts) else 1
-    return PoseBatch(atom_xyz=h_xyz.to(dev, non_blocking=True).view(-1, 3),
-                     atom_elem=h_el.to(dev, non_blocking=True), atom_role=h_ro.to(dev, non_blocking=True),
+    return PoseBatch(atom_xyz=h_xyz.to(dev, non_blocking=True).view(-1, 3), atom_elem=d_el, atom_role=d_ro,
                      atom_off=torch.from_numpy(off).to(dev), max_pose_atoms=max(maxn, 1), n_nodes=A)
 
 
