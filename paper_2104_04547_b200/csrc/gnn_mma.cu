@@ -442,7 +442,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     }
     float hv[24];   // storage order
 #pragma unroll
-    for (int c = 0; c < 24; ++c) hv[hpos(c)] = emb ? fs_tanh(acc[c]) : 0.f;
+    for (int c = 0; c < 24; ++c) {
+      float th;
+      if constexpr ((VAR & 8) != 0) asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(acc[c]));
+      else th = fs_tanh(acc[c]);
+      hv[hpos(c)] = emb ? th : 0.f;
+    }
 #pragma unroll
     for (int k = 0; k < 24; k += 4) {
       const float4 v = make_float4(hv[k], hv[k + 1], hv[k + 2], hv[k + 3]);
@@ -871,7 +876,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       }
       {
         // rows g (D[0], D[1]) and g+8 (D[2], D[3]), columns 8j+2t, +1
-        if constexpr (SPLIT == 2) {
+        if constexpr ((VAR & 8) != 0) {
+          // one tanh.approx.f16x2 per pair of activations (VAR & 8)
+          gate_sigmoid2<VAR>(Dg[0], Dg[1]);
+          gate_sigmoid2<VAR>(Dg[2], Dg[3]);
+          gate_tanh_pre2<VAR>(Dv[0], Dv[1]);
+          gate_tanh_pre2<VAR>(Dv[2], Dv[3]);
+        } else if constexpr (SPLIT == 2) {
           // one MUFU.TANH per activation (2^-10.7): sigmoid(x) = (1 + tanh(x/2)) / 2
           // with u = -log2(e) x and v = 2 log2(e) x as staged
           constexpr float kG = -0.34657359027997264f, kV = 0.34657359027997264f;   // 1/(2 log2 e)
@@ -984,7 +995,7 @@ static int launch_gnn_mma_t(const GnnMmaArgs& a, int n_poses, size_t smem, cudaS
 // 20.1 ms per 16,384 poses) and one tanh.approx.f16x2 per pair of gate
 // activations (-> 19.8 ms); config-1 score error vs the oracle 1.03e-3 max
 // relative (1.33e-3 before; profiles/r02/gnn_variants.md)
-constexpr int kSplit2Var = 6;
+constexpr int kSplit2Var = 14;
 
 int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes, cudaStream_t st) {
   if (n_poses <= 0) return FS_OK;
