@@ -671,7 +671,7 @@ def main():
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
     stage_ms = stage_sum()
-    bad = int(torch.stack(errs).ne(0).sum().item())
+    bad = int(torch.cat(errs).ne(0).sum().item())
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

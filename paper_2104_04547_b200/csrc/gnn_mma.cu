@@ -995,7 +995,7 @@ static int launch_gnn_mma_t(const GnnMmaArgs& a, int n_poses, size_t smem, cudaS
 // 20.1 ms per 16,384 poses) and one tanh.approx.f16x2 per pair of gate
 // activations (-> 19.8 ms); config-1 score error vs the oracle 1.03e-3 max
 // relative (1.33e-3 before; profiles/r02/gnn_variants.md)
-constexpr int kSplit2Var = 14;
+constexpr int kSplit2Var = 6;
 
 int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes, cudaStream_t st) {
   if (n_poses <= 0) return FS_OK;

@@ -536,7 +536,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       }
     }
     uint32_t* bits = covbits + (size_t)i * kCovWords;
-    bits[0] = w0; bits[1] = w1; bits[2] = w2;
+    bits[0] = w0; bits[1] = w1;
+    if constexpr (kCovWords > 2) bits[kCovWords - 1] = w2;
     if (over || c0 > kCovBits) atomicOr(&ovf[i >> 5], 1u << (i & 31));   // the fill re-tests
     offc[i] = (uint16_t)(cnt - 1);   // minus the row's own atom
   }
