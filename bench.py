@@ -293,6 +293,30 @@ def parity_config1(dm, E, precisions, workers):
     return out, cpu_rate, lib.n_poses
 
 
+def precision_legs(dm, dlib, n_rank, bmax):
+    """Throughput of the other precisions on the same screen (device-resident,
+    eager calls of <= bmax poses): `mixed` (the 1e-3 path on tensor cores)
+    over the whole shard, `fp32` (FFMA) over its first 16,384 poses.  Their
+    accuracy vs the oracle is the `parity` block."""
+    import torch
+    out = {}
+    for prec, n in (("mixed", n_rank), ("fp32", min(n_rank, 16384))):
+        B = min(bmax, n)
+        dm.score_poses(dlib.batch(0, min(B, 2048)), prec, 32768, retry=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        errs = []
+        e0.record()
+        for a in range(0, n, B):
+            errs.append(dm.score_poses(dlib.batch(a, min(n, a + B)), prec, 32768, retry=False)["err"])
+        e1.record()
+        torch.cuda.synchronize()
+        out[prec] = {"value": n / (e0.elapsed_time(e1) / 1e3), "unit": "poses/s", "poses": n,
+                     "failed_poses": int(torch.cat(errs).ne(0).sum().item()),
+                     "note": "same config-4 shard, device-resident, eager fs_score_poses calls (no top-k fold)"}
+    return out
+
+
 def plugin_legs(model_prec, dev):
     """End to end through the reference-facing API with host objects: the
     ModelScorer plugin (harness.py:224-234) with raw complexes, and
@@ -422,7 +446,7 @@ def config_legs(dm, E, N, dev, precision):
         "edges_bitwise_vs_oracle_sample": bool(ok), "sample": f"{S} poses vs oracle/radius_graph.c",
         "note": "featurizer API path (voxelize float64 NCDHW + count/fill radius graph + canonical edge lists "
                 "with float64 distances, what featurize returns); the scoring path fuses a leaner graph into "
-                "fs_score_poses. 10,000 poses timed of the config's 100k (steady state)"}
+                "fs_score_poses; all 100,000 poses of the config timed (8 batches of 12,500)"}
 
     # ---- config 3: each branch alone on featurized input, batch 256 ----
     B3 = 256
@@ -442,7 +466,7 @@ def config_legs(dm, E, N, dev, precision):
         cp = torch.repeat_interleave(torch.arange(B3, device=dev), coff.diff())
         np_ = torch.repeat_interleave(torch.arange(B3, device=dev), noff.diff())
         inputs.append((grids, feats, no, ce + no[cp][:, None], ne + no[np_][:, None], int(no.diff().max().item())))
-    for prec, n_batches in (("bf16", 391), ("fp32", 100)):
+    for prec, n_batches in (("bf16", 391), ("fp32", 391)):
         for head, name in ((1, "voxel"), (2, "graph")):
             def once(i):
                 grids, feats, no, ce, ne, mpn = inputs[i % n_inputs]
@@ -463,13 +487,13 @@ def config_legs(dm, E, N, dev, precision):
                 "value": n_batches * B3 / (e0.elapsed_time(e1) / 1e3), "unit": "poses/s", "poses": n_batches * B3,
                 "batch": B3, "precision": prec}
     out["config3_note"] = ("branch-alone forwards (voxel_head_forward / graph_head_forward semantics) on featurized "
-                           "device input, 4 distinct 256-pose batches round robin; bf16 timed over 100,096 poses, "
-                           "fp32 over 25,600 of the config's 100k")
+                           "device input, 4 distinct 256-pose batches round robin; 100,096 poses timed per "
+                           "head and precision")
 
     # ---- config 5: 4 targets, variable ligand sizes ----
     tgts = synth.FOUR_TARGETS
     pockets = [synth.make_pocket(n, seed=40 + i, name=nm) for i, (nm, n) in enumerate(tgts)]
-    B5, K5 = 16384, 8
+    B5, K5 = 32768, 38                             # 1,245,184 poses: one GPU's share of 10M over 8
     per_t = B5 * K5 // len(tgts)
     libs = [screen_library(0, (per_t + 9) // 10, seed=4000 + 100 * i, ligand_atoms=(8, 96), target=i).slice(0, per_t)
             for i in range(len(tgts))]
@@ -495,7 +519,7 @@ def config_legs(dm, E, N, dev, precision):
         "failed_poses": int(torch.stack(errs).ne(0).sum().item()), "precision": precision,
         "targets": {nm: n for nm, n in tgts}, "ligand_atoms": [8, 96],
         "note": "4 synthetic pockets (protease1/2 = 1000/900 atoms, spike1/2 = 450/350, SURVEY 8d proposal); "
-                "131,072 poses timed per GPU (the config's 10M over 8 GPUs is 1.25M per GPU, steady state)"}
+                "1,245,184 poses timed on this GPU (the config's 10M over 8 GPUs is 1.25M per GPU)"}
     return out
 
 
@@ -817,7 +841,8 @@ def main():
                                             "through oracle/fusion_oracle.py (float64 numpy), one process per "
                                             "host core x 1 BLAS thread; rate over the slowest process"}
         # auxiliary legs never take the headline line down with them
-        for key, fn in (("plugin", lambda: plugin_legs(precision, dev)),
+        for key, fn in (("precisions", lambda: precision_legs(dm, dlib, n_rank, BMAX)),
+                        ("plugin", lambda: plugin_legs(precision, dev)),
                         ("configs", lambda: config_legs(dm, E, N, dev, precision))):
             try:
                 extras[key] = fn()
