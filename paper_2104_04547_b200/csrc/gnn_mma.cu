@@ -21,6 +21,7 @@
 // rows 8 CSR-strided partial sums in a fixed tree), fixed reduction trees,
 // fixed pool order -> a pose's latent is bitwise independent of its batch.
 #include <cstdlib>
+#include <type_traits>
 
 #include <cuda_fp16.h>
 
@@ -184,7 +185,9 @@ __device__ __forceinline__ void mma_f16_c(float (&d)[4], const uint32_t (&a)[4],
         "f"(c[3]));
 }
 
-template <int SPLIT, int NT>
+// KT0 = 1: k-tile 0 (neighbour sums s[0..15]) is all zero and skipped (the
+// products it would add are exact zeros)
+template <int SPLIT, int NT, int KT0 = 0>
 __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[3][4], const uint32_t (&alo)[3][4],
                                        const uint32_t* __restrict__ fhi, const uint32_t* __restrict__ flo,
                                        int lane) {
@@ -193,7 +196,7 @@ __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) D[nt][0] = D[nt][1] = D[nt][2] = D[nt][3] = 0.f;
 #pragma unroll
-  for (int kt = 0; kt < 3; ++kt)
+  for (int kt = KT0; kt < 3; ++kt)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const uint2 bh = *reinterpret_cast<const uint2*>(fhi + ((kt * NT + nt) * 32 + lane) * 2);
@@ -472,7 +475,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   const uint32_t* zr_lo = WF + kZrWords;
   const uint32_t* hh_hi = WF + (SPLIT == 2 ? kZrWords : 2 * kZrWords);
   const uint32_t* hh_lo = WF + 2 * kZrWords + kHhWords;
-  auto gru16 = [&](const float (&sv)[2][6], const float (&h)[2][6], float (&hn)[2][6]) {
+  // zs: std::true_type when all 16 rows of the tile have no neighbours (s = 0,
+  // e.g. pocket atoms no ligand atom reaches in the non-covalent phase): the
+  // s k-tile is skipped in both GEMMs -- exact, the skipped products are zeros
+  auto gru16 = [&](auto zs, const float (&sv)[2][6], const float (&h)[2][6], float (&hn)[2][6]) {
+    constexpr int KT0 = decltype(zs)::value ? 1 : 0;
     float bz[6], br[6], bh[6];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {   // columns 8j+2t, 8j+2t+1: one 8-byte load per gate
@@ -485,7 +492,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     uint32_t ahi[3][4], alo[3][4];
     build_a48<SPLIT>(sv, h, ahi, alo);
     float Dzr[6][4];
-    gemm48<SPLIT, 6>(Dzr, ahi, alo, zr_hi, zr_lo, lane);
+    gemm48<SPLIT, 6, KT0>(Dzr, ahi, alo, zr_hi, zr_lo, lane);
     // D n-tile j holds (row g: cols 8j+2t, 8j+2t+1; row g+8: same)
     // elementwise work on column pairs (2j, 2j+1) with packed fp32 ops
     float z[2][6], rh[2][6];
@@ -510,7 +517,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     put_a<SPLIT>(ahi[2], alo[2], 2, rh[0][4], rh[0][5]);
     put_a<SPLIT>(ahi[2], alo[2], 3, rh[1][4], rh[1][5]);
     float Dh[3][4];
-    gemm48<SPLIT, 3>(Dh, ahi, alo, hh_hi, hh_lo, lane);
+    gemm48<SPLIT, 3, KT0>(Dh, ahi, alo, hh_hi, hh_lo, lane);
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
@@ -745,7 +752,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           float h[2][6], hn[2][6];
           load_h(r0, h[0]);
           load_h(r1, h[1]);
-          gru16(sv, h, hn);
+          // (SPLIT 2 only: on the 3-pass path the second GRU instantiation
+          // costs more than the skipped MMAs save, 25.15 -> 25.21 ms)
+          if constexpr (SPLIT == 2) {
+            if (__all_sync(0xffffffffu, d0 == 0 && d1 == 0)) gru16(std::true_type{}, sv, h, hn);
+            else gru16(std::false_type{}, sv, h, hn);
+          } else {
+            gru16(std::false_type{}, sv, h, hn);
+          }
           if (r0 < npad) store_hn(r0, hn[0]);
           if (r1 < npad) store_hn(r1, hn[1]);
         } else {
@@ -767,7 +781,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           }
           load_h(r0, h[0]);
           load_h(r1, h[1]);
-          gru16(sv, h, hn);
+          gru16(std::false_type{}, sv, h, hn);
           if (r0 < npad) store_hn(r0, hn[0]);
           if (r1 < npad) store_hn(r1, hn[1]);
         }
