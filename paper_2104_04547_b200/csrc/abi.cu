@@ -77,9 +77,11 @@ int launch_csr_entries(const fs_pose_batch& b, const int64_t* node_off, const in
                        double* d_cov, double* d_ncov, const int32_t* err, cudaStream_t st);
 bool conv1_fact_supported(int g, int k, int cin, int cout);
 int launch_conv1_fact(const fs_pose_batch& b, const char* cache, int64_t cache_stride, int64_t off_pp,
-                      int64_t off_ppact, int64_t off_wl, int c_elem, double box, __nv_bfloat16* out, cudaStream_t st);
+                      int64_t off_ppact, int64_t off_wl, int c_elem, double box, __nv_bfloat16* out, cudaStream_t st,
+                      int64_t off_ppact_lo, __nv_bfloat16* out_lo);
 int launch_pocket_conv1_fields(const float* pp, int n_pockets, char* cache, int64_t cache_stride, int64_t off_ppact,
-                               int64_t off_wl, const float* w1, int c_elem, cudaStream_t st);
+                               int64_t off_wl, const float* w1, int c_elem, cudaStream_t st, int64_t off_ppact_lo,
+                               int x3);
 int launch_round_bf16(const float* in, float* out, int64_t n, cudaStream_t st);
 int launch_pocket_total(const int64_t* pocket_off, int n_pockets, const float* f, int64_t ld, char* cache,
                         int64_t cache_stride, int64_t off_T, int64_t off_n, cudaStream_t st);
@@ -102,6 +104,7 @@ int launch_dense(const DenseArgs& a, cudaStream_t st);
 int launch_finalize(int n, int mode, const float* pv, const float* pg, float* scores, const int32_t* err, cudaStream_t st);
 int launch_grid_convert(const double* in, void* out, int n_poses, int c, int g, bool bf16, int32_t* err, cudaStream_t st);
 int launch_f64_to_f32(const double* in, float* out, int64_t n, int row, const int32_t* node_pose, int32_t* err, cudaStream_t st);
+int launch_split_bf16(const float* in, __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t n, cudaStream_t st);
 int launch_pose_bound(const int64_t* node_off, int n_poses, int64_t bound, int32_t* err, cudaStream_t st);
 
 struct GnnArgs {
@@ -512,7 +515,7 @@ static int pack_model(fs_model& m, const ParamMap& pm, std::vector<float>& h) {
 struct WsPlan {
   size_t total = 0;
   size_t node_off, deg_cov, deg_ncov, row_cov, row_ncov, col_cov, col_ncov, node_pose, cursor;
-  size_t feats, grid, a1, a2, p1, a3, a4, p2, d1, lat, hb0, hb1, g1, g2, pv, pg, state, scan, umma;
+  size_t feats, grid, grid_hi, grid_lo, a1, a2, p1, a3, a4, p2, d1, lat, hb0, hb1, g1, g2, pv, pg, state, scan, umma;
   size_t fact_cnt, fact_aff;
   size_t take(size_t bytes) { size_t o = total; total = align_up(total + bytes, 256); return o; }
 };
@@ -528,7 +531,14 @@ static WsPlan plan_ws(const fs_model& m, int64_t P, int64_t N, int64_t E, int pr
   w.col_cov = w.take(sizeof(col_t) * E); w.col_ncov = w.take(sizeof(col_t) * E);
   w.node_pose = w.take(4 * N); w.cursor = w.take(8 * (N + 1));
   w.feats = w.take(4 * N * m.F);
-  if (prec != FS_PREC_FP32) {   // tcgen05 conv chain (bf16 / mixed)
+  w.grid_hi = w.grid_lo = 0;
+  if (prec == FS_PREC_MIXED) {   // X3 tcgen05 chain: fp32 grid -> (hi, lo) bf16 operands
+    w.grid = w.take(4 * P * G3 * m.cin);
+    w.grid_hi = w.take(2 * P * G3 * m.cin); w.grid_lo = w.take(2 * P * G3 * m.cin);
+    w.umma = w.take(umma::workspace_bytes(m.d, P, true));
+    w.a1 = w.a2 = w.p1 = w.a3 = w.a4 = 0;
+    w.p2 = w.take(4 * (int64_t)umma::dense_rows_padded(P) * Q3 * m.f2);
+  } else if (prec != FS_PREC_FP32) {   // tcgen05 conv chain (bf16)
     w.grid = w.take(2 * P * G3 * m.cin);
     w.umma = w.take(umma::workspace_bytes(m.d, P));
     w.a1 = w.a2 = w.p1 = w.a3 = w.a4 = 0;
@@ -600,7 +610,7 @@ static SideStream* side_stream() {
 
 // ---- pocket cache (fs_pocket_prepare / fs_score_poses_cached) --------------
 struct PocketCacheLayout {
-  int64_t off_n, off_T, off_pp, off_ppact, off_wl, off_hcov, off_f, bytes;
+  int64_t off_n, off_T, off_pp, off_ppact, off_ppact_lo, off_wl, off_hcov, off_f, bytes;
 };
 
 static PocketCacheLayout cache_layout(const fs_model& m, int max_pocket) {
@@ -609,7 +619,8 @@ static PocketCacheLayout cache_layout(const fs_model& m, int max_pocket) {
   L.off_T = 256;
   L.off_pp = (int64_t)align_up(L.off_T + 8 * 128, 256);
   L.off_ppact = (int64_t)align_up(L.off_pp + (int64_t)4 * m.G * m.G * m.G * m.f1, 256);
-  L.off_wl = (int64_t)align_up(L.off_ppact + (int64_t)2 * m.G * m.G * m.G * m.f1, 256);
+  L.off_ppact_lo = (int64_t)align_up(L.off_ppact + (int64_t)2 * m.G * m.G * m.G * m.f1, 256);
+  L.off_wl = (int64_t)align_up(L.off_ppact_lo + (int64_t)2 * m.G * m.G * m.G * m.f1, 256);
   L.off_hcov = (int64_t)align_up(L.off_wl + (int64_t)4 * m.k1 * m.k1 * m.k1 * m.d.c_elem * m.f1, 256);
   L.off_f = (int64_t)align_up(L.off_hcov + (int64_t)4 * 24 * max_pocket, 256);
   L.bytes = (int64_t)align_up(L.off_f + (int64_t)4 * 128 * max_pocket, 256);
@@ -968,7 +979,17 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
   };
   auto voxel_branch = [&](cudaStream_t vs) {
     int r;
-    if (precision != FS_PREC_FP32) {
+    if (precision == FS_PREC_MIXED) {
+      if ((r = launch_voxelize(*b, d.grid_extent, m->cgrid, d.box_size, FS_GRID_NDHWC_F32, W + w.grid, err, vs)))
+        return r;
+      if ((r = launch_split_bf16((const float*)(W + w.grid), (__nv_bfloat16*)(W + w.grid_hi),
+                                 (__nv_bfloat16*)(W + w.grid_lo), (int64_t)P * m->G * m->G * m->G * m->cin, vs)))
+        return r;
+      if ((r = umma::voxel_convs_x3(d, (const char*)m->blob + m->umma_off, m->P(m->c1b), m->P(m->c2b),
+                                    m->P(m->c3b), m->P(m->c4b), P, (const __nv_bfloat16*)(W + w.grid_hi),
+                                    (const __nv_bfloat16*)(W + w.grid_lo), W + w.umma, (float*)(W + w.p2), vs)))
+        return r;
+    } else if (precision != FS_PREC_FP32) {
       if ((r = launch_voxelize(*b, d.grid_extent, m->cgrid, d.box_size, FS_GRID_NDHWC_BF16, W + w.grid, err, vs)))
         return r;
       if ((r = umma::voxel_convs(d, (const char*)m->blob + m->umma_off, m->P(m->c1b), m->P(m->c2b), m->P(m->c3b),
@@ -1095,14 +1116,18 @@ int fs_pocket_prepare(const fs_model* m, int precision, const double* pocket_xyz
   // conv1 pre-activation of the pocket channels, bf16-valued weights, fp32
   if ((rc = launch_voxelize(pb, d.grid_extent, m->cgrid, d.box_size, FS_GRID_NDHWC_F32, W + w.grid, err, st))) return rc;
   const int64_t nw = (int64_t)m->k1 * m->k1 * m->k1 * m->cin * m->f1;
-  if ((rc = launch_round_bf16(m->P(m->c1w), w1r, nw, st))) return rc;
+  // bf16 caches use the bf16-valued weights of the tcgen05 conv1; mixed
+  // caches the exact fp32 ones (the 3-pass conv1 is fp32-class)
+  const bool x3 = precision == FS_PREC_MIXED;
+  if (!x3 && (rc = launch_round_bf16(m->P(m->c1w), w1r, nw, st))) return rc;
   ConvArgs c{};
-  c.in = (float*)(W + w.grid); c.w = w1r; c.b = m->P(m->c1b); c.out = pp;
+  c.in = (float*)(W + w.grid); c.w = x3 ? m->P(m->c1w) : w1r; c.b = m->P(m->c1b); c.out = pp;
   c.n_vox = (int64_t)n * m->G * m->G * m->G; c.g = m->G; c.cin = m->cin; c.cout = m->f1; c.k = m->k1; c.no_relu = 1;
   if ((rc = launch_conv3d_ffma(c, st))) return rc;
   const size_t ppb = (size_t)4 * m->G * m->G * m->G * m->f1;
   FS_CUDA_CHECK(cudaMemcpy2DAsync(C + L.off_pp, L.bytes, pp, ppb, ppb, n, cudaMemcpyDeviceToDevice, st));
-  return launch_pocket_conv1_fields(pp, n, C, L.bytes, L.off_ppact, L.off_wl, m->P(m->c1w), d.c_elem, st);
+  return launch_pocket_conv1_fields(pp, n, C, L.bytes, L.off_ppact, L.off_wl, m->P(m->c1w), d.c_elem, st,
+                                    L.off_ppact_lo, x3 ? 1 : 0);
 }
 
 int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch* b, const void* cache,
@@ -1144,12 +1169,16 @@ int fs_score_poses_cached(const fs_model* m, int precision, const fs_pose_batch*
     return rc;
   if (ss) FS_CUDA_CHECK(cudaEventRecord(ss->join, gst));
   mark_stage(ST_CONV1, st);
+  const bool x3 = precision == FS_PREC_MIXED;
   if ((rc = launch_conv1_fact(*b, (const char*)cache, L.bytes, L.off_pp, L.off_ppact, L.off_wl, d.c_elem,
-                              d.box_size, umma::act1_ptr(W + w.umma), st)))
+                              d.box_size, umma::act1_ptr(W + w.umma), st, L.off_ppact_lo,
+                              x3 ? umma::act1_lo_ptr(W + w.umma, P) : nullptr)))
     return rc;
-  if ((rc = umma::voxel_convs_from2(d, (const char*)m->blob + m->umma_off, m->P(m->c2b), m->P(m->c3b), m->P(m->c4b),
-                                    P, W + w.umma, (float*)(W + w.p2), st)))
-    return rc;
+  rc = x3 ? umma::voxel_convs_from2_x3(d, (const char*)m->blob + m->umma_off, m->P(m->c2b), m->P(m->c3b),
+                                       m->P(m->c4b), P, W + w.umma, (float*)(W + w.p2), st)
+          : umma::voxel_convs_from2(d, (const char*)m->blob + m->umma_off, m->P(m->c2b), m->P(m->c3b),
+                                    m->P(m->c4b), P, W + w.umma, (float*)(W + w.p2), st);
+  if (rc) return rc;
   if ((rc = voxel_tail(*m, P, W, w, late || pred_v, st, precision == FS_PREC_BF16))) return rc;
   if (ss) FS_CUDA_CHECK(cudaStreamWaitEvent(st, ss->join, 0));
   GnnMmaArgs x{};
@@ -1191,7 +1220,16 @@ int fs_score_features(const fs_model* m, int precision, int32_t n_poses, const d
   int rc;
   FS_CUDA_CHECK(cudaMemsetAsync(err, 0, 4 * (size_t)P, st));
   if (need_v) {
-    if (precision != FS_PREC_FP32) {
+    if (precision == FS_PREC_MIXED) {
+      if ((rc = launch_grid_convert(grids, W + w.grid, P, m->cin, m->G, false, err, st))) return rc;
+      if ((rc = launch_split_bf16((const float*)(W + w.grid), (__nv_bfloat16*)(W + w.grid_hi),
+                                  (__nv_bfloat16*)(W + w.grid_lo), (int64_t)P * m->G * m->G * m->G * m->cin, st)))
+        return rc;
+      if ((rc = umma::voxel_convs_x3(d, (const char*)m->blob + m->umma_off, m->P(m->c1b), m->P(m->c2b),
+                                     m->P(m->c3b), m->P(m->c4b), P, (const __nv_bfloat16*)(W + w.grid_hi),
+                                     (const __nv_bfloat16*)(W + w.grid_lo), W + w.umma, (float*)(W + w.p2), st)))
+        return rc;
+    } else if (precision != FS_PREC_FP32) {
       if ((rc = launch_grid_convert(grids, W + w.grid, P, m->cin, m->G, true, err, st))) return rc;
       if ((rc = umma::voxel_convs(d, (const char*)m->blob + m->umma_off, m->P(m->c1b), m->P(m->c2b),
                                   m->P(m->c3b), m->P(m->c4b), P, (const __nv_bfloat16*)(W + w.grid),

@@ -260,6 +260,23 @@ int launch_pose_bound(const int64_t* node_off, int n_poses, int64_t bound, int32
   return FS_OK;
 }
 
+// fp32 -> (hi, lo) bf16 pair: hi = bf16(x), lo = bf16(x - hi) (the X3 operands)
+__global__ void split_bf16_kernel(const float* in, __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const float x = in[t];
+  const __nv_bfloat16 h = __float2bfloat16_rn(x);
+  hi[t] = h;
+  lo[t] = __float2bfloat16_rn(x - __bfloat162float(h));
+}
+
+int launch_split_bf16(const float* in, __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t n, cudaStream_t st) {
+  if (n <= 0) return FS_OK;
+  split_bf16_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(in, hi, lo, n);
+  FS_LAUNCH_CHECK();
+  return FS_OK;
+}
+
 int launch_f64_to_f32(const double* in, float* out, int64_t n, int row, const int32_t* node_pose,
                       int32_t* err, cudaStream_t st) {
   if (n <= 0) return FS_OK;

@@ -23,8 +23,11 @@ struct Conv1FactArgs {
   int64_t off_pp;               // pre-activation [G^3][COUT] fp32 (pocket channels + bias)
   int64_t off_ppact;            // relu(pre-activation) as bf16 in the act1 layout [COUT/8][G^3][8]
   int64_t off_wl;               // ligand-channel weights [k^3][c_elem][COUT], bf16-valued fp32
+                                //   (X3 caches: the exact fp32 weights)
+  int64_t off_ppact_lo;         // X3: the lo part of relu(pre-activation)
   int c_elem; double box;
   __nv_bfloat16* out;           // [P][COUT/8][G^3][8]
+  __nv_bfloat16* out_lo;        // X3 (FS_PREC_MIXED): lo part, same layout
 };
 
 constexpr int kC1G = 16, kC1K = 5, kC1R = 2, kC1Out = 32, kC1MaxLig = 128;
@@ -38,6 +41,9 @@ constexpr int kC1Threads = 256;
 //     (a 16-byte copy per 8 channels, L2 -> HBM);
 //  3. reached voxels: pocket pre-activation + the ligand atoms' weights, in
 //     atom order (deterministic), ReLU, bf16.
+// X3: the layer in fp32 (exact weights) with the output as a (hi, lo) bf16 pair
+// for the 3-pass tcgen05 conv2 (FS_PREC_MIXED)
+template <bool X3>
 __global__ void __launch_bounds__(kC1Threads) conv1_fact_kernel(Conv1FactArgs a) {
   extern __shared__ __align__(16) float wl[];           // [k^3][c_elem][32]
   __shared__ int4 atoms[kC1MaxLig];                      // (ix, iy, iz, ligand channel)
@@ -92,7 +98,9 @@ __global__ void __launch_bounds__(kC1Threads) conv1_fact_kernel(Conv1FactArgs a)
     __syncthreads();
     const char* pc = a.cache + static_cast<int64_t>(a.b.pose_target[p]) * a.cache_stride;
     const uint4* ppact = reinterpret_cast<const uint4*>(pc + a.off_ppact);
+    const uint4* ppact_lo = reinterpret_cast<const uint4*>(pc + a.off_ppact_lo);
     uint4* op = reinterpret_cast<uint4*>(a.out) + static_cast<int64_t>(p) * (kC1Out / 8) * kC1G3;
+    uint4* op_lo = X3 ? reinterpret_cast<uint4*>(a.out_lo) + static_cast<int64_t>(p) * (kC1Out / 8) * kC1G3 : nullptr;
     // untouched voxels: copy; touched ones: list them
     // touched-voxel bitmask, then the copy of the untouched ones with 4
     // independent 16-byte loads in flight per thread
@@ -123,8 +131,12 @@ __global__ void __launch_bounds__(kC1Threads) conv1_fact_kernel(Conv1FactArgs a)
       for (int r = 0; r < 4; ++r) {
         const int u = u0 + r * kC1Threads;
         if (u >= kUnits) continue;
-        if (!t[r]) op[u] = x[r];
-        else if (u < kC1G3) tlist[atomicAdd(&s_cnt, 1)] = static_cast<uint16_t>(u);
+        if (!t[r]) {
+          op[u] = x[r];
+          if constexpr (X3) op_lo[u] = __ldg(ppact_lo + u);
+        } else if (u < kC1G3) {
+          tlist[atomicAdd(&s_cnt, 1)] = static_cast<uint16_t>(u);
+        }
       }
     }
     __syncthreads();
@@ -161,12 +173,20 @@ __global__ void __launch_bounds__(kC1Threads) conv1_fact_kernel(Conv1FactArgs a)
       }
 #pragma unroll
       for (int q = 0; q < kC1Out / 8; ++q) {
-        uint4 pk;
+        uint4 pk, pl;
         __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&pk);
+        __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&pl);
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-          b2[t] = __floats2bfloat162_rn(fmaxf(acc[8 * q + 2 * t], 0.f), fmaxf(acc[8 * q + 2 * t + 1], 0.f));
+        for (int t = 0; t < 4; ++t) {
+          const float x0 = fmaxf(acc[8 * q + 2 * t], 0.f), x1 = fmaxf(acc[8 * q + 2 * t + 1], 0.f);
+          b2[t] = __floats2bfloat162_rn(x0, x1);
+          if constexpr (X3) {
+            const float2 h = __bfloat1622float2(b2[t]);
+            l2[t] = __floats2bfloat162_rn(x0 - h.x, x1 - h.y);
+          }
+        }
         op[q * kC1G3 + v] = pk;
+        if constexpr (X3) op_lo[q * kC1G3 + v] = pl;
       }
     }
   }
@@ -176,50 +196,67 @@ bool conv1_fact_supported(int g, int k, int cin, int cout) {
   return g == kC1G && k == kC1K && cout == kC1Out && cin % 2 == 0 && cin / 2 <= 8;
 }
 
-int launch_conv1_fact(const fs_pose_batch& b, const char* cache, int64_t cache_stride, int64_t off_pp,
-                      int64_t off_ppact, int64_t off_wl, int c_elem, double box, __nv_bfloat16* out, cudaStream_t st) {
-  if (b.n_poses <= 0) return FS_OK;
-  Conv1FactArgs a;
-  a.b = b; a.cache = cache; a.cache_stride = cache_stride; a.off_pp = off_pp; a.off_ppact = off_ppact;
-  a.off_wl = off_wl; a.c_elem = c_elem; a.box = box; a.out = out;
-  const size_t smem = static_cast<size_t>(kC1K * kC1K * kC1K) * c_elem * kC1Out * 4;
-  FS_CUDA_CHECK(cudaFuncSetAttribute(conv1_fact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+template <bool X3>
+static int launch_conv1_fact_t(const Conv1FactArgs& a, int n_poses, size_t smem, cudaStream_t st) {
+  FS_CUDA_CHECK(cudaFuncSetAttribute(conv1_fact_kernel<X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv1_fact_kernel, kC1Threads, smem);
-  const int grid = static_cast<int>(std::min<int64_t>(b.n_poses, static_cast<int64_t>(sms) * std::max(per_sm, 1)));
-  conv1_fact_kernel<<<grid, kC1Threads, smem, st>>>(a);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv1_fact_kernel<X3>, kC1Threads, smem);
+  const int grid = static_cast<int>(std::min<int64_t>(n_poses, static_cast<int64_t>(sms) * std::max(per_sm, 1)));
+  conv1_fact_kernel<X3><<<grid, kC1Threads, smem, st>>>(a);
   FS_LAUNCH_CHECK();
   return FS_OK;
 }
 
+int launch_conv1_fact(const fs_pose_batch& b, const char* cache, int64_t cache_stride, int64_t off_pp,
+                      int64_t off_ppact, int64_t off_wl, int c_elem, double box, __nv_bfloat16* out, cudaStream_t st,
+                      int64_t off_ppact_lo, __nv_bfloat16* out_lo) {
+  if (b.n_poses <= 0) return FS_OK;
+  Conv1FactArgs a;
+  a.b = b; a.cache = cache; a.cache_stride = cache_stride; a.off_pp = off_pp; a.off_ppact = off_ppact;
+  a.off_wl = off_wl; a.c_elem = c_elem; a.box = box; a.out = out;
+  a.off_ppact_lo = off_ppact_lo; a.out_lo = out_lo;
+  const size_t smem = static_cast<size_t>(kC1K * kC1K * kC1K) * c_elem * kC1Out * 4;
+  return out_lo ? launch_conv1_fact_t<true>(a, b.n_poses, smem, st) : launch_conv1_fact_t<false>(a, b.n_poses, smem, st);
+}
+
 // cache fields derived from the pocket pre-activation: relu'd bf16 act1
 // layout, and (slot-independent) the ligand-channel weights as bf16 values
+// x3 (FS_PREC_MIXED caches): relu'd act1 as a (hi, lo) pair and the exact fp32
+// ligand-channel weights
 __global__ void pocket_conv1_fields_kernel(const float* pp, int64_t pp_ld, char* cache, int64_t cache_stride,
-                                           int64_t off_ppact, int64_t off_wl, const float* w1, int c_elem) {
+                                           int64_t off_ppact, int64_t off_wl, const float* w1, int c_elem,
+                                           int64_t off_ppact_lo, int x3) {
   const int q = blockIdx.y;
   const float* src = pp + static_cast<int64_t>(q) * pp_ld;
   char* c = cache + static_cast<int64_t>(q) * cache_stride;
   __nv_bfloat16* act = reinterpret_cast<__nv_bfloat16*>(c + off_ppact);
+  __nv_bfloat16* act_lo = reinterpret_cast<__nv_bfloat16*>(c + off_ppact_lo);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kC1G3 * kC1Out; i += gridDim.x * blockDim.x) {
     const int v = i / kC1Out, o = i % kC1Out;
-    act[(static_cast<int64_t>(o / 8) * kC1G3 + v) * 8 + (o & 7)] = __float2bfloat16_rn(fmaxf(src[i], 0.f));
+    const float x = fmaxf(src[i], 0.f);
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    const int64_t at = (static_cast<int64_t>(o / 8) * kC1G3 + v) * 8 + (o & 7);
+    act[at] = h;
+    if (x3) act_lo[at] = __float2bfloat16_rn(x - __bfloat162float(h));
   }
   float* wlc = reinterpret_cast<float*>(c + off_wl);
   const int cin = 2 * c_elem, nw = kC1K * kC1K * kC1K * c_elem * kC1Out;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) {
     const int o = i % kC1Out, ch = (i / kC1Out) % c_elem, k = i / (kC1Out * c_elem);
-    wlc[i] = __bfloat162float(__float2bfloat16_rn(w1[(static_cast<int64_t>(k) * cin + c_elem + ch) * kC1Out + o]));
+    const float wv = w1[(static_cast<int64_t>(k) * cin + c_elem + ch) * kC1Out + o];
+    wlc[i] = x3 ? wv : __bfloat162float(__float2bfloat16_rn(wv));
   }
 }
 
 int launch_pocket_conv1_fields(const float* pp, int n_pockets, char* cache, int64_t cache_stride, int64_t off_ppact,
-                               int64_t off_wl, const float* w1, int c_elem, cudaStream_t st) {
+                               int64_t off_wl, const float* w1, int c_elem, cudaStream_t st, int64_t off_ppact_lo,
+                               int x3) {
   if (n_pockets <= 0) return FS_OK;
   dim3 grid(64, n_pockets);
   pocket_conv1_fields_kernel<<<grid, 256, 0, st>>>(pp, static_cast<int64_t>(kC1G3) * kC1Out, cache, cache_stride,
-                                                   off_ppact, off_wl, w1, c_elem);
+                                                   off_ppact, off_wl, w1, c_elem, off_ppact_lo, x3);
   FS_LAUNCH_CHECK();
   return FS_OK;
 }

@@ -149,6 +149,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+  const uint32_t z = 0;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(z)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_zero32(uint32_t taddr) {
   const uint32_t z = 0;
   asm volatile(
@@ -167,11 +187,19 @@ __host__ __device__ constexpr int pow2_cols(int x) {
 // ---------------------------------------------------------------------------
 constexpr int kSlots = 8;   // TMEM accumulator slots (output planes in flight) per tile
 
+// X3 (FS_PREC_MIXED): fp32-class 3-pass split on the same tensor cores.  An
+// fp32 operand x = hi + lo with hi = bf16(x), lo = bf16(x - hi) (relative
+// error ~2^-16); A.B ~ Alo.Bhi + Ahi.Blo + Ahi.Bhi, all accumulated in the
+// same fp32 TMEM slot.  Activations travel as two bf16 tensors (hi, lo);
+// weights hold a hi and a lo set.  AEX: the A operand is exact in bf16 (the
+// voxel grid's integer counts), so its lo pass is skipped (2 passes).
 template <int G_, int CIN_, int COUT_, int KS_, int POSES_, bool POOL_, bool RESID_, bool OUT_F32_, int NSPLIT_,
-          int RING_ = 4>
+          int RING_ = 4, bool X3_ = false, bool AEX_ = false>
 struct Cfg {
   static constexpr int G = G_, CIN = CIN_, COUT = COUT_, KS = KS_, POSES = POSES_, NSPLIT = NSPLIT_;
-  static constexpr bool POOL = POOL_, RESID = RESID_, OUT_F32 = OUT_F32_;
+  static constexpr bool POOL = POOL_, RESID = RESID_, OUT_F32 = OUT_F32_, X3 = X3_, AEX = AEX_;
+  static constexpr int W_SETS = X3 ? 2 : 1;                // weight sets: hi (+ lo)
+  static constexpr int A_SETS = (X3 && !AEX) ? 2 : 1;      // staged input sets per plane: hi (+ lo)
   static constexpr int R = KS / 2;
   static constexpr int HP = G + 2 * R, WP = G + 2 * R;
   static constexpr int CHUNKS = CIN / 8;
@@ -179,7 +207,7 @@ struct Cfg {
   static_assert(G * POSES == 16, "M = 8 w x G h x POSES = 128");
   static constexpr int BOX_BYTES = HP * POSES * WP * 16;  // one TMA box (8 channels)
   static constexpr int CHUNK_BYTES = align_to(BOX_BYTES, 128);
-  static constexpr int PLANE_BYTES = CHUNKS * CHUNK_BYTES;
+  static constexpr int PLANE_BYTES = A_SETS * CHUNKS * CHUNK_BYTES;   // [set][chunk]
   static constexpr int RING = RING_;                       // staged input planes (each consumed once)
   static constexpr int NCTA = COUT / NSPLIT;               // output channels per CTA
   static constexpr int NG = NCTA / 8;
@@ -187,15 +215,15 @@ struct Cfg {
   static constexpr int KSTEPS = KS * STEPS_PER_PLANE;
   static constexpr int JSTEP = NG * 128;                   // bytes of one kernel plane's N rows (one K chunk)
   static constexpr int STEP_BYTES = 2 * KS * JSTEP;        // one (kh,kw,chunk) step: [kc][kd desc][cout]
-  static constexpr int W_BYTES = STEPS_PER_PLANE * STEP_BYTES;   // per N slice
+  static constexpr int W_BYTES = STEPS_PER_PLANE * STEP_BYTES;   // per N slice and weight set
   static constexpr int SLOT_COLS = NCTA;
   static constexpr int TMEM_COLS = pow2_cols(TILES * kSlots * NCTA);
   static_assert(TILES * kSlots * NCTA <= 512, "TMEM budget");
   static_assert(G % kSlots == 0 && kSlots >= KS, "slot ring");
-  static_assert(KS * NCTA <= 256 && NCTA % 16 == 0, "stacked N");
+  static_assert(KS * NCTA <= 256 && NCTA % 16 == 0 && (NCTA % 32 == 0 || NCTA == 16), "stacked N");
   static constexpr int NPLANES = G + KS - 1;               // padded planes per unit
   static constexpr uint32_t SBO = WP * 16;
-  static constexpr int RING_OFF = align_to(W_BYTES, 1024);
+  static constexpr int RING_OFF = align_to(W_SETS * W_BYTES, 1024);
   static constexpr int BAR_OFF = RING_OFF + RING * PLANE_BYTES;
   // a 512-column TMEM allocation admits one CTA per SM: request enough shared
   // memory that the scheduler never co-locates two (the second would block
@@ -210,6 +238,12 @@ using C1 = Cfg<16, 8, 32, 5, 1, false, false, false, 1, 6>;
 using C2 = Cfg<16, 32, 32, 3, 1, true, false, false, 1, 4>;
 using C3 = Cfg<8, 32, 64, 3, 2, false, false, false, 1, 4>;
 using C4 = Cfg<8, 64, 64, 3, 2, true, true, true, 2, 3>;
+// X3 chain (FS_PREC_MIXED): twice the weights and staged planes, so conv3/conv4
+// split N over 2/4 CTAs and conv2/conv4 stage 2 planes ahead
+using C1X = Cfg<16, 8, 32, 5, 1, false, false, false, 1, 6, true>;
+using C2X = Cfg<16, 32, 32, 3, 1, true, false, false, 1, 2, true>;
+using C3X = Cfg<8, 32, 64, 3, 2, false, false, false, 2, 4, true>;
+using C4X = Cfg<8, 64, 64, 3, 2, true, true, true, 4, 2, true>;
 
 // Per K-step A-descriptor low word (start-address and LBO fields, 16-byte
 // units) relative to the plane base of the step's kd.
@@ -236,18 +270,41 @@ __host__ __device__ constexpr uint32_t a_step_lo(int s) {
 }
 
 struct ConvParams {
-  const char* w;            // packed B operands, NSPLIT slices of W_BYTES
+  const char* w;            // packed B operands, NSPLIT slices of W_SETS x W_BYTES
   const float* bias;        // [COUT]
-  const __nv_bfloat16* residual;   // [P][G^3][COUT] (conv4: h3)
+  const __nv_bfloat16* residual;   // [P][G^3][COUT] (conv4: h3; X3: its hi part)
+  const __nv_bfloat16* residual_lo;   // X3: lo part of h3
   void* out;
+  void* out_lo;             // X3, bf16 outputs: the lo part
   int n_poses;
 };
+
+// 8 fp32 values -> one 16-byte bf16 row at uint4 index i of `hi` (and, X3,
+// their residuals x - bf16(x) rounded to bf16 at the same index of `lo`)
+template <bool X3>
+__device__ __forceinline__ void store_split8(void* hi, void* lo, size_t i, const float* x) {
+  uint4 ph, pl;
+  __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&ph);
+  __nv_bfloat162* l2 = reinterpret_cast<__nv_bfloat162*>(&pl);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    h2[t] = __floats2bfloat162_rn(x[2 * t], x[2 * t + 1]);
+    if constexpr (X3) {
+      const float2 hf = __bfloat1622float2(h2[t]);
+      l2[t] = __floats2bfloat162_rn(x[2 * t] - hf.x, x[2 * t + 1] - hf.y);
+    }
+  }
+  reinterpret_cast<uint4*>(hi)[i] = ph;
+  if constexpr (X3) reinterpret_cast<uint4*>(lo)[i] = pl;
+}
 
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
 template <class L>
-__global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant__ CUtensorMap tmap, ConvParams prm) {
+__global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                           const __grid_constant__ CUtensorMap tmap_lo,
+                                                           ConvParams prm) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wsm = smem;
@@ -282,10 +339,11 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
-      const char* wsrc = prm.w + static_cast<size_t>(nsl) * L::W_BYTES;
-      mbar_expect_tx(wbar, L::W_BYTES);
-      for (int off = 0; off < L::W_BYTES; off += 32768) {
-        const int n = min(32768, L::W_BYTES - off);
+      constexpr int WB = L::W_SETS * L::W_BYTES;
+      const char* wsrc = prm.w + static_cast<size_t>(nsl) * WB;
+      mbar_expect_tx(wbar, WB);
+      for (int off = 0; off < WB; off += 32768) {
+        const int n = min(32768, WB - off);
         bulk_load(wsm + off, wsrc + off, n, wbar);
       }
       uint32_t gq = 0;
@@ -294,10 +352,14 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
         for (int q = 0; q < L::NPLANES; ++q, ++gq) {
           const int slot = gq % L::RING;
           mbar_wait(&empty[slot], ((gq / L::RING) & 1) ^ 1);
-          mbar_expect_tx(&full[slot], L::CHUNKS * L::BOX_BYTES);
+          mbar_expect_tx(&full[slot], L::A_SETS * L::CHUNKS * L::BOX_BYTES);
           unsigned char* dst = ring + slot * L::PLANE_BYTES;
           for (int c = 0; c < L::CHUNKS; ++c)
             tma_load_5d(dst + c * L::CHUNK_BYTES, &tmap, &full[slot], -8 * L::R, p0, -L::R, q - L::R, c);
+          if constexpr (L::A_SETS == 2)
+            for (int c = 0; c < L::CHUNKS; ++c)
+              tma_load_5d(dst + (L::CHUNKS + c) * L::CHUNK_BYTES, &tmap_lo, &full[slot], -8 * L::R, p0, -L::R,
+                          q - L::R, c);
         }
       }
     }
@@ -347,9 +409,20 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
             for (int s2 = 0; s2 < L::STEPS_PER_PLANE; ++s2) {
               const uint32_t a_lo = a_lo0 + a_step_lo<L>(s2);
               const uint32_t b_lo = b_lo1 + s2 * B_STEP;
-              if (lane == 0)
+              if (lane == 0) {
+                if constexpr (L::X3) {
+                  // small cross terms first, the hi.hi product last (one fp32 slot)
+                  constexpr uint32_t A_SET = (L::CHUNKS * L::CHUNK_BYTES) >> 4;
+                  constexpr uint32_t B_SET = L::W_BYTES >> 4;
+                  if constexpr (L::A_SETS == 2)
+                    umma_bf16(dtm, (static_cast<uint64_t>(A_HI) << 32) | (a_lo + A_SET),
+                              (static_cast<uint64_t>(B_HI) << 32) | b_lo, idesc, 1u);
+                  umma_bf16(dtm, (static_cast<uint64_t>(A_HI) << 32) | a_lo,
+                            (static_cast<uint64_t>(B_HI) << 32) | (b_lo + B_SET), idesc, 1u);
+                }
                 umma_bf16(dtm, (static_cast<uint64_t>(A_HI) << 32) | a_lo,
                           (static_cast<uint64_t>(B_HI) << 32) | b_lo, idesc, 1u);
+              }
             }
           }
         }
@@ -377,7 +450,10 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
 #pragma unroll
       for (int wh = 0; wh < L::TILES; ++wh)
 #pragma unroll
-        for (int c0 = 0; c0 < L::NCTA; c0 += 32) tmem_zero32(tq + (wh * kSlots + s) * L::SLOT_COLS + c0);
+        for (int c0 = 0; c0 < L::NCTA; c0 += 32) {
+          if constexpr (L::NCTA % 32 == 0) tmem_zero32(tq + (wh * kSlots + s) * L::SLOT_COLS + c0);
+          else tmem_zero16(tq + (wh * kSlots + s) * L::SLOT_COLS + c0);   // NCTA == 16 (C4X)
+        }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     tc_fence_before();
     for (int s = 0; s < kSlots; ++s) mbar_arrive(&tempty[s]);
@@ -400,8 +476,13 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
 #pragma unroll
           for (int c0 = 0; c0 < L::NCTA; c0 += 32) {
             const uint32_t ta = tq + (wh * kSlots + slot) * L::SLOT_COLS + c0;
-            tmem_ld32(ta, v + c0);
-            tmem_zero32(ta);
+            if constexpr (L::NCTA % 32 == 0) {
+              tmem_ld32(ta, v + c0);
+              tmem_zero32(ta);
+            } else {
+              tmem_ld16(ta, v + c0);
+              tmem_zero16(ta);
+            }
           }
 #pragma unroll
           for (int j = 0; j < L::NCTA; ++j) v[j] = fmaxf(v[j] + bias[j], 0.0f);
@@ -416,11 +497,18 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
               for (int q = 0; q < L::NCTA / 8; ++q) {
                 uint4 pk = rp[q * G3];
                 const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&pk);
+                float2 rl[4] = {};
+                if constexpr (L::X3) {   // h3 = hi + lo
+                  const uint4 pl = reinterpret_cast<const uint4*>(prm.residual_lo)[(rp - reinterpret_cast<const uint4*>(prm.residual)) + q * G3];
+                  const __nv_bfloat162* l2 = reinterpret_cast<const __nv_bfloat162*>(&pl);
+#pragma unroll
+                  for (int t = 0; t < 4; ++t) rl[t] = __bfloat1622float2(l2[t]);
+                }
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                   float2 f = __bfloat1622float2(b2[t]);
-                  v[q * 8 + 2 * t] += f.x;
-                  v[q * 8 + 2 * t + 1] += f.y;
+                  v[q * 8 + 2 * t] += f.x + rl[t].x;
+                  v[q * 8 + 2 * t + 1] += f.y + rl[t].y;
                 }
               }
             }
@@ -448,30 +536,16 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
               } else {
                 constexpr size_t GO3 = static_cast<size_t>(GO) * GO * GO;
                 const size_t ovx = (static_cast<size_t>(d / 2) * GO + h / 2) * GO + w / 2;
-                uint4* op = reinterpret_cast<uint4*>(prm.out) +
-                            (static_cast<size_t>(pose) * (L::COUT / 8) + n0 / 8) * GO3 + ovx;
+                const size_t oi = (static_cast<size_t>(pose) * (L::COUT / 8) + n0 / 8) * GO3 + ovx;
 #pragma unroll
-                for (int q = 0; q < L::NCTA / 8; ++q) {
-                  uint4 pk;
-                  __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&pk);
-#pragma unroll
-                  for (int t = 0; t < 4; ++t)
-                    b2[t] = __floats2bfloat162_rn(pmax[wh * L::NCTA + q * 8 + 2 * t],
-                                                  pmax[wh * L::NCTA + q * 8 + 2 * t + 1]);
-                  op[q * GO3] = pk;
-                }
+                for (int q = 0; q < L::NCTA / 8; ++q)
+                  store_split8<L::X3>(prm.out, prm.out_lo, oi + q * GO3, pmax + wh * L::NCTA + q * 8);
               }
             }
           } else if (live) {
-            uint4* op = reinterpret_cast<uint4*>(prm.out) + (static_cast<size_t>(pose) * (L::COUT / 8) + n0 / 8) * G3 + vox;
+            const size_t oi = (static_cast<size_t>(pose) * (L::COUT / 8) + n0 / 8) * G3 + vox;
 #pragma unroll
-            for (int q = 0; q < L::NCTA / 8; ++q) {
-              uint4 pk;
-              __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&pk);
-#pragma unroll
-              for (int t = 0; t < 4; ++t) b2[t] = __floats2bfloat162_rn(v[q * 8 + 2 * t], v[q * 8 + 2 * t + 1]);
-              op[q * G3] = pk;
-            }
+            for (int q = 0; q < L::NCTA / 8; ++q) store_split8<L::X3>(prm.out, prm.out_lo, oi + q * G3, v + q * 8);
           }
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -526,11 +600,13 @@ static int make_map(CUtensorMap* map, const void* base, int n_poses) {
 static int g_num_sms = 0;
 
 template <class L>
-static int launch_layer(const void* in, ConvParams prm, cudaStream_t st) {
+static int launch_layer(const void* in, ConvParams prm, cudaStream_t st, const void* in_lo = nullptr) {
   if (prm.n_poses <= 0) return FS_OK;
-  CUtensorMap map;
+  CUtensorMap map, map_lo;
   int rc = make_map<L>(&map, in, prm.n_poses);
   if (rc) return rc;
+  if (L::A_SETS == 2 && !in_lo) return FS_EINVAL;
+  if ((rc = make_map<L>(&map_lo, L::A_SETS == 2 ? in_lo : in, prm.n_poses))) return rc;
   if (!g_num_sms) {
     int dev = 0;
     FS_CUDA_CHECK(cudaGetDevice(&dev));
@@ -542,7 +618,7 @@ static int launch_layer(const void* in, ConvParams prm, cudaStream_t st) {
   const int per_sm = (!one_per_sm && L::TMEM_COLS <= 256 && (227 * 1024) / (L::SMEM + 1024) >= 2) ? 2 : 1;
   const int ctas = max(1, min(units, g_num_sms * per_sm / L::NSPLIT));
   dim3 grid(ctas, L::NSPLIT);
-  conv_umma_kernel<L><<<grid, 192, L::SMEM, st>>>(map, prm);
+  conv_umma_kernel<L><<<grid, 192, L::SMEM, st>>>(map, map_lo, prm);
   FS_LAUNCH_CHECK();
   return FS_OK;
 }
@@ -689,7 +765,11 @@ static constexpr size_t OFF_W1 = 0;
 static constexpr size_t OFF_W2 = align_to(C1::W_BYTES * C1::NSPLIT, 1024);
 static constexpr size_t OFF_W3 = OFF_W2 + align_to(C2::W_BYTES * C2::NSPLIT, 1024);
 static constexpr size_t OFF_W4 = OFF_W3 + align_to(C3::W_BYTES * C3::NSPLIT, 1024);
-static constexpr size_t W_TOTAL = OFF_W4 + align_to(C4::W_BYTES * C4::NSPLIT, 1024);
+static constexpr size_t OFF_X1 = OFF_W4 + align_to(C4::W_BYTES * C4::NSPLIT, 1024);
+static constexpr size_t OFF_X2 = OFF_X1 + align_to(2 * C1X::W_BYTES * C1X::NSPLIT, 1024);
+static constexpr size_t OFF_X3 = OFF_X2 + align_to(2 * C2X::W_BYTES * C2X::NSPLIT, 1024);
+static constexpr size_t OFF_X4 = OFF_X3 + align_to(2 * C3X::W_BYTES * C3X::NSPLIT, 1024);
+static constexpr size_t W_TOTAL = OFF_X4 + align_to(2 * C4X::W_BYTES * C4X::NSPLIT, 1024);
 
 size_t weights_bytes(const fs_model_desc& d) { return supports(d) ? W_TOTAL : 0; }
 
@@ -701,6 +781,14 @@ static uint16_t to_bf16(double x) {
   u += 0x7fffu + ((u >> 16) & 1u);                                                  // RNE
   return static_cast<uint16_t>(u >> 16);
 }
+static double from_bf16(uint16_t h) {
+  const uint32_t u = static_cast<uint32_t>(h) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+// the X3 lo part of a weight: bf16(w - bf16(w)), from the fp64 reference value
+static uint16_t to_bf16_lo(double x) { return to_bf16(x - from_bf16(to_bf16(x))); }
 
 // B operand layout per N slice: [step (kh,kw,chunk)][kchunk 2][kd descending]
 // [n-group][8 rows][8 ch] bf16 -- the N rows of one step are the KS kernel
@@ -708,10 +796,11 @@ static uint16_t to_bf16(double x) {
 // plane q reads the contiguous rows of kd = q-a down to q-b.
 template <class L>
 static void pack_layer(const double* w, char* out) {
-  // w: reference [O][C][k][k][k]
+  // w: reference [O][C][k][k][k]; per N slice: W_SETS sets of W_BYTES (hi, lo)
   const int K = L::KS, C = L::CIN;
-  for (int sl = 0; sl < L::NSPLIT; ++sl) {
-    uint16_t* o = reinterpret_cast<uint16_t*>(out + static_cast<size_t>(sl) * L::W_BYTES);
+  for (int sl = 0; sl < L::NSPLIT; ++sl)
+  for (int set = 0; set < L::W_SETS; ++set) {
+    uint16_t* o = reinterpret_cast<uint16_t*>(out + static_cast<size_t>(sl * L::W_SETS + set) * L::W_BYTES);
     std::memset(o, 0, L::W_BYTES);
     for (int s = 0; s < L::STEPS_PER_PLANE; ++s)
       for (int kc = 0; kc < 2; ++kc) {
@@ -733,7 +822,7 @@ static void pack_layer(const double* w, char* out) {
             for (int e = 0; e < 8; ++e) {
               const int ic = c0 + e;
               const double v = w[((((size_t)oc * C + ic) * K + kd) * K + kh) * K + kw];
-              o[core * 64 + (n % 8) * 8 + e] = to_bf16(v);
+              o[core * 64 + (n % 8) * 8 + e] = set == 0 ? to_bf16(v) : to_bf16_lo(v);
             }
           }
         }
@@ -748,6 +837,10 @@ void pack_weights(const fs_model_desc& d, const double* c1, const double* c2, co
   pack_layer<C2>(c2, out + OFF_W2);
   pack_layer<C3>(c3, out + OFF_W3);
   pack_layer<C4>(c4, out + OFF_W4);
+  pack_layer<C1X>(c1, out + OFF_X1);
+  pack_layer<C2X>(c2, out + OFF_X2);
+  pack_layer<C3X>(c3, out + OFF_X3);
+  pack_layer<C4X>(c4, out + OFF_X4);
 }
 
 // act1 [P][16^3][32] bf16, act2 (pooled) [P][8^3][32] bf16, act3 [P][8^3][64] bf16
@@ -755,9 +848,39 @@ static size_t act1_bytes(int64_t P) { return static_cast<size_t>(P) * 4096 * 32 
 static size_t act2_bytes(int64_t P) { return static_cast<size_t>(P + 1) * 512 * 32 * 2; }
 static size_t act3_bytes(int64_t P) { return static_cast<size_t>(P + 1) * 512 * 64 * 2; }
 
-size_t workspace_bytes(const fs_model_desc& d, int64_t P) {
+size_t workspace_bytes(const fs_model_desc& d, int64_t P, bool x3) {
   if (!supports(d)) return 0;
-  return act1_bytes(P) + act2_bytes(P) + act3_bytes(P) + 4096;
+  return (x3 ? 2 : 1) * (act1_bytes(P) + act2_bytes(P) + act3_bytes(P)) + 4096;
+}
+
+// X3 chain (FS_PREC_MIXED): activations as hi/lo bf16 pairs, 3-pass MMAs
+int voxel_convs_x3(const fs_model_desc& d, const char* wblob, const float* b1, const float* b2, const float* b3,
+                   const float* b4, int P, const __nv_bfloat16* grid, const __nv_bfloat16* grid_lo, char* ws,
+                   float* flat_out, cudaStream_t st) {
+  if (!supports(d)) return FS_ENOTSUP;
+  if (P <= 0) return FS_OK;
+  char* a1 = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 1023) & ~static_cast<uintptr_t>(1023));
+  char* a2 = a1 + act1_bytes(P);
+  char* a3 = a2 + act2_bytes(P);
+  char* l1 = a3 + act3_bytes(P);
+  char* l2 = l1 + act1_bytes(P);
+  char* l3 = l2 + act2_bytes(P);
+  int rc;
+  ConvParams p{};
+  p.n_poses = P;
+  mark_stage(ST_CONV1, st);
+  p.w = wblob + OFF_X1; p.bias = b1; p.out = a1; p.out_lo = l1;
+  if ((rc = launch_layer<C1X>(grid, p, st, grid_lo))) return rc;
+  mark_stage(ST_CONV2, st);
+  p.w = wblob + OFF_X2; p.bias = b2; p.out = a2; p.out_lo = l2;
+  if ((rc = launch_layer<C2X>(a1, p, st, l1))) return rc;
+  mark_stage(ST_CONV3, st);
+  p.w = wblob + OFF_X3; p.bias = b3; p.out = a3; p.out_lo = l3;
+  if ((rc = launch_layer<C3X>(a2, p, st, l2))) return rc;
+  mark_stage(ST_CONV4, st);
+  p.w = wblob + OFF_X4; p.bias = b4; p.out = flat_out; p.out_lo = nullptr;
+  p.residual = reinterpret_cast<const __nv_bfloat16*>(a3); p.residual_lo = reinterpret_cast<const __nv_bfloat16*>(l3);
+  return launch_layer<C4X>(a3, p, st, l3);
 }
 
 int voxel_convs(const fs_model_desc& d, const char* wblob, const float* b1, const float* b2, const float* b3,
@@ -809,6 +932,37 @@ int voxel_convs_from2(const fs_model_desc& d, const char* wblob, const float* b2
   mark_stage(ST_CONV4, st);
   p.w = wblob + OFF_W4; p.bias = b4; p.out = flat_out; p.residual = reinterpret_cast<const __nv_bfloat16*>(a3);
   return launch_layer<C4>(a3, p, st);
+}
+
+// X3 workspace: a1, a2, a3 (hi) then l1, l2, l3 (lo)
+__nv_bfloat16* act1_lo_ptr(char* ws, int64_t P) {
+  return reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(act1_ptr(ws)) + act1_bytes(P) + act2_bytes(P) +
+                                          act3_bytes(P));
+}
+
+int voxel_convs_from2_x3(const fs_model_desc& d, const char* wblob, const float* b2, const float* b3, const float* b4,
+                         int P, char* ws, float* flat_out, cudaStream_t st) {
+  if (!supports(d)) return FS_ENOTSUP;
+  if (P <= 0) return FS_OK;
+  char* a1 = reinterpret_cast<char*>(act1_ptr(ws));
+  char* a2 = a1 + act1_bytes(P);
+  char* a3 = a2 + act2_bytes(P);
+  char* l1 = a3 + act3_bytes(P);
+  char* l2 = l1 + act1_bytes(P);
+  char* l3 = l2 + act2_bytes(P);
+  int rc;
+  ConvParams p{};
+  p.n_poses = P;
+  mark_stage(ST_CONV2, st);
+  p.w = wblob + OFF_X2; p.bias = b2; p.out = a2; p.out_lo = l2;
+  if ((rc = launch_layer<C2X>(a1, p, st, l1))) return rc;
+  mark_stage(ST_CONV3, st);
+  p.w = wblob + OFF_X3; p.bias = b3; p.out = a3; p.out_lo = l3;
+  if ((rc = launch_layer<C3X>(a2, p, st, l2))) return rc;
+  mark_stage(ST_CONV4, st);
+  p.w = wblob + OFF_X4; p.bias = b4; p.out = flat_out; p.out_lo = nullptr;
+  p.residual = reinterpret_cast<const __nv_bfloat16*>(a3); p.residual_lo = reinterpret_cast<const __nv_bfloat16*>(l3);
+  return launch_layer<C4X>(a3, p, st, l3);
 }
 
 int debug_layer(const fs_model_desc& d, const char* wblob, const float* bias, const float* residual_unused,
