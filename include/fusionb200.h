@@ -65,9 +65,13 @@ extern "C" {
  *                   x fp16 weights (2 passes, fp32 accumulate; transcendentals
  *                   via ex2.approx / tanh.approx in the pool), fp32 fusion MLP.
  *                   Stated tolerance vs the reference: see DESIGN.md section 4.
- *   FS_PREC_MIXED : the 1e-3 path on tensor cores.  Conv3d as FS_PREC_BF16,
- *                   dense1 FFMA fp32, SG-CNN GEMMs bf16 hi/lo x hi/lo (3 passes,
- *                   fp32-class), fp32 fusion MLP. */
+ *   FS_PREC_MIXED : fp32-class on the tensor cores (the 1e-3 path).  Every
+ *                   tensor-core GEMM is a 3-pass bf16 split (x = hi + lo,
+ *                   A.B ~ Alo.Bhi + Ahi.Blo + Ahi.Bhi, fp32 accumulate): tcgen05
+ *                   Conv3d with activations carried as (hi, lo) bf16 pairs and
+ *                   hi/lo weight sets, SG-CNN GEMMs on mma.sync likewise with
+ *                   fp32 node states and accurate ex2/rcp gates; dense1 FFMA
+ *                   fp32; fp32 fusion MLP. */
 #define FS_PREC_FP32  0
 #define FS_PREC_BF16  1
 #define FS_PREC_MIXED 2
