@@ -235,9 +235,11 @@ struct Cfg {
 // conv1 8->32 k5 on 16^3; conv2 32->32 k3 +pool; conv3 32->64 k3 (pose pairs);
 // conv4 64->64 k3 +residual +pool (pose pairs, N split over 2 CTAs).
 using C1 = Cfg<16, 8, 32, 5, 1, false, false, false, 1, 6>;
-using C2 = Cfg<16, 32, 32, 3, 1, true, false, false, 1, 4>;
+// (ring depths leave room for one or two co-resident radius-graph CTAs of the
+// overlapped graph branch: conv2 118.5 KB, conv4 162 KB)
+using C2 = Cfg<16, 32, 32, 3, 1, true, false, false, 1, 3>;
 using C3 = Cfg<8, 32, 64, 3, 2, false, false, false, 1, 4>;
-using C4 = Cfg<8, 64, 64, 3, 2, true, true, true, 2, 3>;
+using C4 = Cfg<8, 64, 64, 3, 2, true, true, true, 2, 2>;
 // X3 chain (FS_PREC_MIXED): twice the weights and staged planes, so conv3/conv4
 // split N over 2/4 CTAs and conv2/conv4 stage 2 planes ahead
 using C1X = Cfg<16, 8, 32, 5, 1, false, false, false, 1, 6, true>;
