@@ -72,7 +72,7 @@ def test_factored_vs_oracle(env):
     for p in (0, 17, 45):
         pos, el, ro = synth.complex_arrays(pockets[lib.target[p]], lib, p)
         want = orc.score_pose(params, (VOXEL, GRAPH, COHERENT), pos, el, ro)["score"]
-        assert abs(fact[p] - want) / abs(want) < 3e-2
+        assert abs(fact[p] - want) / abs(want) < 1e-3       # mixed: fp32-class
 
 
 def test_factored_batch_invariance_bitwise(env):

@@ -102,8 +102,9 @@ def test_umma_layer_matches_torch_reference(setup, layer, P):
 
 
 def test_bf16_scores_within_stated_tolerance(setup):
-    """Stated bf16 tolerance: max relative error <= 3e-2 vs the
-    fp32 path and centred-score Pearson >= 0.99 over a 512-pose screen."""
+    """Stated bf16 tolerance: max relative error <= 3e-3
+    vs the fp32 path and centred-score Pearson >= 0.9999 over a 512-pose
+    screen (measured ~1e-3 / 0.99998)."""
     torch, N, m, dm = setup
     from paper_2104_04547_b200 import engine as E
     from paper_2104_04547_b200 import synth
@@ -117,8 +118,8 @@ def test_bf16_scores_within_stated_tolerance(setup):
     rel = np.max(np.abs(s16 - s32) / np.abs(s32))
     pear = np.corrcoef(s16 - s16.mean(), s32 - s32.mean())[0, 1]
     print(f"bf16 vs fp32: max rel {rel:.3e}, centred Pearson {pear:.5f}")
-    assert rel <= 3e-2
-    assert pear >= 0.99
+    assert rel <= 3e-3
+    assert pear >= 0.9999
 
 
 def test_bf16_voxel_latent_close_to_fp32(setup):

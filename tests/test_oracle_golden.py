@@ -132,3 +132,16 @@ def test_c_radius_oracle_matches_numpy_oracle():
         pos, _, ro = synth.complex_arrays(pk, lib, p)
         for a, b in zip(orc.radius_pairs(pos, ro), radius_c.radius_pairs(pos, ro)):
             assert np.array_equal(a, b)
+
+
+def test_config1_oracle_fixture_matches_oracle():
+    """tests/golden/config1_oracle.npz (scores the GPU config-1 test compares
+    against) is the pinned oracle's output: spot-check 3 of its poses."""
+    from paper_2104_04547_b200 import synth
+    z = load("config1_oracle.npz")
+    pocket = synth.make_pocket(1000, seed=0)
+    lib = synth.make_poses(103, 10, seed=1, ligand_atoms=(16, 64)).slice(0, 1024)
+    params = orc.init_params(VOXEL, GRAPH, COHERENT, 0)
+    for p in (0, 511, 1023):
+        s = orc.score_pose(params, (VOXEL, GRAPH, COHERENT), *synth.complex_arrays(pocket, lib, p))["score"]
+        assert s == z["scores"][p]
