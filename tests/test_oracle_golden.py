@@ -144,4 +144,4 @@ def test_config1_oracle_fixture_matches_oracle():
     params = orc.init_params(VOXEL, GRAPH, COHERENT, 0)
     for p in (0, 511, 1023):
         s = orc.score_pose(params, (VOXEL, GRAPH, COHERENT), *synth.complex_arrays(pocket, lib, p))["score"]
-        assert s == z["scores"][p]
+        assert abs(s - z["scores"][p]) <= 1e-12 * abs(s)    # BLAS thread count changes the last ulp
