@@ -7,9 +7,10 @@ with the reference's reason strings, batch-partition invariant) as
 in libfusionb200 on the GPU.  Training (``train``/``train_head``/tapes) is out
 of scope: the hot path is inference.
 
-Precision: ``FusionModel.precision`` is "fp32" (FFMA, reference within 1e-3
-relative) by default; "bf16" selects the tcgen05 tensor-core Conv3d path
-(stated, measured tolerance).
+Precision: ``FusionModel.precision`` is "auto" by default -- the fp32-class
+tensor-core path ("mixed": 3-pass bf16 hi/lo splits, reference within 1e-3,
+measured 1.3e-5) where the configuration has it, else FFMA "fp32"; "bf16"
+selects the fastest path (stated, measured tolerance).
 """
 
 from __future__ import annotations
@@ -296,7 +297,7 @@ class FusionModel:
     """Two head parameter sets plus fusion layers (models.py:412-568)."""
 
     def __init__(self, voxel_cfg: VoxelHeadConfig, graph_cfg: GraphHeadConfig, fusion_cfg: FusionConfig,
-                 seed: int = 0, heads_pretrained: bool = False, precision: str = "fp32"):
+                 seed: int = 0, heads_pretrained: bool = False, precision: str = "auto"):
         rng = np.random.default_rng(seed)
         self.voxel_cfg, self.graph_cfg, self.fusion_cfg = voxel_cfg, graph_cfg, fusion_cfg
         self.voxel_params = init_voxel_params(voxel_cfg, rng)
@@ -420,6 +421,14 @@ class FusionModel:
             out[slot] = dev if rows else torch.zeros((0, width), dtype=dt, device="cuda")
         return out[0], torch.from_numpy(off).to("cuda", non_blocking=True), out[1], out[2], off
 
+    def _precision(self, dm) -> str:
+        """"auto" (the default): the fp32-class tensor-core path ("mixed",
+        reference within 1e-3; measured 1.3e-5) where the configuration has
+        it, else FFMA "fp32".  "fp32" / "mixed" / "bf16" force a path."""
+        if self.precision != "auto":
+            return self.precision
+        return "mixed" if dm.supports("mixed") else "fp32"
+
     def _thread_stream(self):
         """Each host thread scores on its own CUDA stream, so the reference's
         campaign driver -- which calls the scorer plugin from a thread pool
@@ -467,7 +476,7 @@ class FusionModel:
         feats, node_off, ce, ne, off = self._upload_graphs([items[i][1] for i in valid])
         dm = self.device_model()
         out = dm.score_features(len(valid), grids=self._upload_grids(items, valid), feats=feats, node_off=node_off,
-                                cov_edges=ce, ncov_edges=ne, heads=7, precision=self.precision,
+                                cov_edges=ce, ncov_edges=ne, heads=7, precision=self._precision(dm),
                                 max_pose_nodes=int(np.diff(off).max()))
         scores = out["scores"].cpu().numpy().astype(np.float64)
         err = out["err"].cpu().numpy()
@@ -520,7 +529,7 @@ class FusionModel:
         dm = self.device_model()
         with self._thread_stream():
             b = batch_from_complexes(complexes)
-            out = dm.score_poses(b, self.precision)
+            out = dm.score_poses(b, self._precision(dm))
             return out["scores"].cpu().numpy().astype(np.float64), out["err"].cpu().numpy()
 
     # -- parameter bookkeeping (models.py:532-568) -----------------------------
@@ -545,7 +554,7 @@ class FusionModel:
         save_checkpoint(path, self.all_params(), optimizer, meta)
 
     @classmethod
-    def load(cls, path, precision: str = "fp32") -> "FusionModel":
+    def load(cls, path, precision: str = "auto") -> "FusionModel":
         """Loads reference checkpoints (checkpoint.py:48-71 format) unchanged."""
         params, _, meta = load_checkpoint(path)
         m = cls(VoxelHeadConfig(**meta["voxel_cfg"]), GraphHeadConfig(**meta["graph_cfg"]),
