@@ -64,6 +64,11 @@ VOXEL_FLOP = 659_570_816
 CONV_FLOP = {"conv1": 2 * 131_072_000, "conv2": 2 * 113_246_208, "conv3": 2 * 28_311_552,
              "conv4": 2 * 56_623_104}
 DENSE_FLOP = 2 * (4096 * 128 + 128 * 64)
+# fraction of CONV_FLOP the tensor cores actually issue: the kernels skip the
+# all-zero "same"-padding depth planes (umma_conv.cu issuer), i.e. the
+# R(R+1) of G*KS (input plane, output plane) pairs that read only padding
+CONV_GKS = {"conv1": (16, 5), "conv2": (16, 3), "conv3": (8, 3), "conv4": (8, 3)}
+CONV_ISSUED = {k: 1.0 - (ks // 2) * (ks // 2 + 1) / (g * ks) for k, (g, ks) in CONV_GKS.items()}
 
 
 def graph_flop(n, ec, en):
@@ -862,7 +867,8 @@ def main():
                 continue
             if nm in CONV_FLOP:
                 kern[nm] = {"bound": "tensor", "achieved": CONV_FLOP[nm] / t_s / 1e12, "peak": bf16_burst,
-                            "unit": "TFLOP/s"}
+                            "unit": "TFLOP/s", "issued_flop_frac": round(CONV_ISSUED[nm], 4),
+                            "issued_tflops": CONV_ISSUED[nm] * CONV_FLOP[nm] / t_s / 1e12}
             elif nm == "gnn":
                 kern[nm] = {"bound": "tensor", "achieved": gflop / t_s / 1e12, "peak": bf16_sus, "unit": "TFLOP/s"}
             elif nm == "dense":

@@ -351,7 +351,9 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
       uint32_t gq = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int p0 = u * L::POSES;
-        for (int q = 0; q < L::NPLANES; ++q, ++gq) {
+        // only the G real input planes are staged: the KS-1 "same"-padding
+        // planes are all zero and contribute nothing (see the issuer)
+        for (int q = L::R; q < L::G + L::R; ++q, ++gq) {
           const int slot = gq % L::RING;
           mbar_wait(&empty[slot], ((gq / L::RING) & 1) ^ 1);
           mbar_expect_tx(&full[slot], L::A_SETS * L::CHUNKS * L::BOX_BYTES);
@@ -381,9 +383,13 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
     const uint32_t b_lo0 = ((wbase >> 4) & 0x3FFFu) | (((L::KS * L::JSTEP) >> 4) << 16);
     uint32_t gq = 0, uo = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, uo += L::G) {
-      for (int q = 0; q < L::NPLANES; ++q, ++gq) {
+      for (int q = 0; q < L::NPLANES; ++q) {
+        // input planes q < R and q >= G + R are the zero "same" padding: their
+        // MMAs would add exact zeros, so they are skipped (no staging, no MMA;
+        // output slots start zeroed) -- 20% of the MMAs at KS = 5 / G = 8
+        const bool real = q >= L::R && q < L::G + L::R;
         const uint32_t rs = gq % L::RING;
-        mbar_wait(&full[rs], (gq / L::RING) & 1);
+        if (real) mbar_wait(&full[rs], (gq / L::RING) & 1);
         const int dlo = q - L::KS + 1 > 0 ? q - L::KS + 1 : 0;
         const int dhi = q < L::G - 1 ? q : L::G - 1;
         if (q < L::G) {   // output plane q enters: its slot must be drained and zeroed
@@ -391,6 +397,7 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
           mbar_wait(&tempty[o % kSlots], (o / kSlots) & 1);
         }
         tc_fence_after();
+        if (real) {
         // [dlo, dhi] split where it crosses a multiple of kSlots (G % kSlots == 0,
         // so output d of every unit lives in slot d % kSlots)
         const int dmid = (dlo / kSlots + 1) * kSlots;      // first plane of the next slot cycle
@@ -428,12 +435,12 @@ __global__ void __launch_bounds__(192, 1) conv_umma_kernel(const __grid_constant
             }
           }
         }
-        if (lane == 0) {
-          umma_commit(&empty[rs]);                         // plane q is read by no later MMA
-          if (q >= L::KS - 1) {                            // output plane q-KS+1 is complete
-            const uint32_t o = uo + q - L::KS + 1;
-            umma_commit(&tfull[o % kSlots]);
-          }
+        if (lane == 0) umma_commit(&empty[rs]);         // plane q is read by no later MMA
+        ++gq;
+        }   // real
+        if (lane == 0 && q >= L::KS - 1) {               // output plane q-KS+1 is complete
+          const uint32_t o = uo + q - L::KS + 1;
+          umma_commit(&tfull[o % kSlots]);
         }
         __syncwarp();
       }
