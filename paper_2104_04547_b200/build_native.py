@@ -14,14 +14,18 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 _BOUNDS = bool(os.environ.get("FS_BOUNDS"))     # device-side index checks: a separate debug library
-BUILD = os.path.join(HERE, "_build_bounds" if _BOUNDS else "_build")
-LIB = os.path.join(HERE, "libfusionb200_bounds.so" if _BOUNDS else "libfusionb200.so")
+# FS_BUILD_TAG + FS_EXTRA_FLAGS: a side build for kernel A/B experiments
+# (libfusionb200_<tag>.so, loaded with FS_LIB=...)
+_TAG = os.environ.get("FS_BUILD_TAG") or ("bounds" if _BOUNDS else "")
+BUILD = os.path.join(HERE, f"_build_{_TAG}" if _TAG else "_build")
+LIB = os.path.join(HERE, f"libfusionb200_{_TAG}.so" if _TAG else "libfusionb200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", INCLUDE, "-I", CSRC]
 if _BOUNDS:
     FLAGS.append("-DFS_BOUNDS")
+FLAGS += os.environ.get("FS_EXTRA_FLAGS", "").split()
 
 
 def sources():

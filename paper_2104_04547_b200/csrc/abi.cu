@@ -17,6 +17,7 @@
 #include <cuda_fp16.h>
 
 #include "common.cuh"
+#include "gnn_mma.cuh"
 #include "umma_conv.cuh"
 
 namespace fs {
@@ -116,24 +117,6 @@ struct GnnArgs {
   int k_steps[2]; int gn; float* state; float* lat; int64_t ld_lat; const int32_t* err; int smem_state;
 };
 int gnn_padded_width(int d);
-struct GnnMmaArgs {
-  const float* feats; int F; const int64_t* node_off;
-  const int64_t* row_cov; const int32_t* deg_cov; const col_t* col_cov;
-  const int64_t* row_ncov; const int32_t* deg_ncov; const col_t* col_ncov;
-  const float* we; const float* be; const uint32_t* wfrag[2]; const float* wbias[2];
-  const uint32_t* gfrag; const uint32_t* wfrag16[2]; const uint32_t* gfrag16;
-  const float* gbias; int k_steps[2]; float* lat; int64_t ld_lat; const int32_t* err;
-  const int32_t* fact_cnt; int64_t fact_stride; const int32_t* fact_aff; const int32_t* pose_target;
-  const char* cache; int64_t cache_stride; int64_t off_hcov, off_f, off_T, off_n;
-  float* dump_hcov; float* dump_f; int64_t dump_ld;
-  int heavy_cap;
-  int ids_padded;
-};
-int gnn_mma_phase_words();
-int gnn_mma_gather_words();
-bool gnn_mma_fits(int max_nodes);
-int gnn_mma_max_nodes();
-int launch_gnn_mma(const GnnMmaArgs& a, int split, int n_poses, int max_nodes, cudaStream_t st);
 int launch_gnn(const GnnArgs& a, int dpad, int n_poses, int max_nodes, cudaStream_t st);
 bool gnn_needs_global_state(int dpad, int max_nodes);
 
@@ -169,6 +152,7 @@ struct fs_model {
   bool gmma_ok = false;  // tensor-core SG-CNN (widths 24 / 128)
   size_t gm_wf[2], gm_wb[2], gm_gf, gm_gb;
   size_t gm_wf16[2], gm_gf16;   // fp16 weight fragments of the 2-pass SG-CNN
+  size_t gm_wb16[2], gm_gb16;   // its biases (tanh-scaled like the fp16 fragments)
   const float* P(size_t off) const { return blob + off; }
 };
 
@@ -237,6 +221,8 @@ static size_t plan_model(fs_model& m) {
     m.gm_gb = L.take(256);
     for (int ph = 0; ph < 2; ++ph) m.gm_wf16[ph] = L.take(gnn_mma_phase_words() / 2);
     m.gm_gf16 = L.take(gnn_mma_gather_words() / 2);
+    for (int ph = 0; ph < 2; ++ph) m.gm_wb16[ph] = L.take(72);
+    m.gm_gb16 = L.take(256);
   }
   size_t bytes = L.n * 4;
   m.umma_ok = umma::supports(d);
@@ -439,28 +425,38 @@ static int pack_model(fs_model& m, const ParamMap& pm, std::vector<float>& h) {
         for (int t2 = 0; t2 < dg; ++t2) acc += msg[(size_t)c * dg + t2] * W[q][(size_t)t2 * dg + k];
         return acc;
       };
-      // gate pre-activations carry the ex2 scale of their activation
-      // (fs_sigmoid_pre / fs_tanh_pre): z, r by -log2(e), h~ by 2 log2(e)
+      // gate pre-activations carry the scale of their activation:
+      //  bf16 sets (3-pass): the ex2 scale (fs_sigmoid_pre / fs_tanh_pre),
+      //   z, r by -log2(e), h~ by 2 log2(e);
+      //  fp16 set (2-pass): the tanh scale, z, r by 1/2 (sigmoid(x) =
+      //   (1 + tanh(x/2)) / 2), h~ by 1 -- exact power-of-two scalings
+      auto pack = [&](const double (&sc)[3], std::vector<double>& Wzr, std::vector<double>& Whh) {
+        for (int c = 0; c < 24; ++c)
+          for (int k = 0; k < 24; ++k) {
+            Wzr[(size_t)c * 48 + k] = sc[0] * fold(0, c, k);
+            Wzr[(size_t)c * 48 + 24 + k] = sc[1] * fold(1, c, k);
+            Wzr[(size_t)(24 + c) * 48 + k] = sc[0] * U[0][(size_t)c * dg + k];
+            Wzr[(size_t)(24 + c) * 48 + 24 + k] = sc[1] * U[1][(size_t)c * dg + k];
+            Whh[(size_t)c * 24 + k] = sc[2] * fold(2, c, k);
+            Whh[(size_t)(24 + c) * 24 + k] = sc[2] * U[2][(size_t)c * dg + k];
+          }
+      };
       std::vector<double> Wzr((size_t)48 * 48), Whh((size_t)48 * 24);
       const double sc[3] = {kNegLog2e, kNegLog2e, kTwoLog2e};
-      for (int c = 0; c < 24; ++c)
-        for (int k = 0; k < 24; ++k) {
-          Wzr[(size_t)c * 48 + k] = sc[0] * fold(0, c, k);
-          Wzr[(size_t)c * 48 + 24 + k] = sc[1] * fold(1, c, k);
-          Wzr[(size_t)(24 + c) * 48 + k] = sc[0] * U[0][(size_t)c * dg + k];
-          Wzr[(size_t)(24 + c) * 48 + 24 + k] = sc[1] * U[1][(size_t)c * dg + k];
-          Whh[(size_t)c * 24 + k] = sc[2] * fold(2, c, k);
-          Whh[(size_t)(24 + c) * 24 + k] = sc[2] * U[2][(size_t)c * dg + k];
-        }
+      pack(sc, Wzr, Whh);
       uint32_t* wf = reinterpret_cast<uint32_t*>(&h[m.gm_wf[ph]]);
       const int zr = 3 * 6 * 64, hh = 3 * 3 * 64;
       frags(Wzr, 48, 48, wf, wf + zr);
       frags(Whh, 48, 24, wf + 2 * zr, wf + 2 * zr + hh);
+      for (int q = 0; q < 3; ++q)
+        for (int k = 0; k < 24; ++k) h[m.gm_wb[ph] + q * 24 + k] = (float)(sc[q] * B[q][k]);
+      const double st[3] = {0.5, 0.5, 1.0};
+      pack(st, Wzr, Whh);
       uint32_t* wf16 = reinterpret_cast<uint32_t*>(&h[m.gm_wf16[ph]]);
       frags16(Wzr, 48, 48, wf16);
       frags16(Whh, 48, 24, wf16 + zr);
       for (int q = 0; q < 3; ++q)
-        for (int k = 0; k < 24; ++k) h[m.gm_wb[ph] + q * 24 + k] = (float)(sc[q] * B[q][k]);
+        for (int k = 0; k < 24; ++k) h[m.gm_wb16[ph] + q * 24 + k] = (float)(st[q] * B[q][k]);
     }
     const double* ggw = need("graph/gather_gate_w"); const double* ggb = need("graph/gather_gate_b");
     const double* gfw = need("graph/gather_feat_w"); const double* gfb = need("graph/gather_feat_b");
@@ -472,10 +468,20 @@ static int pack_model(fs_model& m, const ParamMap& pm, std::vector<float>& h) {
       }
     uint32_t* gf = reinterpret_cast<uint32_t*>(&h[m.gm_gf]);
     frags(Gm, 32, 256, gf, gf + gnn_mma_gather_words() / 2);
-    frags16(Gm, 32, 256, reinterpret_cast<uint32_t*>(&h[m.gm_gf16]));
     for (int k = 0; k < 128; ++k) {
       h[m.gm_gb + k] = (float)(kNegLog2e * ggb[k]);
       h[m.gm_gb + 128 + k] = (float)(kTwoLog2e * gfb[k]);
+    }
+    // fp16 pool weights: gate by 1/2 (tanh form of the sigmoid), value by 1
+    for (int c = 0; c < 24; ++c)
+      for (int k = 0; k < 128; ++k) {
+        Gm[(size_t)c * 256 + k] = 0.5 * ggw[(size_t)c * 128 + k];
+        Gm[(size_t)c * 256 + 128 + k] = gfw[(size_t)c * 128 + k];
+      }
+    frags16(Gm, 32, 256, reinterpret_cast<uint32_t*>(&h[m.gm_gf16]));
+    for (int k = 0; k < 128; ++k) {
+      h[m.gm_gb16 + k] = (float)(0.5 * ggb[k]);
+      h[m.gm_gb16 + 128 + k] = (float)gfb[k];
     }
   }
   if ((rc = copy("graph/dense1_w", m.gd1w, (size_t)m.gn * m.w1))) return rc;
@@ -723,8 +729,12 @@ static int graph_head(const fs_model& m, int P, int max_nodes, char* ws, const W
       q.wbias[ph] = m.P(m.gm_wb[ph]);
     }
     q.gfrag = reinterpret_cast<const uint32_t*>(m.P(m.gm_gf)); q.gbias = m.P(m.gm_gb);
-    for (int ph = 0; ph < 2; ++ph) q.wfrag16[ph] = reinterpret_cast<const uint32_t*>(m.P(m.gm_wf16[ph]));
+    for (int ph = 0; ph < 2; ++ph) {
+      q.wfrag16[ph] = reinterpret_cast<const uint32_t*>(m.P(m.gm_wf16[ph]));
+      q.wbias16[ph] = m.P(m.gm_wb16[ph]);
+    }
     q.gfrag16 = reinterpret_cast<const uint32_t*>(m.P(m.gm_gf16));
+    q.gbias16 = m.P(m.gm_gb16);
     q.k_steps[0] = m.d.k_cov; q.k_steps[1] = m.d.k_noncov;
     q.lat = g.lat; q.ld_lat = g.ld_lat; q.err = err;
     q.ids_padded = ids_padded ? 1 : 0;

@@ -26,42 +26,10 @@
 #include <cuda_fp16.h>
 
 #include "common.cuh"
+#include "gnn_mma.cuh"
 
 namespace fs {
 
-struct GnnMmaArgs {
-  const float* feats; int F;
-  const int64_t* node_off;
-  const int64_t* row_cov; const int32_t* deg_cov; const col_t* col_cov;     // row start + degree
-  const int64_t* row_ncov; const int32_t* deg_ncov; const col_t* col_ncov;
-  const float* we; const float* be;       // [F][24], [24]
-  const uint32_t* wfrag[2];               // per phase, see gnn_mma_phase_words()
-  const float* wbias[2];                  // per phase [72] = bz | br | bh
-  const uint32_t* gfrag;                  // gather fragments [2 hi/lo][2 kt][32 nt][32][2]
-  const uint32_t* wfrag16[2];             // fp16 phase fragments (SPLIT 2), [zr | hh] in the hi layout
-  const uint32_t* gfrag16;                // fp16 gather fragments (SPLIT 2)
-  const float* gbias;                     // [256] = bg | bf
-  int k_steps[2];
-  float* lat; int64_t ld_lat;             // [P][ld_lat], columns 0..127
-  const int32_t* err;
-  // ---- pocket factoring (fs_score_poses_cached); fact_cnt == nullptr: off.
-  // Pose p owns node slice [p*fact_stride, +fact_stride): ligand rows
-  // [0, nL), zero rows up to nLp = roundup16(nL), then the nA pocket atoms
-  // the ligand touches (ids fact_aff[]), whose covalent phase is taken from
-  // the pocket cache (cache_hcov) and whose untouched neighbours enter the
-  // pool through cache_T - sum(cache_f[affected]).
-  const int32_t* fact_cnt;                // [P][2] = (nL, nA)
-  int64_t fact_stride;
-  const int32_t* fact_aff;                // [P*fact_stride]
-  const int32_t* pose_target;             // [P]
-  const char* cache; int64_t cache_stride;
-  int64_t off_hcov, off_f, off_T, off_n;  // byte offsets inside one pocket's cache
-  // ---- pocket preparation dumps (plain path): node states after the covalent
-  // phase [P][dump_ld][24] and per-node pool terms [P][dump_ld][128]
-  float* dump_hcov; float* dump_f; int64_t dump_ld;
-  int heavy_cap;                          // rows of the heavy-sum buffer (set by launch_gnn_mma)
-  int ids_padded;                         // CSR rows padded to 4 ids with the zero row (graph_csr.cu)
-};
 
 constexpr int kMaxMmaWarps = 24;   // smem reduction buffers are sized for this many warps
 constexpr int kZrWords = 3 * 6 * 64;      // [kt][nt][lane][2] per hi/lo
@@ -70,6 +38,17 @@ constexpr int kPhaseWords = 2 * (kZrWords + kHhWords);   // hi and lo
 constexpr int kGatherWords = 2 * 2 * 32 * 64;
 
 int gnn_mma_phase_words() { return kPhaseWords; }
+
+#ifdef FS_GNN_PROF
+// per-warp clock64 timeline of the first 8 poses (profiling builds only):
+// [pose][slot][warp][4]; slot 0: (kernel start, embedding done), slots 1..9:
+// steps (loop start, loop end, items, gather cycles, claim cycles, GRU
+// cycles), slot 10: (pool done)
+__device__ unsigned long long fs_gnn_prof_buf[8][12][kMaxMmaWarps][6];
+#define GPROF(slot, k, v) do { if (blockIdx.x < 8) fs_gnn_prof_buf[blockIdx.x][slot][warp][k] = (v); } while (0)
+#else
+#define GPROF(slot, k, v) do {} while (0)
+#endif
 int gnn_mma_gather_words() { return kGatherWords; }
 
 __device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -187,14 +166,19 @@ __device__ __forceinline__ void mma_f16_c(float (&d)[4], const uint32_t (&a)[4],
 
 // KT0 = 1: k-tile 0 (neighbour sums s[0..15]) is all zero and skipped (the
 // products it would add are exact zeros)
-template <int SPLIT, int NT, int KT0 = 0>
-__device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[3][4], const uint32_t (&alo)[3][4],
-                                       const uint32_t* __restrict__ fhi, const uint32_t* __restrict__ flo,
-                                       int lane) {
+// LO0 = false: k-tile 0 has no lo term (its A is a single fp16 pass)
+// D starts at C (the gate biases of columns 8nt+2t, 8nt+2t+1 of both rows)
+template <int SPLIT, int NT, int KT0 = 0, bool LO0 = true>
+__device__ __forceinline__ void gemm48(float (&D)[NT][4], const float (&C)[NT][2], const uint32_t (&ahi)[3][4],
+                                       const uint32_t (&alo)[3][4], const uint32_t* __restrict__ fhi,
+                                       const uint32_t* __restrict__ flo, int lane) {
   // small cross terms first, the hi.hi product last, all into one
   // accumulator: NT independent chains keep the tensor pipe busy
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) D[nt][0] = D[nt][1] = D[nt][2] = D[nt][3] = 0.f;
+  for (int nt = 0; nt < NT; ++nt) {
+    D[nt][0] = D[nt][2] = C[nt][0];
+    D[nt][1] = D[nt][3] = C[nt][1];
+  }
 #pragma unroll
   for (int kt = KT0; kt < 3; ++kt)
 #pragma unroll
@@ -205,7 +189,7 @@ __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[
         mma_bf16(D[nt], alo[kt], bh.x, bh.y);
         mma_bf16(D[nt], ahi[kt], bl.x, bl.y);
       } else if (SPLIT == 2) {
-        mma_t<2>(D[nt], alo[kt], bh.x, bh.y);
+        if (LO0 || kt > 0) mma_t<2>(D[nt], alo[kt], bh.x, bh.y);
       }
       mma_t<SPLIT>(D[nt], ahi[kt], bh.x, bh.y);
     }
@@ -217,7 +201,29 @@ __device__ __forceinline__ void gemm48(float (&D)[NT][4], const uint32_t (&ahi)[
 // together.  Both forms read 8 (row, neighbour) pairs per 12 lane-instructions.
 constexpr int kHeavyDeg = 32;
 constexpr int kBins = kHeavyDeg + 1;
+// tensor-core gathers (VAR & 16) have no heavy rows: a finer degree sort
+// (degrees 0..kNatBins-2, the rest in one bin) keeps tile padding low
+constexpr int kNatBins = 129;   // (NAT: hist + cursors live in the unused heavy-sum buffer)
 constexpr int kCtlWords = 6 + 2 * kBins;
+
+// ---- tensor-core neighbour sums (VAR & 16) --------------------------------
+// S(16 rows x 24) += I16 . B, B = the c-th neighbour row of each of the tile's
+// 16 rows (fp16 gather copies, natural column order, 48-byte rows), loaded
+// k-major by ldmatrix.trans straight into m16n8k16 B fragments; the identity
+// A makes the tensor core an fp32 adder (one nonzero product per output), and
+// the D fragments are the A-fragment layout of the GRU GEMM.
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_f16_id(float (&d)[4], uint32_t ai, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%5,%4}, {%6,%7}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(ai), "r"(0u), "r"(b0), "r"(b1));
+}
 
 // Node-state rows are stored lane-major: the 6 columns lane t owns in the
 // MMA fragments ({2t,2t+1, 8+2t,9+2t, 16+2t,17+2t}) sit contiguously at
@@ -297,28 +303,28 @@ __device__ __forceinline__ void acc_row_at16(float (&q)[4], float (&d)[2], const
   fhadd2(q[2], q[3], v.y);
   fhadd2(d[0], d[1], w);
 }
-// gate activations of a pre-scaled pair (see fs_sigmoid_pre / fs_tanh_pre):
-// VAR & 1: one tanh.approx.f32 per value; VAR & 2: one tanh.approx.f16x2
-// per pair; else ex2 + rcp per value.  sigmoid(x) = (1 + tanh(x/2)) / 2.
-constexpr float kSigPre = -0.34657359027997264f;   // u = -log2(e) x  ->  x/2
-constexpr float kTanhPre = 0.34657359027997264f;   // u = 2 log2(e) x ->  x
+// gate activations of a pair.  VAR & 3 (the fp16 2-pass path): the fp16
+// weights are tanh-scaled (z, r by 1/2: sigmoid(x) = (1 + tanh(x/2)) / 2;
+// h~ by 1), VAR & 1: one tanh.approx.f32 per value, VAR & 2: one
+// tanh.approx.f16x2 per pair.  Else the ex2-scaled bf16 weights (see
+// fs_sigmoid_pre / fs_tanh_pre): ex2 + rcp per value.
 template <int VAR>
-__device__ __forceinline__ void gate_tanh2(float& u0, float& u1, float k) {
+__device__ __forceinline__ void gate_tanh2(float& u0, float& u1) {
   if constexpr (VAR & 2) {
-    const __half2 x = __floats2half2_rn(u0 * k, u1 * k);
+    const __half2 x = __floats2half2_rn(u0, u1);
     uint32_t xi = *reinterpret_cast<const uint32_t*>(&x), yi;
     asm("tanh.approx.f16x2 %0, %1;" : "=r"(yi) : "r"(xi));
     const float2 y = __half22float2(*reinterpret_cast<const __half2*>(&yi));
     u0 = y.x; u1 = y.y;
   } else {
-    asm("tanh.approx.f32 %0, %1;" : "=f"(u0) : "f"(u0 * k));
-    asm("tanh.approx.f32 %0, %1;" : "=f"(u1) : "f"(u1 * k));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(u0) : "f"(u0));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(u1) : "f"(u1));
   }
 }
 template <int VAR>
 __device__ __forceinline__ void gate_sigmoid2(float& u0, float& u1) {
   if constexpr ((VAR & 3) != 0) {
-    gate_tanh2<VAR>(u0, u1, kSigPre);
+    gate_tanh2<VAR>(u0, u1);
     ffma2(u0, u1, 0.5f, 0.5f, 0.5f, 0.5f);
   } else {
     sigmoid_pre2(u0, u1);
@@ -326,7 +332,7 @@ __device__ __forceinline__ void gate_sigmoid2(float& u0, float& u1) {
 }
 template <int VAR>
 __device__ __forceinline__ void gate_tanh_pre2(float& u0, float& u1) {
-  if constexpr ((VAR & 3) != 0) gate_tanh2<VAR>(u0, u1, kTanhPre);
+  if constexpr ((VAR & 3) != 0) gate_tanh2<VAR>(u0, u1);
   else tanh_pre2(u0, u1);
 }
 
@@ -346,6 +352,10 @@ __host__ __device__ constexpr int hpos(int c) { return 6 * ((c % 8) / 2) + 2 * (
 template <int SPLIT, bool FACT, int kMmaWarps, int VAR = 0>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a) {
   constexpr bool G16 = (VAR & 4) != 0;
+  constexpr bool NAT = (VAR & 16) != 0;   // tensor-core gathers, natural-order fp16 copies
+  static_assert(!NAT || (G16 && SPLIT == 2), "tensor-core gathers read the fp16 copies");
+  static_assert(SPLIT != 2 || (VAR & 3) != 0, "the fp16 weights are tanh-scaled");
+  constexpr int NB = NAT ? kNatBins : kBins;   // degree bins of the gather-order sort
   extern __shared__ __align__(16) float sm[];
   __shared__ int wcnt[kMmaWarps];
   const int p = blockIdx.x;
@@ -387,8 +397,24 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   uint16_t* PERM = reinterpret_cast<uint16_t*>(CTL + kCtlWords);   // gather order [npad]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  GPROF(0, 0, clock64());
 #define COLS(c) ((c) < 2 ? 2 * t + (c) : (c) < 4 ? 6 + 2 * t + (c) : 12 + 2 * t + (c))
 #define PCOL(c) (6 * t + (c))   // storage position of the lane's c-th state column
+  // NAT: both fp16 gather copies of a row from its 24 states in storage order
+  auto store_nat16 = [&](__half* d0, __half* d1, const float (&hv)[24]) {
+    uint32_t w[12];
+#pragma unroll
+    for (int c = 0; c < 24; c += 2) {
+      const __half2 v = __floats2half2_rn(hv[hpos(c)], hv[hpos(c + 1)]);
+      w[c / 2] = *reinterpret_cast<const uint32_t*>(&v);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const uint4 u = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+      reinterpret_cast<uint4*>(d0)[k] = u;
+      reinterpret_cast<uint4*>(d1)[k] = u;
+    }
+  };
 
   // ---- embedding h0 = tanh(X.We + be) into both buffers (rows a phase does
   // not update must read the same in either); padded rows and row npad are
@@ -403,6 +429,17 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     if (FACT && i >= nLp && i < n) {
       const float4* src = reinterpret_cast<const float4*>(
           reinterpret_cast<const float*>(pc + a.off_hcov) + static_cast<int64_t>(a.fact_aff[base + i]) * 24);
+      if constexpr (NAT) {
+        float hv[24];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const float4 v = src[k];
+          reinterpret_cast<float4*>(Hc + i * 24)[k] = v;
+          hv[4 * k] = v.x; hv[4 * k + 1] = v.y; hv[4 * k + 2] = v.z; hv[4 * k + 3] = v.w;
+        }
+        store_nat16(Gc + i * 24, Gn + i * 24, hv);
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
         const float4 v = src[k];
@@ -451,11 +488,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       else th = fs_tanh(acc[c]);
       hv[hpos(c)] = emb ? th : 0.f;
     }
+    if constexpr (NAT) store_nat16(Gc + i * 24, Gn + i * 24, hv);
 #pragma unroll
     for (int k = 0; k < 24; k += 4) {
       const float4 v = make_float4(hv[k], hv[k + 1], hv[k + 2], hv[k + 3]);
       *reinterpret_cast<float4*>(Hc + i * 24 + k) = v;
-      if constexpr (G16) {
+      if constexpr (NAT) {
+        // fp16 copies written above
+      } else if constexpr (G16) {
         const __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
         uint2 u;
         u.x = *reinterpret_cast<const uint32_t*>(&lo);
@@ -480,19 +520,33 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   // s k-tile is skipped in both GEMMs -- exact, the skipped products are zeros
   auto gru16 = [&](auto zs, const float (&sv)[2][6], const float (&h)[2][6], float (&hn)[2][6]) {
     constexpr int KT0 = decltype(zs)::value ? 1 : 0;
-    float bz[6], br[6], bh[6];
+    // biases as the GEMMs' initial accumulators: columns 8j+2t, 8j+2t+1,
+    // one 8-byte load per gate and n-tile
+    float cz[6][2];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {   // columns 8j+2t, 8j+2t+1: one 8-byte load per gate
-      const float2 z2 = *reinterpret_cast<const float2*>(WB + 8 * j + 2 * t);
-      const float2 r2 = *reinterpret_cast<const float2*>(WB + 24 + 8 * j + 2 * t);
-      const float2 h2 = *reinterpret_cast<const float2*>(WB + 48 + 8 * j + 2 * t);
-      bz[2 * j] = z2.x; bz[2 * j + 1] = z2.y; br[2 * j] = r2.x; br[2 * j + 1] = r2.y;
-      bh[2 * j] = h2.x; bh[2 * j + 1] = h2.y;
+    for (int j = 0; j < 6; ++j) {
+      const float2 b2 = *reinterpret_cast<const float2*>(WB + 8 * j + 2 * t);   // z | r
+      cz[j][0] = b2.x; cz[j][1] = b2.y;
     }
     uint32_t ahi[3][4], alo[3][4];
-    build_a48<SPLIT>(sv, h, ahi, alo);
+    // VAR & 32: the neighbour sums enter as one fp16 pass (no lo term); they
+    // are sums of fp16-rounded rows, so their own rounding is of the same order
+    constexpr bool SLO = !(SPLIT == 2 && (VAR & 32));
+    if constexpr (SLO) {
+      build_a48<SPLIT>(sv, h, ahi, alo);
+    } else {
+      const float z6[2][6] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}};
+      build_a48<SPLIT>(z6, h, ahi, alo);   // h hi/lo (s slots overwritten below)
+      put_a<5>(ahi[0], alo[0], 0, sv[0][0], sv[0][1]);
+      put_a<5>(ahi[0], alo[0], 1, sv[1][0], sv[1][1]);
+      put_a<5>(ahi[0], alo[0], 2, sv[0][2], sv[0][3]);
+      put_a<5>(ahi[0], alo[0], 3, sv[1][2], sv[1][3]);
+      put_a<5>(ahi[1], alo[1], 0, sv[0][4], sv[0][5]);
+      put_a<5>(ahi[1], alo[1], 1, sv[1][4], sv[1][5]);
+      alo[1][0] = 0u; alo[1][1] = 0u;
+    }
     float Dzr[6][4];
-    gemm48<SPLIT, 6, KT0>(Dzr, ahi, alo, zr_hi, zr_lo, lane);
+    gemm48<SPLIT, 6, KT0, SLO>(Dzr, cz, ahi, alo, zr_hi, zr_lo, lane);
     // D n-tile j holds (row g: cols 8j+2t, 8j+2t+1; row g+8: same)
     // elementwise work on column pairs (2j, 2j+1) with packed fp32 ops
     float z[2][6], rh[2][6];
@@ -502,10 +556,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       for (int rr = 0; rr < 2; ++rr) {
         const int c = 2 * j;
         z[rr][c] = Dzr[j][2 * rr]; z[rr][c + 1] = Dzr[j][2 * rr + 1];
-        fadd2(z[rr][c], z[rr][c + 1], bz[c], bz[c + 1]);
         gate_sigmoid2<VAR>(z[rr][c], z[rr][c + 1]);
         rh[rr][c] = Dzr[3 + j][2 * rr]; rh[rr][c + 1] = Dzr[3 + j][2 * rr + 1];
-        fadd2(rh[rr][c], rh[rr][c + 1], br[c], br[c + 1]);
         gate_sigmoid2<VAR>(rh[rr][c], rh[rr][c + 1]);
         fmul2(rh[rr][c], rh[rr][c + 1], h[rr][c], h[rr][c + 1]);
       }
@@ -516,15 +568,19 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     put_a<SPLIT>(ahi[2], alo[2], 1, rh[1][2], rh[1][3]);
     put_a<SPLIT>(ahi[2], alo[2], 2, rh[0][4], rh[0][5]);
     put_a<SPLIT>(ahi[2], alo[2], 3, rh[1][4], rh[1][5]);
-    float Dh[3][4];
-    gemm48<SPLIT, 3, KT0>(Dh, ahi, alo, hh_hi, hh_lo, lane);
+    float Dh[3][4], ch[3][2];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const float2 b2 = *reinterpret_cast<const float2*>(WB + 48 + 8 * j + 2 * t);
+      ch[j][0] = b2.x; ch[j][1] = b2.y;
+    }
+    gemm48<SPLIT, 3, KT0, SLO>(Dh, ch, ahi, alo, hh_hi, hh_lo, lane);
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         const int c = 2 * j;
         float u0 = Dh[j][2 * rr], u1 = Dh[j][2 * rr + 1];
-        fadd2(u0, u1, bh[c], bh[c + 1]);
         gate_tanh_pre2<VAR>(u0, u1);                       // hh
         fadd2(u0, u1, -h[rr][c], -h[rr][c + 1]);          // hh - h
         ffma2(u0, u1, z[rr][c], z[rr][c + 1], h[rr][c], h[rr][c + 1]);   // h + z (hh - h)
@@ -545,10 +601,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     FS_DCHECK(row >= 0 && row < npad, "gnn state row", row, npad);
     if constexpr (G16) {
       // fp32 state in place (read only by this warp), fp16 copy for the gathers
+      // (NAT: natural column order, columns 8j+2t, 8j+2t+1)
 #pragma unroll
       for (int c = 0; c < 6; c += 2) {
         *reinterpret_cast<float2*>(Hc + row * 24 + PCOL(c)) = make_float2(v[c], v[c + 1]);
-        *reinterpret_cast<__half2*>(Gn + row * 24 + PCOL(c)) = __floats2half2_rn(v[c], v[c + 1]);
+        *reinterpret_cast<__half2*>(Gn + row * 24 + (NAT ? 4 * c + 2 * t : PCOL(c))) = __floats2half2_rn(v[c], v[c + 1]);
       }
     } else {
 #pragma unroll
@@ -557,6 +614,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   };
 
   int gstep = 0;
+  GPROF(0, 1, clock64());
   for (int ph = 0; ph < 2; ++ph) {
     __syncthreads();
     if (!FACT && ph == 1 && a.dump_hcov) {   // pocket preparation: post-covalent states
@@ -570,8 +628,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     } else {
       for (int i = threadIdx.x; i < kPhaseWords; i += blockDim.x) WF[i] = a.wfrag[ph][i];
     }
-    for (int i = threadIdx.x; i < 72; i += blockDim.x) WB[i] = a.wbias[ph][i];
-    if (threadIdx.x < kBins) hist[threadIdx.x] = 0;
+    for (int i = threadIdx.x; i < 72; i += blockDim.x) WB[i] = (SPLIT == 2 ? a.wbias16 : a.wbias)[ph][i];
+    // NAT: bins and cursors in the (unused) heavy-sum buffer; per sorted slot
+    // the row's CSR offset and degree (SOFF, SDEG) in the upper half of the
+    // phase-fragment area (SPLIT 2 stages only the lower half)
+    int* hst = NAT ? reinterpret_cast<int*>(HS) : hist;
+    uint32_t* SOFF = WF + kZrWords + kHhWords;
+    uint16_t* SDEG = reinterpret_cast<uint16_t*>(SOFF + npad);
+    if (threadIdx.x < NB) hst[threadIdx.x] = 0;
     if (threadIdx.x < 4) CTL[threadIdx.x] = 0;
     const int64_t* rows = ph == 0 ? a.row_cov : a.row_ncov;
     const int32_t* degs = ph == 0 ? a.deg_cov : a.deg_ncov;
@@ -580,21 +644,41 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     // gather order: counting sort by degree, descending (bin 0: >= kHeavyDeg).
     // Where a row lands never changes its result (its sum has a fixed order,
     // its GRU row is independent of the tile's other rows).
+    constexpr int TOPB = NB - 1;   // bin of degree d: TOPB - min(d, TOPB)
     for (int i = threadIdx.x; i < prow; i += blockDim.x) {
       const int d = i < n ? degs[base + i] : 0;
-      atomicAdd(&hist[kHeavyDeg - min(d, kHeavyDeg)], 1);
+      atomicAdd(&hst[TOPB - min(d, TOPB)], 1);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int acc = 0;
-      for (int b = 0; b < kBins; ++b) { const int c = hist[b]; hist[kBins + b] = acc; acc += c; }
+    if (warp == 0) {   // exclusive scan of the bins into the cursors (5 bins per lane)
+      constexpr int PL = (NB + 31) / 32;
+      int loc[PL], sum = 0;
+#pragma unroll
+      for (int k = 0; k < PL; ++k) {
+        const int b = lane * PL + k;
+        loc[k] = b < NB ? hst[b] : 0;
+        sum += loc[k];
+      }
+      int inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      int run = inc - sum;
+#pragma unroll
+      for (int k = 0; k < PL; ++k) {
+        const int b = lane * PL + k;
+        if (b < NB) hst[NB + b] = run;
+        run += loc[k];
+      }
     }
     __syncthreads();
     // heavy rows beyond the HS capacity join the first light tiles; which rows
     // those are must be deterministic (heavy and light sums differ in order),
     // so bin 0 is placed in ascending row order by a block prefix count
-    const int nh = min(hist[1 + kBins] - hist[kBins], a.heavy_cap);
-    {
+    const int nh = NAT ? 0 : min(hist[1 + kBins] - hist[kBins], a.heavy_cap);
+    if constexpr (!NAT) {
       int run = 0;
       for (int i0 = 0; i0 < prow; i0 += blockDim.x) {
         const int i = i0 + threadIdx.x;
@@ -609,9 +693,18 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         __syncthreads();
       }
     }
+    const int64_t row0 = n > 0 ? rows[base] : 0;   // the pose's first CSR entry
+    const col_t* cbase = colv + row0;
     for (int i = threadIdx.x; i < prow; i += blockDim.x) {
       const int d = i < n ? degs[base + i] : 0;
-      if (d < kHeavyDeg) PERM[atomicAdd(&hist[kBins + kHeavyDeg - d], 1)] = static_cast<uint16_t>(i);
+      if (NAT || d < kHeavyDeg) {
+        const int pos = atomicAdd(&hst[NB + TOPB - min(d, TOPB)], 1);
+        PERM[pos] = static_cast<uint16_t>(i);
+        if constexpr (NAT) {
+          SOFF[pos] = i < n ? static_cast<uint32_t>(rows[base + i] - row0) : 0u;
+          SDEG[pos] = static_cast<uint16_t>(d);
+        }
+      }
     }
     __syncthreads();
     const int nlt = (prow - nh + 15) / 16, nht = (nh + 15) / 16;
@@ -639,7 +732,135 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       // (GRU from HS, after every heavy sum is in).
       int* ctr = CTL + (gstep & 1);
       int* hdone = CTL + 2 + (gstep & 1);
+#ifdef FS_GNN_PROF
+      long long prof_items = 0, prof_gather = 0, prof_claim = 0, prof_gru = 0;
+#endif
+      GPROF(1 + gstep, 0, clock64());
+      if constexpr (NAT) {
+        // 16 degree-sorted rows per item; lane l stages slot l & 15 (row k of
+        // the tile) for the ldmatrix loads and owns rows g and g+8 in the GRU.
+        // Chunk c = the c-th neighbour of every row of the tile; past a row's
+        // degree its slot reads the all-zero row npad.  The next item's row
+        // metadata and first CSR ids are fetched during this item's GRU, and
+        // long rows prefetch their ids two 8-chunk rounds ahead (lanes < 16
+        // load chunks q..q+3 of their row, lanes >= 16 chunks q+4..q+7).
+        const uint32_t gs = static_cast<uint32_t>(__cvta_generic_to_shared(Gc));
+        const uint32_t ga = gs + ((lane >> 4) << 4);   // columns 0-7 / 8-15
+        const uint32_t gcl = gs + 32;                  // columns 16-23
+        const uint32_t ai = (g == 2 * t ? 0x3C00u : 0u) | (g == 2 * t + 1 ? 0x3C000000u : 0u);   // I16 fragment
+        const uint32_t padw = static_cast<uint32_t>(npad) * 0x10001u;
+        const int kk = lane & 15, hi4 = (lane >> 4) << 2;
+        struct Meta { int rk, dk, ek, nch; const col_t* ck; };
+        // (instantiated for padded and packed CSR rows: no per-load branch)
+        auto nat_items = [&](auto padded) {
+        constexpr bool PADDED = decltype(padded)::value;
+        auto meta = [&](int it, Meta& m) {
+          const int ks = it * 16 + kk;
+          const bool in = it < nitems && ks < prow;
+          m.rk = in ? PERM[ks] : npad;
+          m.dk = in ? SDEG[ks] : 0;
+          m.ck = cbase + (in ? SOFF[ks] : 0u);
+          m.ek = PADDED ? ((m.dk + 3) & ~3) : m.dk;
+          m.nch = __reduce_max_sync(0xffffffffu, m.dk);
+        };
+        auto ld4 = [&](const Meta& m, int q) -> uint2 {   // ids q..q+3 of the lane's row
+          if constexpr (PADDED) return q < m.ek ? __ldg(reinterpret_cast<const uint2*>(m.ck + q)) : make_uint2(padw, padw);
+          uint32_t j[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            j[u] = q + u < m.ek ? static_cast<uint32_t>(__ldg(m.ck + q + u)) : static_cast<uint32_t>(npad);
+          return make_uint2(j[0] | (j[1] << 16), j[2] | (j[3] << 16));
+        };
+        Meta cur;
+        meta(warp, cur);
+        uint2 x = cur.nch > 0 ? ld4(cur, hi4) : make_uint2(padw, padw);
+        for (int item = warp; item < nitems;) {
+#ifdef FS_GNN_PROF
+          ++prof_items;
+          const long long prof_t0 = clock64();
+#endif
+          int next = 0;
+          if (lane == 0) next = atomicAdd(ctr, 1) + kMmaWarps;
+          next = __shfl_sync(0xffffffffu, next, 0);
+#ifdef FS_GNN_PROF
+          const long long prof_t1 = clock64() + (next == -7 ? 1 : 0);
+          prof_claim += prof_t1 - prof_t0;
+#endif
+          float D0[3][4], D1[3][4];
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) { D0[j][e] = 0.f; D1[j][e] = 0.f; }
+          auto pair = [&](uint32_t w) {   // chunks (w & 0xffff, w >> 16) into D0, D1
+            const uint32_t i0 = w & 0xffffu, i1 = w >> 16;
+            FS_DCHECK(i0 <= static_cast<uint32_t>(npad) && i1 <= static_cast<uint32_t>(npad), "gnn gather row",
+                      i0 > i1 ? i0 : i1, npad);
+            uint32_t b[4], c[4], e[4];
+            ldsm_x4_t(b, ga + i0 * 48u);
+            ldsm_x4_t(c, ga + i1 * 48u);
+            ldsm_x4_t(e, gcl + (lane < 16 ? i0 : i1) * 48u);
+            mma_f16_id(D0[0], ai, b[0], b[1]);
+            mma_f16_id(D0[1], ai, b[2], b[3]);
+            mma_f16_id(D0[2], ai, e[0], e[1]);
+            mma_f16_id(D1[0], ai, c[0], c[1]);
+            mma_f16_id(D1[1], ai, c[2], c[3]);
+            mma_f16_id(D1[2], ai, e[2], e[3]);
+          };
+          const int nch = cur.nch;
+          if (nch > 0) {
+            uint2 y = nch > 8 ? ld4(cur, 8 + hi4) : make_uint2(padw, padw);
+            for (int q = 0; q < nch; q += 8) {
+              const uint2 z = q + 16 < nch ? ld4(cur, q + 16 + hi4) : make_uint2(padw, padw);
+              uint2 o;
+              o.x = __shfl_xor_sync(0xffffffffu, x.x, 16);
+              o.y = __shfl_xor_sync(0xffffffffu, x.y, 16);
+              const uint2 wl = lane < 16 ? x : o, wh = lane < 16 ? o : x;   // chunks q..q+3, q+4..q+7
+              pair(wl.x);
+              if (q + 2 < nch) pair(wl.y);
+              if (q + 4 < nch) pair(wh.x);
+              if (q + 6 < nch) pair(wh.y);
+              x = y;
+              y = z;
+            }
+          }
+          float sv[2][6];
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            fadd2(D0[j][0], D0[j][1], D1[j][0], D1[j][1]);
+            fadd2(D0[j][2], D0[j][3], D1[j][2], D1[j][3]);
+            sv[0][2 * j] = D0[j][0]; sv[0][2 * j + 1] = D0[j][1];
+            sv[1][2 * j] = D0[j][2]; sv[1][2 * j + 1] = D0[j][3];
+          }
+#ifdef FS_GNN_PROF
+          const long long prof_t2 = clock64() + (sv[0][0] == 1e30f ? 1 : 0);
+          prof_gather += prof_t2 - prof_t1;
+#endif
+          const int r0 = __shfl_sync(0xffffffffu, cur.rk, g), r1 = __shfl_sync(0xffffffffu, cur.rk, g + 8);
+          Meta nm;   // the next item's rows and first ids, in flight during the GRU
+          meta(next, nm);
+          const uint2 nx = nm.nch > 0 ? ld4(nm, hi4) : make_uint2(padw, padw);
+          float h[2][6], hn[2][6];
+          load_h(r0, h[0]);
+          load_h(r1, h[1]);
+          if (nch == 0) gru16(std::true_type{}, sv, h, hn);
+          else gru16(std::false_type{}, sv, h, hn);
+          if (r0 < npad) store_hn(r0, hn[0]);
+          if (r1 < npad) store_hn(r1, hn[1]);
+#ifdef FS_GNN_PROF
+          prof_gru += clock64() - prof_t2 + (hn[0][0] == 1e30f ? 1 : 0);
+#endif
+          cur = nm;
+          x = nx;
+          item = next;
+        }
+        };
+        if (a.ids_padded) nat_items(std::true_type{});
+        else nat_items(std::false_type{});
+      } else
       for (int item = warp; item < nitems;) {
+#ifdef FS_GNN_PROF
+        ++prof_items;
+#endif
         // claim the next item now: the counter's round trip overlaps this
         // item's work (items are claimed in increasing order, so a warp
         // spinning in a heavy tile never holds an unprocessed heavy sum)
@@ -787,6 +1008,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         }
         item = __shfl_sync(0xffffffffu, next, 0);
       }
+#ifdef FS_GNN_PROF
+      GPROF(1 + gstep, 1, clock64());
+      GPROF(1 + gstep, 2, prof_items);
+      GPROF(1 + gstep, 3, prof_gather);
+      GPROF(1 + gstep, 4, prof_claim);
+      GPROF(1 + gstep, 5, prof_gru);
+#endif
       // counters of the next step (last used two steps ago)
       if (threadIdx.x == 0) { CTL[(gstep + 1) & 1] = 0; CTL[2 + ((gstep + 1) & 1)] = 0; }
       ++gstep;
@@ -808,13 +1036,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   // is large enough, else read them through L1
   // SPLIT 2: one fp16 fragment set (the layout of the bf16 "hi" half)
   const uint32_t* gsrc = SPLIT == 2 ? a.gfrag16 : a.gfrag;
-  const float* gb = a.gbias;
+  const float* gb = SPLIT == 2 ? a.gbias16 : a.gbias;
   if (hrows * 24 >= kGatherWords + 256) {
     uint32_t* gs = reinterpret_cast<uint32_t*>(Hn);
     const int gw = SPLIT == 2 ? kGatherWords / 2 : kGatherWords;
     for (int i = threadIdx.x; i < gw; i += blockDim.x) gs[i] = gsrc[i];
     float* gbs = reinterpret_cast<float*>(gs + kGatherWords);
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) gbs[i] = a.gbias[i];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) gbs[i] = gb[i];
     gsrc = gs;
     gb = gbs;
   }
@@ -898,13 +1126,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           gate_tanh_pre2<VAR>(Dv[2], Dv[3]);
         } else if constexpr (SPLIT == 2) {
           // one MUFU.TANH per activation (2^-10.7): sigmoid(x) = (1 + tanh(x/2)) / 2
-          // with u = -log2(e) x and v = 2 log2(e) x as staged
-          constexpr float kG = -0.34657359027997264f, kV = 0.34657359027997264f;   // 1/(2 log2 e)
+          // (the fp16 pool weights carry the 1/2)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             float tg, tv;
-            asm("tanh.approx.f32 %0, %1;" : "=f"(tg) : "f"(Dg[e] * kG));
-            asm("tanh.approx.f32 %0, %1;" : "=f"(tv) : "f"(Dv[e] * kV));
+            asm("tanh.approx.f32 %0, %1;" : "=f"(tg) : "f"(Dg[e]));
+            asm("tanh.approx.f32 %0, %1;" : "=f"(tv) : "f"(Dv[e]));
             Dg[e] = fmaf(0.5f, tg, 0.5f);
             Dv[e] = tv;
           }
@@ -962,6 +1189,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   if (threadIdx.x < 128) {
     float tot = 0.f;
     for (int w = 0; w < kMmaWarps; ++w) tot += RED[w * 128 + threadIdx.x];
+    GPROF(10, 0, clock64());
     if constexpr (FACT) {
       // untouched pocket nodes: cached total minus the touched ones' cached terms
       double corr = reinterpret_cast<const double*>(pc + a.off_T)[threadIdx.x];
@@ -973,6 +1201,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     }
   }
 }
+
+#ifdef FS_GNN_PROF
+extern "C" int fs_debug_gnn_prof(void* host) {
+  return cudaMemcpyFromSymbol(host, fs_gnn_prof_buf, sizeof(fs_gnn_prof_buf)) == cudaSuccess ? 0 : -3;
+}
+#endif
 
 static size_t gnn_smem_bytes(int max_nodes, int heavy_cap) {
   const int npad = (max_nodes + 15) / 16 * 16;
@@ -1009,7 +1243,16 @@ static int launch_gnn_mma_t(const GnnMmaArgs& a, int n_poses, size_t smem, cudaS
 // 20.1 ms per 16,384 poses) and one tanh.approx.f16x2 per pair of gate
 // activations (-> 19.8 ms); config-1 score error vs the oracle 1.03e-3 max
 // relative (1.33e-3 before; profiles/r02/gnn_variants.md)
-constexpr int kSplit2Var = 6;
+#ifdef FS_GNN_WARPS
+constexpr int kSplit2Warps = FS_GNN_WARPS;
+#else
+constexpr int kSplit2Warps = 20;
+#endif
+#ifdef FS_GNN_VAR
+constexpr int kSplit2Var = FS_GNN_VAR;   // A/B builds (build_native FS_BUILD_TAG / FS_EXTRA_FLAGS)
+#else
+constexpr int kSplit2Var = 53;
+#endif
 
 int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes, cudaStream_t st) {
   if (n_poses <= 0) return FS_OK;
@@ -1019,8 +1262,11 @@ int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes
   const size_t smem = gnn_mma_smem_bytes(max_nodes);
   if (split == 2) {
     if (!a.wfrag16[0] || !a.wfrag16[1] || !a.gfrag16) return FS_EINVAL;
-    if (a.fact_cnt) return launch_gnn_mma_t<2, true, 20, kSplit2Var>(a, n_poses, smem, st);
-    return launch_gnn_mma_t<2, false, 20, kSplit2Var>(a, n_poses, smem, st);
+    // NAT row metadata (6 bytes per row) in the upper half of the fragment area
+    if ((kSplit2Var & 16) && (max_nodes + 15) / 16 * 16 * 6 > (kPhaseWords - kZrWords - kHhWords) * 4)
+      return FS_ECAPACITY;
+    if (a.fact_cnt) return launch_gnn_mma_t<2, true, kSplit2Warps, kSplit2Var>(a, n_poses, smem, st);
+    return launch_gnn_mma_t<2, false, kSplit2Warps, kSplit2Var>(a, n_poses, smem, st);
   }
   if (split != 3) return FS_EINVAL;
   if (a.fact_cnt) return launch_gnn_mma_t<3, true, 20>(a, n_poses, smem, st);
