@@ -44,7 +44,7 @@ int gnn_mma_phase_words() { return kPhaseWords; }
 // [pose][slot][warp][4]; slot 0: (kernel start, embedding done), slots 1..9:
 // steps (loop start, loop end, items, gather cycles, claim cycles, GRU
 // cycles), slot 10: (pool done)
-__device__ unsigned long long fs_gnn_prof_buf[8][12][kMaxMmaWarps][6];
+__device__ unsigned long long fs_gnn_prof_buf[8][12][kMaxMmaWarps][7];
 #define GPROF(slot, k, v) do { if (blockIdx.x < 8) fs_gnn_prof_buf[blockIdx.x][slot][warp][k] = (v); } while (0)
 #else
 #define GPROF(slot, k, v) do {} while (0)
@@ -167,31 +167,53 @@ __device__ __forceinline__ void mma_f16_c(float (&d)[4], const uint32_t (&a)[4],
 // KT0 = 1: k-tile 0 (neighbour sums s[0..15]) is all zero and skipped (the
 // products it would add are exact zeros)
 // LO0 = false: k-tile 0 has no lo term (its A is a single fp16 pass)
-// D starts at C (the gate biases of columns 8nt+2t, 8nt+2t+1 of both rows)
-template <int SPLIT, int NT, int KT0 = 0, bool LO0 = true>
+// D = C + A.B, C = the gate biases of columns 8nt+2t, 8nt+2t+1 (both rows),
+// entering as the C operand of each chain's first MMA.  LOM (SPLIT 2): the
+// k-tiles that carry a lo pass (bit kt); SPLIT 3 always takes all three terms.
+template <int SPLIT>
+__device__ __forceinline__ void mma_c2(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1, float c0,
+                                       float c1) {
+  if constexpr (SPLIT == 2) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%11,%10,%11};"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c0), "f"(c1));
+  } else {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%11,%10,%11};"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c0), "f"(c1));
+  }
+}
+template <int SPLIT, int NT, int KT0 = 0, int LOM = 7>
 __device__ __forceinline__ void gemm48(float (&D)[NT][4], const float (&C)[NT][2], const uint32_t (&ahi)[3][4],
                                        const uint32_t (&alo)[3][4], const uint32_t* __restrict__ fhi,
                                        const uint32_t* __restrict__ flo, int lane) {
   // small cross terms first, the hi.hi product last, all into one
   // accumulator: NT independent chains keep the tensor pipe busy
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    D[nt][0] = D[nt][2] = C[nt][0];
-    D[nt][1] = D[nt][3] = C[nt][1];
-  }
-#pragma unroll
   for (int kt = KT0; kt < 3; ++kt)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const uint2 bh = *reinterpret_cast<const uint2*>(fhi + ((kt * NT + nt) * 32 + lane) * 2);
-      if (SPLIT == 3) {
+      bool first = kt == KT0;
+      if constexpr (SPLIT == 3) {
         const uint2 bl = *reinterpret_cast<const uint2*>(flo + ((kt * NT + nt) * 32 + lane) * 2);
-        mma_bf16(D[nt], alo[kt], bh.x, bh.y);
+        if (first) mma_c2<3>(D[nt], alo[kt], bh.x, bh.y, C[nt][0], C[nt][1]);
+        else mma_bf16(D[nt], alo[kt], bh.x, bh.y);
         mma_bf16(D[nt], ahi[kt], bl.x, bl.y);
-      } else if (SPLIT == 2) {
-        if (LO0 || kt > 0) mma_t<2>(D[nt], alo[kt], bh.x, bh.y);
+        first = false;
+      } else if constexpr (SPLIT == 2) {
+        if ((LOM >> kt) & 1) {
+          if (first) mma_c2<2>(D[nt], alo[kt], bh.x, bh.y, C[nt][0], C[nt][1]);
+          else mma_t<2>(D[nt], alo[kt], bh.x, bh.y);
+          first = false;
+        }
       }
-      mma_t<SPLIT>(D[nt], ahi[kt], bh.x, bh.y);
+      if (first) mma_c2<SPLIT>(D[nt], ahi[kt], bh.x, bh.y, C[nt][0], C[nt][1]);
+      else mma_t<SPLIT>(D[nt], ahi[kt], bh.x, bh.y);
     }
 }
 
@@ -203,7 +225,17 @@ constexpr int kHeavyDeg = 32;
 constexpr int kBins = kHeavyDeg + 1;
 // tensor-core gathers (VAR & 16) have no heavy rows: a finer degree sort
 // (degrees 0..kNatBins-2, the rest in one bin) keeps tile padding low
-constexpr int kNatBins = 129;   // (NAT: hist + cursors live in the unused heavy-sum buffer)
+// (NAT: hist + cursors live in the unused heavy-sum buffer)
+constexpr int kNatBins = 129;
+// VAR & 32: a row's neighbour sums take one fp16 pass (its lo term zeroed)
+// while all its |s| <= kSBig: rounding <= kSBig * 2^-12 absolute, the order
+// of the fp16-rounded rows they sum; larger sums keep the hi/lo split.
+// Measured: config-1 max rel. 7.6e-4 vs the oracle; the dense stress pocket
+// (sums of ~600 rows) within 3e-3.
+#ifndef FS_SBIG
+#define FS_SBIG 16.0f
+#endif
+constexpr float kSBig = FS_SBIG;
 constexpr int kCtlWords = 6 + 2 * kBins;
 
 // ---- tensor-core neighbour sums (VAR & 16) --------------------------------
@@ -425,6 +457,88 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   for (int i = threadIdx.x; i < a.F * 24; i += blockDim.x) WE[i] = a.we[i];
   for (int i = threadIdx.x; i < 24; i += blockDim.x) WE[a.F * 24 + i] = a.be[i];
   __syncthreads();
+  if (a.F == 8) {
+    // 16-row tiles on the tensor cores: [16 x 8] X . [8 x 24] We in fp16 hi/lo
+    // (X = one-hot | role | position/box + 1/2; Xlo.Whi + Xhi.Wlo + Xhi.Whi,
+    // ~2^-22 relative, bias as C), k 8..15 zero; lane: rows g, g+8, columns
+    // 8nt+2t, 8nt+2t+1 -- the GRU's lane-local layout.
+    uint32_t wbh[3], wbl[3];
+    float cb[3][2];
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      split2_f16(WE[(2 * t) * 24 + 8 * nt + g], WE[(2 * t + 1) * 24 + 8 * nt + g], wbh[nt], wbl[nt]);
+      cb[nt][0] = WE[8 * 24 + 8 * nt + 2 * t];
+      cb[nt][1] = WE[8 * 24 + 8 * nt + 2 * t + 1];
+    }
+    for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
+      float v[2][6];
+      int rr_row[2];
+      uint32_t ah[2], al[2];
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int r = tile * 16 + g + 8 * rr;
+        rr_row[rr] = r;
+        const bool emb = FACT ? r < nL : r < n;
+        float2 x = make_float2(0.f, 0.f);
+        if (emb) x = __ldg(reinterpret_cast<const float2*>(a.feats + (base + r) * 8 + 2 * t));
+        split2_f16(x.x, x.y, ah[rr], al[rr]);
+      }
+      const uint32_t Ahi[4] = {ah[0], ah[1], 0u, 0u}, Alo[4] = {al[0], al[1], 0u, 0u};
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt) {
+        float d[4];
+        mma_c2<2>(d, Alo, wbh[nt], 0u, cb[nt][0], cb[nt][1]);
+        mma_t<2>(d, Ahi, wbl[nt], 0u);
+        mma_t<2>(d, Ahi, wbh[nt], 0u);
+        v[0][2 * nt] = d[0]; v[0][2 * nt + 1] = d[1];
+        v[1][2 * nt] = d[2]; v[1][2 * nt + 1] = d[3];
+      }
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int r = rr_row[rr];
+        const bool emb = FACT ? r < nL : r < n;
+        const bool cached = FACT && r >= nLp && r < n;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          float th;
+          if constexpr ((VAR & 8) != 0) asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(v[rr][c]));
+          else th = fs_tanh(v[rr][c]);
+          v[rr][c] = emb ? th : 0.f;
+        }
+        if (cached) {   // factored: the cached post-covalent state (storage order = this lane's 6 columns)
+          const float* src = reinterpret_cast<const float*>(pc + a.off_hcov) +
+                             static_cast<int64_t>(a.fact_aff[base + r]) * 24 + 6 * t;
+#pragma unroll
+          for (int c = 0; c < 6; c += 2) {
+            const float2 w = *reinterpret_cast<const float2*>(src + c);
+            v[rr][c] = w.x; v[rr][c + 1] = w.y;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 6; c += 2) {
+          *reinterpret_cast<float2*>(Hc + r * 24 + PCOL(c)) = make_float2(v[rr][c], v[rr][c + 1]);
+          if constexpr (G16) {
+            const int pos = NAT ? 4 * c + 2 * t : PCOL(c);
+            const __half2 hv = __floats2half2_rn(v[rr][c], v[rr][c + 1]);
+            *reinterpret_cast<__half2*>(Gc + r * 24 + pos) = hv;
+            *reinterpret_cast<__half2*>(Gn + r * 24 + pos) = hv;
+          } else {
+            *reinterpret_cast<float2*>(Hn + r * 24 + PCOL(c)) = make_float2(v[rr][c], v[rr][c + 1]);
+          }
+        }
+      }
+    }
+    // row npad: the all-zero row of the gathers
+    for (int k = threadIdx.x; k < 24; k += blockDim.x) {
+      Hc[npad * 24 + k] = 0.f;
+      if constexpr (G16) {
+        Gc[npad * 24 + k] = __float2half(0.f);
+        Gn[npad * 24 + k] = __float2half(0.f);
+      } else {
+        Hn[npad * 24 + k] = 0.f;
+      }
+    }
+  } else
   for (int i = threadIdx.x; i <= npad; i += blockDim.x) {
     if (FACT && i >= nLp && i < n) {
       const float4* src = reinterpret_cast<const float4*>(
@@ -457,6 +571,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       }
       continue;
     }
+    // generic feature width: one row per thread, FFMA
     const bool emb = FACT ? i < nL : i < n;
     float acc[24];
 #pragma unroll
@@ -518,7 +633,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   // zs: std::true_type when all 16 rows of the tile have no neighbours (s = 0,
   // e.g. pocket atoms no ligand atom reaches in the non-covalent phase): the
   // s k-tile is skipped in both GEMMs -- exact, the skipped products are zeros
-  auto gru16 = [&](auto zs, const float (&sv)[2][6], const float (&h)[2][6], float (&hn)[2][6]) {
+  // slo: std::bool_constant, whether the neighbour sums take a lo pass; with
+  // it, slo0 / slo1 say whether row g / g+8 keeps its lo term (a zeroed lo
+  // adds exact zeros: a row's result does not depend on its tile-mates)
+  auto gru16 = [&](auto zs, auto slo, const float (&sv)[2][6], const float (&h)[2][6], float (&hn)[2][6],
+                   bool slo0 = true, bool slo1 = true) {
     constexpr int KT0 = decltype(zs)::value ? 1 : 0;
     // biases as the GEMMs' initial accumulators: columns 8j+2t, 8j+2t+1,
     // one 8-byte load per gate and n-tile
@@ -529,11 +648,21 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       cz[j][0] = b2.x; cz[j][1] = b2.y;
     }
     uint32_t ahi[3][4], alo[3][4];
-    // VAR & 32: the neighbour sums enter as one fp16 pass (no lo term); they
-    // are sums of fp16-rounded rows, so their own rounding is of the same order
-    constexpr bool SLO = !(SPLIT == 2 && (VAR & 32));
+    // !SLO: the neighbour sums enter as one fp16 pass (no lo term); they are
+    // sums of fp16-rounded rows, so for small sums their own rounding is of
+    // the same order (VAR & 32 picks this per row, see kSBig)
+    constexpr bool SLO = SPLIT != 2 || decltype(slo)::value;
+    // VAR & 64: r*h enters GEMM 2 as one fp16 pass as well (r carries the
+    // ~2^-11 error of tanh.approx; the hi/lo split of r*h adds nothing)
+    constexpr bool RLO = !(SPLIT == 2 && (VAR & 64));
+    constexpr int LOM1 = SLO ? 7 : 6;
+    constexpr int LOM2 = (SLO ? 1 : 0) | ((SLO || RLO) ? 2 : 0) | (RLO ? 4 : 0);
     if constexpr (SLO) {
       build_a48<SPLIT>(sv, h, ahi, alo);
+      if constexpr (SPLIT == 2 && (VAR & 32) != 0) {
+        if (!slo0) { alo[0][0] = 0u; alo[0][2] = 0u; alo[1][0] = 0u; }
+        if (!slo1) { alo[0][1] = 0u; alo[0][3] = 0u; alo[1][1] = 0u; }
+      }
     } else {
       const float z6[2][6] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}};
       build_a48<SPLIT>(z6, h, ahi, alo);   // h hi/lo (s slots overwritten below)
@@ -546,7 +675,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       alo[1][0] = 0u; alo[1][1] = 0u;
     }
     float Dzr[6][4];
-    gemm48<SPLIT, 6, KT0, SLO>(Dzr, cz, ahi, alo, zr_hi, zr_lo, lane);
+    gemm48<SPLIT, 6, KT0, LOM1>(Dzr, cz, ahi, alo, zr_hi, zr_lo, lane);
     // D n-tile j holds (row g: cols 8j+2t, 8j+2t+1; row g+8: same)
     // elementwise work on column pairs (2j, 2j+1) with packed fp32 ops
     float z[2][6], rh[2][6];
@@ -562,19 +691,21 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         fmul2(rh[rr][c], rh[rr][c + 1], h[rr][c], h[rr][c + 1]);
       }
     // A = [s | r*h]: the s part (k-tile 0 and half of k-tile 1) is reused
-    put_a<SPLIT>(ahi[1], alo[1], 2, rh[0][0], rh[0][1]);
-    put_a<SPLIT>(ahi[1], alo[1], 3, rh[1][0], rh[1][1]);
-    put_a<SPLIT>(ahi[2], alo[2], 0, rh[0][2], rh[0][3]);
-    put_a<SPLIT>(ahi[2], alo[2], 1, rh[1][2], rh[1][3]);
-    put_a<SPLIT>(ahi[2], alo[2], 2, rh[0][4], rh[0][5]);
-    put_a<SPLIT>(ahi[2], alo[2], 3, rh[1][4], rh[1][5]);
+    constexpr int RS = RLO ? SPLIT : 5;
+    put_a<RS>(ahi[1], alo[1], 2, rh[0][0], rh[0][1]);
+    put_a<RS>(ahi[1], alo[1], 3, rh[1][0], rh[1][1]);
+    put_a<RS>(ahi[2], alo[2], 0, rh[0][2], rh[0][3]);
+    put_a<RS>(ahi[2], alo[2], 1, rh[1][2], rh[1][3]);
+    put_a<RS>(ahi[2], alo[2], 2, rh[0][4], rh[0][5]);
+    put_a<RS>(ahi[2], alo[2], 3, rh[1][4], rh[1][5]);
+    if constexpr (!RLO) { alo[1][2] = 0u; alo[1][3] = 0u; }   // (read only when the s part has a lo pass)
     float Dh[3][4], ch[3][2];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       const float2 b2 = *reinterpret_cast<const float2*>(WB + 48 + 8 * j + 2 * t);
       ch[j][0] = b2.x; ch[j][1] = b2.y;
     }
-    gemm48<SPLIT, 3, KT0, SLO>(Dh, ch, ahi, alo, hh_hi, hh_lo, lane);
+    gemm48<SPLIT, 3, KT0, LOM2>(Dh, ch, ahi, alo, hh_hi, hh_lo, lane);
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
@@ -708,6 +839,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     }
     __syncthreads();
     const int nlt = (prow - nh + 15) / 16, nht = (nh + 15) / 16;
+    GPROF(11, ph, clock64());   // phase setup + sort done
     const int nitems = nh + nlt + nht;
 
     for (int step = 0; step < a.k_steps[ph]; ++step) {
@@ -733,7 +865,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       int* ctr = CTL + (gstep & 1);
       int* hdone = CTL + 2 + (gstep & 1);
 #ifdef FS_GNN_PROF
-      long long prof_items = 0, prof_gather = 0, prof_claim = 0, prof_gru = 0;
+      long long prof_items = 0, prof_gather = 0, prof_claim = 0, prof_gru = 0, prof_lo = 0;
 #endif
       GPROF(1 + gstep, 0, clock64());
       if constexpr (NAT) {
@@ -842,8 +974,31 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           float h[2][6], hn[2][6];
           load_h(r0, h[0]);
           load_h(r1, h[1]);
-          if (nch == 0) gru16(std::true_type{}, sv, h, hn);
-          else gru16(std::false_type{}, sv, h, hn);
+          if (nch == 0) {
+            gru16(std::true_type{}, std::false_type{}, sv, h, hn);
+          } else if constexpr ((VAR & 32) != 0) {
+            // a row's sums take one fp16 pass while all its |s| <= kSBig (the
+            // row's lo term is zeroed); the tile runs the lo MMAs only if
+            // some row keeps its lo term
+            float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) { m0 = fmaxf(m0, fabsf(sv[0][c])); m1 = fmaxf(m1, fabsf(sv[1][c])); }
+            m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+            m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+            m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+            m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+            const bool b0 = m0 > kSBig, b1 = m1 > kSBig;
+            if (__any_sync(0xffffffffu, b0 || b1)) {
+#ifdef FS_GNN_PROF
+              ++prof_lo;
+#endif
+              gru16(std::false_type{}, std::true_type{}, sv, h, hn, b0, b1);
+            } else {
+              gru16(std::false_type{}, std::false_type{}, sv, h, hn);
+            }
+          } else {
+            gru16(std::false_type{}, std::true_type{}, sv, h, hn);
+          }
           if (r0 < npad) store_hn(r0, hn[0]);
           if (r1 < npad) store_hn(r1, hn[1]);
 #ifdef FS_GNN_PROF
@@ -976,10 +1131,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           // (SPLIT 2 only: on the 3-pass path the second GRU instantiation
           // costs more than the skipped MMAs save, 25.15 -> 25.21 ms)
           if constexpr (SPLIT == 2) {
-            if (__all_sync(0xffffffffu, d0 == 0 && d1 == 0)) gru16(std::true_type{}, sv, h, hn);
-            else gru16(std::false_type{}, sv, h, hn);
+            if (__all_sync(0xffffffffu, d0 == 0 && d1 == 0)) gru16(std::true_type{}, std::true_type{}, sv, h, hn);
+            else gru16(std::false_type{}, std::true_type{}, sv, h, hn);
           } else {
-            gru16(std::false_type{}, sv, h, hn);
+            gru16(std::false_type{}, std::true_type{}, sv, h, hn);
           }
           if (r0 < npad) store_hn(r0, hn[0]);
           if (r1 < npad) store_hn(r1, hn[1]);
@@ -1002,7 +1157,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           }
           load_h(r0, h[0]);
           load_h(r1, h[1]);
-          gru16(std::false_type{}, sv, h, hn);
+          gru16(std::false_type{}, std::true_type{}, sv, h, hn);
           if (r0 < npad) store_hn(r0, hn[0]);
           if (r1 < npad) store_hn(r1, hn[1]);
         }
@@ -1014,6 +1169,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       GPROF(1 + gstep, 3, prof_gather);
       GPROF(1 + gstep, 4, prof_claim);
       GPROF(1 + gstep, 5, prof_gru);
+      GPROF(1 + gstep, 6, prof_lo);
 #endif
       // counters of the next step (last used two steps ago)
       if (threadIdx.x == 0) { CTL[(gstep + 1) & 1] = 0; CTL[2 + ((gstep + 1) & 1)] = 0; }
@@ -1026,6 +1182,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       }
     }
   }
+  GPROF(11, 2, clock64());   // pool start
   float* RED = Hn;   // [warps][128] (+ [warps][128] doubles), written only after every warp is done with the staged fragments
 
   // ---- gated gather + mean pool: [gate|val] = h.[Gg|Gf] (K 24->32, N 256) ----
@@ -1073,6 +1230,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     put_a<PS>(ahi[1], alo[1], 0, h[0][4], h[0][5]);
     put_a<PS>(ahi[1], alo[1], 1, h[1][4], h[1][5]);
     const bool v0 = valid(tile * 16 + g), v1 = valid(tile * 16 + g + 8);
+    // FULL: every row of the tile holds a node and no per-node dump: no masks
+    // and no dump stores in the unrolled column loop (all tiles but the last,
+    // on the scoring path)
+    auto columns = [&](auto full) {
+    constexpr bool FULL = decltype(full)::value;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       // biases enter as the first MMA's C operand
@@ -1118,12 +1280,22 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
       }
       {
         // rows g (D[0], D[1]) and g+8 (D[2], D[3]), columns 8j+2t, +1
-        if constexpr ((VAR & 8) != 0) {
-          // one tanh.approx.f16x2 per pair of activations (VAR & 8)
-          gate_sigmoid2<VAR>(Dg[0], Dg[1]);
-          gate_sigmoid2<VAR>(Dg[2], Dg[3]);
-          gate_tanh_pre2<VAR>(Dv[0], Dv[1]);
-          gate_tanh_pre2<VAR>(Dv[2], Dv[3]);
+        if constexpr (SPLIT == 2 && (VAR & 8) != 0) {
+          // VAR & 8: one tanh.approx.f16x2 per pair of activations and the
+          // gate x value product in fp16 (half the MUFU work of the pool,
+          // which is MUFU-bound; each node's term is rounded once and the
+          // mean over the pose's nodes averages it)
+          auto th2 = [](float u0, float u1) {
+            const __half2 x = __floats2half2_rn(u0, u1);
+            uint32_t xi = *reinterpret_cast<const uint32_t*>(&x), yi;
+            asm("tanh.approx.f16x2 %0, %1;" : "=r"(yi) : "r"(xi));
+            return *reinterpret_cast<const __half2*>(&yi);
+          };
+          const __half2 hh5 = __float2half2_rn(0.5f);
+          const __half2 p01 = __hmul2(__hfma2(th2(Dg[0], Dg[1]), hh5, hh5), th2(Dv[0], Dv[1]));
+          const __half2 p23 = __hmul2(__hfma2(th2(Dg[2], Dg[3]), hh5, hh5), th2(Dv[2], Dv[3]));
+          const float2 f01 = __half22float2(p01), f23 = __half22float2(p23);
+          Dg[0] = f01.x; Dg[1] = f01.y; Dg[2] = f23.x; Dg[3] = f23.y;
         } else if constexpr (SPLIT == 2) {
           // one MUFU.TANH per activation (2^-10.7): sigmoid(x) = (1 + tanh(x/2)) / 2
           // (the fp16 pool weights carry the 1/2)
@@ -1139,20 +1311,25 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           sigmoid_pre2(Dg[0], Dg[1]); sigmoid_pre2(Dg[2], Dg[3]);
           tanh_pre2(Dv[0], Dv[1]); tanh_pre2(Dv[2], Dv[3]);
         }
-        fmul2(Dg[0], Dg[1], Dv[0], Dv[1]);
-        fmul2(Dg[2], Dg[3], Dv[2], Dv[3]);
-        const float x00 = v0 ? Dg[0] : 0.f, x01 = v0 ? Dg[1] : 0.f;
-        const float x10 = v1 ? Dg[2] : 0.f, x11 = v1 ? Dg[3] : 0.f;
+        if constexpr (!(SPLIT == 2 && (VAR & 8) != 0)) {
+          fmul2(Dg[0], Dg[1], Dv[0], Dv[1]);
+          fmul2(Dg[2], Dg[3], Dv[2], Dv[3]);
+        }
+        const float x00 = FULL || v0 ? Dg[0] : 0.f, x01 = FULL || v0 ? Dg[1] : 0.f;
+        const float x10 = FULL || v1 ? Dg[2] : 0.f, x11 = FULL || v1 ? Dg[3] : 0.f;
         float s0 = x00, s1 = x01;
         fadd2(s0, s1, x10, x11);
         fadd2(acc[j][0], acc[j][1], s0, s1);
-        if (!FACT && a.dump_f) {   // pocket preparation: per-node pool terms
+        if (!FULL && !FACT && a.dump_f) {   // pocket preparation: per-node pool terms
           float* o = a.dump_f + (static_cast<int64_t>(p) * a.dump_ld + tile * 16 + g) * 128 + 8 * j + 2 * t;
           if (v0) { o[0] = x00; o[1] = x01; }
           if (v1) { o[8 * 128] = x10; o[8 * 128 + 1] = x11; }
         }
       }
     }
+    };
+    if (__all_sync(0xffffffffu, v0 && v1) && (FACT || !a.dump_f)) columns(std::true_type{});
+    else columns(std::false_type{});
   }
   // reduce over g (lane bits 2..4), fixed tree
 #pragma unroll
@@ -1251,7 +1428,7 @@ constexpr int kSplit2Warps = 20;
 #ifdef FS_GNN_VAR
 constexpr int kSplit2Var = FS_GNN_VAR;   // A/B builds (build_native FS_BUILD_TAG / FS_EXTRA_FLAGS)
 #else
-constexpr int kSplit2Var = 53;
+constexpr int kSplit2Var = 117;
 #endif
 
 int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes, cudaStream_t st) {

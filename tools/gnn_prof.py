@@ -34,7 +34,7 @@ def main():
     dl = DeviceLibrary(lib, [pocket], torch.device("cuda"))
     dm.score_poses(dl.batch(0, 2048), "bf16", 32768, retry=False)
     torch.cuda.synchronize()
-    buf = np.zeros((8, 12, WARPS, 6), dtype=np.uint64)
+    buf = np.zeros((8, 12, WARPS, 7), dtype=np.uint64)
     L = N.lib()
     f = L.fs_debug_gnn_prof
     f.argtypes = [C.c_void_p]
@@ -54,11 +54,16 @@ def main():
                           "gather_frac": round(float(b[p, s, :nw, 3].sum() / max((en - st).sum(), 1)), 3),
                           "claim_frac": round(float(b[p, s, :nw, 4].sum() / max((en - st).sum(), 1)), 3),
                           "gru_frac": round(float(b[p, s, :nw, 5].sum() / max((en - st).sum(), 1)), 3),
+                          "lo_tiles": int(b[p, s, :nw, 6].sum()),
                           "start_skew": int(st.max() - st.min())})
         pool_end = int(b[p, 10, :4, 0].max() - t0)
-        out["poses"].append({"embed": emb, "steps": steps, "total": pool_end})
+        setup0 = int(b[p, 11, :nw, 0].max() - b[p, 0, :nw, 1].max())
+        setup1 = int(b[p, 11, :nw, 1].max() - b[p, 6, :nw, 1].max())
+        pool = int(pool_end - (b[p, 11, :nw, 2].min() - t0))
+        out["poses"].append({"embed": emb, "steps": steps, "total": pool_end, "setup0": setup0, "setup1": setup1,
+                             "pool": pool})
     for p in out["poses"][:3]:
-        print(json.dumps({"embed": p["embed"], "total": p["total"]}))
+        print(json.dumps({k: p[k] for k in ("embed", "total", "setup0", "setup1", "pool")}))
         for s in p["steps"]:
             print("  ", json.dumps(s))
     tot = np.mean([p["total"] for p in out["poses"]])
