@@ -1423,7 +1423,7 @@ static int launch_gnn_mma_t(const GnnMmaArgs& a, int n_poses, size_t smem, cudaS
 #ifdef FS_GNN_WARPS
 constexpr int kSplit2Warps = FS_GNN_WARPS;
 #else
-constexpr int kSplit2Warps = 20;
+constexpr int kSplit2Warps = 16;
 #endif
 #ifdef FS_GNN_VAR
 constexpr int kSplit2Var = FS_GNN_VAR;   // A/B builds (build_native FS_BUILD_TAG / FS_EXTRA_FLAGS)
