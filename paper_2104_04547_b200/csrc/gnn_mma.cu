@@ -256,6 +256,14 @@ __device__ __forceinline__ void mma_f16_id(float (&d)[4], uint32_t ai, uint32_t 
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(ai), "r"(0u), "r"(b0), "r"(b1));
 }
+// the same with C = 0 (a chain's first chunk: no accumulator zeroing)
+__device__ __forceinline__ void mma_f16_id0(float (&d)[4], uint32_t ai, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%5,%4}, {%6,%7}, "
+      "{%8,%8,%8,%8};"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(ai), "r"(0u), "r"(b0), "r"(b1), "f"(0.0f));
+}
 
 // Node-state rows are stored lane-major: the 6 columns lane t owns in the
 // MMA fragments ({2t,2t+1, 8+2t,9+2t, 16+2t,17+2t}) sit contiguously at
@@ -905,7 +913,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         };
         Meta cur;
         meta(warp, cur);
-        uint2 x = cur.nch > 0 ? ld4(cur, hi4) : make_uint2(padw, padw);
+        // first ids of an item: chunks 0..3 in every lane for rows of <= 4
+        // chunks, else lanes >= 16 take chunks 4..7
+        auto ld_first = [&](const Meta& m) -> uint2 {
+          if (m.nch <= 0) return make_uint2(padw, padw);
+          return ld4(m, m.nch > 4 ? hi4 : 0);
+        };
+        uint2 x = ld_first(cur);
         for (int item = warp; item < nitems;) {
 #ifdef FS_GNN_PROF
           ++prof_items;
@@ -919,11 +933,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           prof_claim += prof_t1 - prof_t0;
 #endif
           float D0[3][4], D1[3][4];
-#pragma unroll
-          for (int j = 0; j < 3; ++j)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) { D0[j][e] = 0.f; D1[j][e] = 0.f; }
-          auto pair = [&](uint32_t w) {   // chunks (w & 0xffff, w >> 16) into D0, D1
+          // chunks (w & 0xffff, w >> 16) into D0, D1; FIRST: the chains' first MMAs (C = 0)
+          auto pair = [&](uint32_t w, auto first) {
             const uint32_t i0 = w & 0xffffu, i1 = w >> 16;
             FS_DCHECK(i0 <= static_cast<uint32_t>(npad) && i1 <= static_cast<uint32_t>(npad), "gnn gather row",
                       i0 > i1 ? i0 : i1, npad);
@@ -931,28 +942,58 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             ldsm_x4_t(b, ga + i0 * 48u);
             ldsm_x4_t(c, ga + i1 * 48u);
             ldsm_x4_t(e, gcl + (lane < 16 ? i0 : i1) * 48u);
-            mma_f16_id(D0[0], ai, b[0], b[1]);
-            mma_f16_id(D0[1], ai, b[2], b[3]);
-            mma_f16_id(D0[2], ai, e[0], e[1]);
-            mma_f16_id(D1[0], ai, c[0], c[1]);
-            mma_f16_id(D1[1], ai, c[2], c[3]);
-            mma_f16_id(D1[2], ai, e[2], e[3]);
+            if constexpr (decltype(first)::value) {
+              mma_f16_id0(D0[0], ai, b[0], b[1]);
+              mma_f16_id0(D0[1], ai, b[2], b[3]);
+              mma_f16_id0(D0[2], ai, e[0], e[1]);
+              mma_f16_id0(D1[0], ai, c[0], c[1]);
+              mma_f16_id0(D1[1], ai, c[2], c[3]);
+              mma_f16_id0(D1[2], ai, e[2], e[3]);
+            } else {
+              mma_f16_id(D0[0], ai, b[0], b[1]);
+              mma_f16_id(D0[1], ai, b[2], b[3]);
+              mma_f16_id(D0[2], ai, e[0], e[1]);
+              mma_f16_id(D1[0], ai, c[0], c[1]);
+              mma_f16_id(D1[1], ai, c[2], c[3]);
+              mma_f16_id(D1[2], ai, e[2], e[3]);
+            }
           };
           const int nch = cur.nch;
-          if (nch > 0) {
-            uint2 y = nch > 8 ? ld4(cur, 8 + hi4) : make_uint2(padw, padw);
-            for (int q = 0; q < nch; q += 8) {
-              const uint2 z = q + 16 < nch ? ld4(cur, q + 16 + hi4) : make_uint2(padw, padw);
-              uint2 o;
-              o.x = __shfl_xor_sync(0xffffffffu, x.x, 16);
-              o.y = __shfl_xor_sync(0xffffffffu, x.y, 16);
-              const uint2 wl = lane < 16 ? x : o, wh = lane < 16 ? o : x;   // chunks q..q+3, q+4..q+7
-              pair(wl.x);
-              if (q + 2 < nch) pair(wl.y);
-              if (q + 4 < nch) pair(wh.x);
-              if (q + 6 < nch) pair(wh.y);
-              x = y;
-              y = z;
+          if (nch == 0) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) { D0[j][e] = 0.f; D1[j][e] = 0.f; }
+          } else if (nch <= 4) {   // one round, ids 0..3 in every lane
+            pair(x.x, std::true_type{});
+            if (nch > 2) pair(x.y, std::false_type{});
+          } else {
+            const uint2 y0 = nch > 8 ? ld4(cur, 8 + hi4) : make_uint2(padw, padw);
+            uint2 o;
+            o.x = __shfl_xor_sync(0xffffffffu, x.x, 16);
+            o.y = __shfl_xor_sync(0xffffffffu, x.y, 16);
+            {
+              const uint2 wl = lane < 16 ? x : o, wh = lane < 16 ? o : x;   // chunks 0..3, 4..7
+              pair(wl.x, std::true_type{});
+              pair(wl.y, std::false_type{});   // (nch > 4)
+              pair(wh.x, std::false_type{});
+              if (nch > 6) pair(wh.y, std::false_type{});
+            }
+            if (nch > 8) {   // long rows: ids two rounds ahead
+              x = y0;
+              uint2 y = nch > 16 ? ld4(cur, 16 + hi4) : make_uint2(padw, padw);
+              for (int q = 8; q < nch; q += 8) {
+                const uint2 z = q + 16 < nch ? ld4(cur, q + 16 + hi4) : make_uint2(padw, padw);
+                o.x = __shfl_xor_sync(0xffffffffu, x.x, 16);
+                o.y = __shfl_xor_sync(0xffffffffu, x.y, 16);
+                const uint2 wl = lane < 16 ? x : o, wh = lane < 16 ? o : x;   // chunks q..q+3, q+4..q+7
+                pair(wl.x, std::false_type{});
+                if (q + 2 < nch) pair(wl.y, std::false_type{});
+                if (q + 4 < nch) pair(wh.x, std::false_type{});
+                if (q + 6 < nch) pair(wh.y, std::false_type{});
+                x = y;
+                y = z;
+              }
             }
           }
           float sv[2][6];
@@ -970,7 +1011,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           const int r0 = __shfl_sync(0xffffffffu, cur.rk, g), r1 = __shfl_sync(0xffffffffu, cur.rk, g + 8);
           Meta nm;   // the next item's rows and first ids, in flight during the GRU
           meta(next, nm);
-          const uint2 nx = nm.nch > 0 ? ld4(nm, hi4) : make_uint2(padw, padw);
+          const uint2 nx = ld_first(nm);
           float h[2][6], hn[2][6];
           load_h(r0, h[0]);
           load_h(r1, h[1]);

@@ -54,11 +54,17 @@ def main():
                             pocket=(pocket1.xyz, pocket1.elem, pocket1.role, np.array([0, 1000])),
                             pose_target=lib1.target)
     got = dm.score_poses(b, prec)["scores"].cpu().numpy()
+    ref = os.path.join(ROOT, "gpurun_out", f"gnn_ab_scores_{prec}.npy")   # the first variant run in this box
+    same = None
+    if os.path.exists(ref):
+        same = bool(np.array_equal(np.load(ref), got))
+    else:
+        np.save(ref, got)
     st = bench._rel_stats(got, want)
     top, wtop = bench._topk_idx(got, 100), bench._topk_idx(want, 100)
     st["top100_overlap"] = len(set(top.tolist()) & set(wtop.tolist())) / 100
     st["top10_equal"] = bool(np.array_equal(top[:10], wtop[:10]))
-    print(json.dumps({"var": mode, "prec": prec, "gnn_ms_16384": min(tg), "all": tg, **st}))
+    print(json.dumps({"var": mode, "prec": prec, "gnn_ms_16384": min(tg), "bitwise_equal_first": same, "all": tg, **st}))
 
 
 if __name__ == "__main__":
