@@ -925,11 +925,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           ++prof_items;
           const long long prof_t0 = clock64();
 #endif
+          // claim the next item; its index is read (shuffled) only after the
+          // gather, so the atomic's round trip overlaps it
           int next = 0;
           if (lane == 0) next = atomicAdd(ctr, 1) + kMmaWarps;
-          next = __shfl_sync(0xffffffffu, next, 0);
 #ifdef FS_GNN_PROF
-          const long long prof_t1 = clock64() + (next == -7 ? 1 : 0);
+          const long long prof_t1 = clock64();
           prof_claim += prof_t1 - prof_t0;
 #endif
           float D0[3][4], D1[3][4];
@@ -1009,6 +1010,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           prof_gather += prof_t2 - prof_t1;
 #endif
           const int r0 = __shfl_sync(0xffffffffu, cur.rk, g), r1 = __shfl_sync(0xffffffffu, cur.rk, g + 8);
+          next = __shfl_sync(0xffffffffu, next, 0);
           Meta nm;   // the next item's rows and first ids, in flight during the GRU
           meta(next, nm);
           const uint2 nx = ld_first(nm);
