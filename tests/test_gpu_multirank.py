@@ -8,6 +8,7 @@ import os
 import socket
 import subprocess
 import sys
+import tempfile
 
 import pytest
 
@@ -28,10 +29,15 @@ def _run(world, compounds):
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(HERE, "_nccl_worker.py")]
-    env = dict(os.environ, FS_TEST_COMPOUNDS=str(compounds), NCCL_DEBUG_FILE="/dev/stderr")
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
-    assert r.returncode == 0, r.stderr[-3000:]
-    res = [json.loads(line[len("RESULT "):]) for line in r.stdout.splitlines() if line.startswith("RESULT ")]
+    with tempfile.TemporaryDirectory() as out:
+        # one result file per rank (the ranks' stdout lines can interleave)
+        env = dict(os.environ, FS_TEST_COMPOUNDS=str(compounds), FS_TEST_OUT=out, NCCL_DEBUG_FILE="/dev/stderr")
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res = []
+        for f in sorted(os.listdir(out)):
+            with open(os.path.join(out, f)) as fh:
+                res.append(json.load(fh))
     assert len(res) == world
     return sorted(res, key=lambda x: x["rank"])
 
