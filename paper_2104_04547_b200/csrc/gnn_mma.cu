@@ -1249,7 +1249,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   __syncthreads();
   const uint32_t* g_hi = gsrc;
   const uint32_t* g_lo = gsrc + kGatherWords / 2;
-  for (int tile = warp; tile < ntiles; tile += kMmaWarps) {
+  // items = (tile, column half): 2 x ntiles items spread the pool over the
+  // warps in finer rounds (ntiles is ~4 x the warp count: whole-tile items
+  // left a round with one busy warp)
+  for (int pit = warp; pit < 2 * ntiles; pit += kMmaWarps) {
+    const int tile = pit >> 1, half = pit & 1;
     float h[2][6];
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr) {
@@ -1280,6 +1284,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     constexpr bool FULL = decltype(full)::value;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
+      if ((j >> 3) != half) continue;   // this item's 8 column groups
       // biases enter as the first MMA's C operand
       float Dg[4], Dv[4];
       {
