@@ -595,7 +595,7 @@ static SideStream* side_stream() {
   // memory for one radius-graph CTA per SM (measured 43.7 -> 42.8 ms/step)
   static const int env_mode = getenv("FS_OVERLAP") ? atoi(getenv("FS_OVERLAP")) : 2;
   const int mode = g_overlap_mode >= 0 ? g_overlap_mode : env_mode;
-  if (mode != 1 && mode != 2) return nullptr;
+  if (mode < 1 || mode > 3) return nullptr;
   static thread_local std::map<int, SideStream> streams;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
@@ -604,7 +604,7 @@ static SideStream* side_stream() {
   if (!ss.s) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, mode == 2 ? hi : lo) != cudaSuccess ||
+    if (cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, mode >= 2 ? hi : lo) != cudaSuccess ||
         cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
       ss = SideStream{};
@@ -1027,6 +1027,9 @@ int fs_score_poses(const fs_model* m, int precision, const fs_pose_batch* b, int
     if (ss->mode == 2) {
       if ((rc = voxel_branch(ss->s))) return rc;
       if ((rc = graph_branch(st))) return rc;
+    } else if (ss->mode == 3) {   // graph branch on the high-priority side stream, issued first
+      if ((rc = graph_branch(ss->s))) return rc;
+      if ((rc = voxel_branch(st))) return rc;
     } else {
       if ((rc = graph_branch(ss->s))) return rc;
       if ((rc = voxel_branch(st))) return rc;

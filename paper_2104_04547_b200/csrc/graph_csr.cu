@@ -33,9 +33,12 @@ struct GraphCsrArgs {
   int c_elem; double box;
 };
 
+#ifndef FS_CELLS_AXIS
+#define FS_CELLS_AXIS 9
+#endif
 constexpr int kCsrThreads = 256;
 constexpr int kCsrWarps = kCsrThreads / 32;
-constexpr int kCellsAxis = 9;           // cells grow past t_cov for boxes > 9*t_cov
+constexpr int kCellsAxis = FS_CELLS_AXIS;   // cells grow past t_cov for boxes > kCellsAxis * t_cov
 constexpr int kMaskWords = 2;         // bipartite bitmask path for |S| <= 64
 constexpr int kCovBits = 96;          // covalent candidates per row whose hit bits are kept
 constexpr int kCovWords = kCovBits / 32;
