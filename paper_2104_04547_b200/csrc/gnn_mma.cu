@@ -1473,6 +1473,11 @@ constexpr int kSplit2Warps = FS_GNN_WARPS;
 #else
 constexpr int kSplit2Warps = 16;
 #endif
+#ifdef FS_GNN_WARPS3
+constexpr int kSplit3Warps = FS_GNN_WARPS3;
+#else
+constexpr int kSplit3Warps = 20;
+#endif
 #ifdef FS_GNN_VAR
 constexpr int kSplit2Var = FS_GNN_VAR;   // A/B builds (build_native FS_BUILD_TAG / FS_EXTRA_FLAGS)
 #else
@@ -1494,8 +1499,8 @@ int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes
     return launch_gnn_mma_t<2, false, kSplit2Warps, kSplit2Var>(a, n_poses, smem, st);
   }
   if (split != 3) return FS_EINVAL;
-  if (a.fact_cnt) return launch_gnn_mma_t<3, true, 20>(a, n_poses, smem, st);
-  return launch_gnn_mma_t<3, false, 20>(a, n_poses, smem, st);
+  if (a.fact_cnt) return launch_gnn_mma_t<3, true, kSplit3Warps>(a, n_poses, smem, st);
+  return launch_gnn_mma_t<3, false, kSplit3Warps>(a, n_poses, smem, st);
 }
 
 }  // namespace fs
