@@ -625,7 +625,11 @@ static int launch_layer(const void* in, ConvParams prm, cudaStream_t st, const v
   const int units = (prm.n_poses + L::POSES - 1) / L::POSES;
   static const bool one_per_sm = getenv("FS_UMMA_ONE_CTA_PER_SM") != nullptr;
   const int per_sm = (!one_per_sm && L::TMEM_COLS <= 256 && (227 * 1024) / (L::SMEM + 1024) >= 2) ? 2 : 1;
-  const int ctas = max(1, min(units, g_num_sms * per_sm / L::NSPLIT));
+  // FS_CONV_SMS (A/B): cap the persistent grid below the SM count, leaving
+  // SMs to a concurrently running graph branch
+  static const int conv_sms = getenv("FS_CONV_SMS") ? atoi(getenv("FS_CONV_SMS")) : 0;
+  const int sms = conv_sms > 0 && conv_sms < g_num_sms ? conv_sms : g_num_sms;
+  const int ctas = max(1, min(units, sms * per_sm / L::NSPLIT));
   dim3 grid(ctas, L::NSPLIT);
   conv_umma_kernel<L><<<grid, 192, L::SMEM, st>>>(map, map_lo, prm);
   FS_LAUNCH_CHECK();
