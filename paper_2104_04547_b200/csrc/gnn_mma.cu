@@ -784,8 +784,21 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     // Where a row lands never changes its result (its sum has a fixed order,
     // its GRU row is independent of the tile's other rows).
     constexpr int TOPB = NB - 1;   // bin of degree d: TOPB - min(d, TOPB)
+    // NAT: a thread's rows (degree, CSR offset) stay in registers from the
+    // count to the placement pass (one global round trip per phase)
+    constexpr int kKeep = 3;
+    const int64_t row0 = n > 0 ? rows[base] : 0;   // the pose's first CSR entry
+    int kd[kKeep];
+    uint32_t ko[kKeep];
+#pragma unroll
+    for (int k = 0; k < kKeep; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      kd[k] = NAT && i < n ? degs[base + i] : 0;
+      ko[k] = NAT && i < n ? static_cast<uint32_t>(rows[base + i] - row0) : 0u;
+    }
     for (int i = threadIdx.x; i < prow; i += blockDim.x) {
-      const int d = i < n ? degs[base + i] : 0;
+      const int k = (i - static_cast<int>(threadIdx.x)) / static_cast<int>(blockDim.x);
+      const int d = NAT && k < kKeep ? (k == 0 ? kd[0] : k == 1 ? kd[1] : kd[2]) : (i < n ? degs[base + i] : 0);
       atomicAdd(&hst[TOPB - min(d, TOPB)], 1);
     }
     __syncthreads();
@@ -832,15 +845,17 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
         __syncthreads();
       }
     }
-    const int64_t row0 = n > 0 ? rows[base] : 0;   // the pose's first CSR entry
     const col_t* cbase = colv + row0;
     for (int i = threadIdx.x; i < prow; i += blockDim.x) {
-      const int d = i < n ? degs[base + i] : 0;
+      const int k = (i - static_cast<int>(threadIdx.x)) / static_cast<int>(blockDim.x);
+      const bool kept = NAT && k < kKeep;
+      const int d = kept ? (k == 0 ? kd[0] : k == 1 ? kd[1] : kd[2]) : (i < n ? degs[base + i] : 0);
       if (NAT || d < kHeavyDeg) {
         const int pos = atomicAdd(&hst[NB + TOPB - min(d, TOPB)], 1);
         PERM[pos] = static_cast<uint16_t>(i);
         if constexpr (NAT) {
-          SOFF[pos] = i < n ? static_cast<uint32_t>(rows[base + i] - row0) : 0u;
+          SOFF[pos] = kept ? (k == 0 ? ko[0] : k == 1 ? ko[1] : ko[2])
+                           : (i < n ? static_cast<uint32_t>(rows[base + i] - row0) : 0u);
           SDEG[pos] = static_cast<uint16_t>(d);
         }
       }
