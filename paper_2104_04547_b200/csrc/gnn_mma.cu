@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
           float th;
-          if constexpr ((VAR & 8) != 0) asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(v[rr][c]));
+          if constexpr ((VAR & (8 | 128)) != 0) asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(v[rr][c]));
           else th = fs_tanh(v[rr][c]);
           v[rr][c] = emb ? th : 0.f;
         }
@@ -1478,7 +1478,12 @@ static int launch_gnn_mma_t(const GnnMmaArgs& a, int n_poses, size_t smem, cudaS
   return FS_OK;
 }
 
-// FS_PREC_BF16 (SPLIT 2) runs VAR 6: neighbour gathers from fp16 copies of
+// FS_PREC_BF16 (SPLIT 2) variant bits: 1 tanh.approx.f32 gates, 2 f16x2 gates,
+// 4 fp16 gather copies, 8 f16x2 pool + approximate embedding tanh, 16
+// tensor-core neighbour sums, 32 one-pass fp16 sums for |s| <= kSBig, 64 one-pass
+// r*h, 128 approximate (tanh.approx.f32) embedding tanh.  Shipped: 245 =
+// 1|4|16|32|64|128 (profiles/r02/gnn_variants.md).
+// Round-2 midpoint ran VAR 6: neighbour gathers from fp16 copies of
 // the node states (half the shared-memory bytes of the fp32 rows: 21.7 ->
 // 20.1 ms per 16,384 poses) and one tanh.approx.f16x2 per pair of gate
 // activations (-> 19.8 ms); config-1 score error vs the oracle 1.03e-3 max
@@ -1496,7 +1501,7 @@ constexpr int kSplit3Warps = 20;
 #ifdef FS_GNN_VAR
 constexpr int kSplit2Var = FS_GNN_VAR;   // A/B builds (build_native FS_BUILD_TAG / FS_EXTRA_FLAGS)
 #else
-constexpr int kSplit2Var = 117;
+constexpr int kSplit2Var = 245;
 #endif
 
 int launch_gnn_mma(const GnnMmaArgs& a_in, int split, int n_poses, int max_nodes, cudaStream_t st) {
