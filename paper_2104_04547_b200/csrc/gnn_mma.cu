@@ -998,17 +998,27 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             if (nch > 8) {   // long rows: ids two rounds ahead
               x = y0;
               uint2 y = nch > 16 ? ld4(cur, 16 + hi4) : make_uint2(padw, padw);
-              for (int q = 8; q < nch; q += 8) {
+              int q = 8;
+              for (; q + 8 <= nch; q += 8) {   // full rounds: four unconditional pairs
                 const uint2 z = q + 16 < nch ? ld4(cur, q + 16 + hi4) : make_uint2(padw, padw);
                 o.x = __shfl_xor_sync(0xffffffffu, x.x, 16);
                 o.y = __shfl_xor_sync(0xffffffffu, x.y, 16);
                 const uint2 wl = lane < 16 ? x : o, wh = lane < 16 ? o : x;   // chunks q..q+3, q+4..q+7
                 pair(wl.x, std::false_type{});
+                pair(wl.y, std::false_type{});
+                pair(wh.x, std::false_type{});
+                pair(wh.y, std::false_type{});
+                x = y;
+                y = z;
+              }
+              if (q < nch) {   // the last, partial round
+                o.x = __shfl_xor_sync(0xffffffffu, x.x, 16);
+                o.y = __shfl_xor_sync(0xffffffffu, x.y, 16);
+                const uint2 wl = lane < 16 ? x : o, wh = lane < 16 ? o : x;
+                pair(wl.x, std::false_type{});
                 if (q + 2 < nch) pair(wl.y, std::false_type{});
                 if (q + 4 < nch) pair(wh.x, std::false_type{});
                 if (q + 6 < nch) pair(wh.y, std::false_type{});
-                x = y;
-                y = z;
               }
             }
           }
