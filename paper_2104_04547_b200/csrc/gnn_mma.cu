@@ -227,6 +227,10 @@ constexpr int kBins = kHeavyDeg + 1;
 // (degrees 0..kNatBins-2, the rest in one bin) keeps tile padding low
 // (NAT: hist + cursors live in the unused heavy-sum buffer)
 constexpr int kNatBins = 129;
+#ifndef FS_POOL_SPLIT
+#define FS_POOL_SPLIT 4
+#endif
+constexpr int kPoolSplit = FS_POOL_SPLIT;   // pool items per 16-row tile (column groups split evenly)
 // VAR & 32: a row's neighbour sums take one fp16 pass (its lo term zeroed)
 // while all its |s| <= kSBig: rounding <= kSBig * 2^-12 absolute, the order
 // of the fp16-rounded rows they sum; larger sums keep the hi/lo split.
@@ -1274,11 +1278,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
   __syncthreads();
   const uint32_t* g_hi = gsrc;
   const uint32_t* g_lo = gsrc + kGatherWords / 2;
-  // items = (tile, column half): 2 x ntiles items spread the pool over the
+  // items = (tile, column quarter): 4 x ntiles items spread the pool over the
   // warps in finer rounds (ntiles is ~4 x the warp count: whole-tile items
   // left a round with one busy warp)
-  for (int pit = warp; pit < 2 * ntiles; pit += kMmaWarps) {
-    const int tile = pit >> 1, half = pit & 1;
+  for (int pit = warp; pit < kPoolSplit * ntiles; pit += kMmaWarps) {
+    const int tile = pit / kPoolSplit, half = pit % kPoolSplit;
     float h[2][6];
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr) {
@@ -1309,7 +1313,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
     constexpr bool FULL = decltype(full)::value;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      if ((j >> 3) != half) continue;   // this item's 8 column groups
+      if (j / (16 / kPoolSplit) != half) continue;   // this item's column groups
       // biases enter as the first MMA's C operand
       float Dg[4], Dv[4];
       {
