@@ -939,6 +939,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           return ld4(m, m.nch > 4 ? hi4 : 0);
         };
         uint2 x = ld_first(cur);
+        // long rows: their second 8-chunk round, fetched with the first
+        uint2 x2 = cur.nch > 8 ? ld4(cur, 8 + hi4) : make_uint2(padw, padw);
         for (int item = warp; item < nitems;) {
 #ifdef FS_GNN_PROF
           ++prof_items;
@@ -988,7 +990,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             pair(x.x, std::true_type{});
             if (nch > 2) pair(x.y, std::false_type{});
           } else {
-            const uint2 y0 = nch > 8 ? ld4(cur, 8 + hi4) : make_uint2(padw, padw);
+            const uint2 y0 = x2;
             uint2 o;
             o.x = __shfl_xor_sync(0xffffffffu, x.x, 16);
             o.y = __shfl_xor_sync(0xffffffffu, x.y, 16);
@@ -1043,6 +1045,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           Meta nm;   // the next item's rows and first ids, in flight during the GRU
           meta(next, nm);
           const uint2 nx = ld_first(nm);
+          const uint2 nx2 = nm.nch > 8 ? ld4(nm, 8 + hi4) : make_uint2(padw, padw);
           float h[2][6], hn[2][6];
           load_h(r0, h[0]);
           load_h(r1, h[1]);
@@ -1078,6 +1081,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
 #endif
           cur = nm;
           x = nx;
+          x2 = nx2;
           item = next;
         }
         };
