@@ -1058,12 +1058,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
             float m0 = 0.f, m1 = 0.f;
 #pragma unroll
             for (int c = 0; c < 6; ++c) { m0 = fmaxf(m0, fabsf(sv[0][c])); m1 = fmaxf(m1, fabsf(sv[1][c])); }
-            m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
-            m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
-            m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
-            m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
-            const bool b0 = m0 > kSBig, b1 = m1 > kSBig;
-            if (__any_sync(0xffffffffu, b0 || b1)) {
+            // a row's 24 sums sit in its 4 lanes (bits 4g..4g+3 of a ballot)
+            const unsigned q0 = __ballot_sync(0xffffffffu, m0 > kSBig), q1 = __ballot_sync(0xffffffffu, m1 > kSBig);
+            const bool b0 = (q0 >> (4 * g)) & 15u, b1 = (q1 >> (4 * g)) & 15u;
+            if (q0 | q1) {
 #ifdef FS_GNN_PROF
               ++prof_lo;
 #endif
