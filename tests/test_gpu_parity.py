@@ -227,6 +227,25 @@ def test_fused_pose_path_equals_featurized_path(pkg):
     assert _rel(fused, staged) < 1e-5
 
 
+def test_bf16_featurized_items_match_fused_path(pkg):
+    """The bf16 SG-CNN on caller CSR (predict_batch on reference-format items:
+    packed rows, the kernel's unpadded-id path) agrees with the fused bf16
+    path (padded device CSR, neighbours in stencil order) -- only the fp32
+    summation order of the neighbour sums differs -- and with the goldens at
+    the stated bf16 tolerance."""
+    cx, E, models, synth = pkg
+    z = load("model_golden.npz")
+    vcfg, gcfg = models.VoxelHeadConfig(), models.GraphHeadConfig()
+    model = models.FusionModel(vcfg, gcfg, models.table_coherent_fusion_config(), seed=0, precision="bf16")
+    cs, items = _reference_items(z, cx, models, vcfg, gcfg)
+    fused, err = model.score_complexes(cs)
+    assert not err.any()
+    staged, errors = model.predict_batch([(it.grid, it.graph) for it in items])
+    assert not errors
+    assert _rel(fused, staged) < 1e-4
+    assert _rel(staged, z["scores"]) < 3e-3
+
+
 def test_batch_partition_invariance_bitwise(pkg):
     """SPEC.md:275 asks 1e-10; per-pose kernels make it bitwise."""
     cx, E, models, synth = pkg
