@@ -593,7 +593,7 @@ def main():
     L = N.lib()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     bounds = [(min(n_rank, i * B), min(n_rank, (i + 1) * B)) for i in range(K)]
-    BMAX = 32768                       # poses per fs_score_poses call (workspace ~0.6 MB/pose)
+    BMAX = int(os.environ.get("FS_BENCH_BMAX", "32768"))   # poses per fs_score_poses call (workspace ~0.6 MB/pose)
     n_comp = c1 - c0
 
     # one set of stage events per fs_score_poses call (a step is one or more calls)
