@@ -4,9 +4,12 @@
 // Same math as gnn.cu (models.py:334-371): per step
 //   [z|r] = sigma([s|h] . [[Wmsg.Wz  Wmsg.Wr]; [Uz Ur]] + [bz|br])
 //   hh    = tanh ([s|r*h] . [[Wmsg.Wh]; [Uh]] + bh);   h <- h + z*(hh-h)
-// with s = sum of neighbour h rows.  Each step is two passes over shared
-// memory: (1) S = neighbour sums (degree-balanced work items, see kHeavyDeg),
-// (2) the GRU update of 16-node tiles on the tensor cores, in place.
+// with s = sum of neighbour h rows.  Each step walks 16-node tiles (rows
+// counting-sorted by degree): (1) S = the tile's neighbour sums -- on the
+// fp16 path (VAR & 16) as identity-A MMAs over ldmatrix.trans-loaded
+// neighbour rows (see "tensor-core neighbour sums"), on the 3-pass path as
+// per-lane fp32 gathers with whole-warp heavy rows (kHeavyDeg); (2) the GRU
+// update of the tile on the tensor cores.
 // The m16n8k16 fragment layouts line up so that each lane holds, for rows
 // g and g+8 (g = lane/4), exactly the columns {2t,2t+1,8+2t,9+2t,16+2t,17+2t}
 // (t = lane%4) of s, h, z, r, hh and h': the whole GRU update is lane-local
@@ -16,9 +19,12 @@
 // the activations into fp16 hi + lo (22 significant bits) against fp16
 // weights (2^-12 relative rounding): two passes, half the weight-fragment
 // shared-memory traffic of SPLIT = 3; SPLIT = 1 is a
-// single bf16 pass.  Node states stay fp32 in shared memory.
-// Determinism: every row's sum has a fixed order (CSR order, or for heavy
-// rows 8 CSR-strided partial sums in a fixed tree), fixed reduction trees,
+// single bf16 pass.  Node states stay fp32 in shared memory (the fp16 path
+// gathers from double-buffered fp16 copies).
+// Determinism: every row's sum has a fixed order that depends on its own CSR
+// list only (CSR order; even / odd chunk accumulators on the MMA path; for
+// heavy rows 8 CSR-strided partial sums in a fixed tree), a row's GEMM
+// precision choice is a function of the row alone, fixed reduction trees,
 // fixed pool order -> a pose's latent is bitwise independent of its batch.
 #include <cstdlib>
 #include <type_traits>
