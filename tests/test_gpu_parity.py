@@ -431,3 +431,36 @@ def test_dense_and_oversize_poses_vs_oracle(pkg, case):
         assert not out["err"].cpu().numpy().any()
         got = out["scores"].cpu().numpy().astype(np.float64)
         assert _rel(got, want) < tol, (case, precision, got, want)
+
+
+def test_odd_pose_shapes_tensor_core_paths_vs_oracle(pkg):
+    """Ragged shapes through the tensor-core SG-CNN and Conv3d (bf16 and
+    mixed) against the float64 oracle: single-atom and 2-atom complexes
+    (one 16-row tile, zero-degree rows, empty CSR rows), ligand-only poses (no
+    pocket), a tiny pocket, and tile-boundary sizes (15 / 16 / 17 / 33 nodes),
+    all in one batch."""
+    cx, E, models, synth = pkg
+    rng = np.random.default_rng(51)
+    sizes = [1, 2, 15, 16, 17, 33, 40]
+    pos, el, ro, off = [], [], [], [0]
+    for k in sizes:
+        c = rng.uniform(-3.0, 3.0, size=3)
+        pos.append(c + rng.normal(scale=1.2, size=(k, 3)))
+        el.append(rng.integers(0, 4, size=k))
+        ro.append(rng.integers(0, 2, size=k))
+        off.append(off[-1] + k)
+    xyz, elem, role = np.vstack(pos), np.concatenate(el), np.concatenate(ro)
+    b = E.batch_from_arrays(xyz, elem, role, np.array(off))
+    vcfg, gcfg, fcfg = VOXEL, GRAPH, COHERENT
+    model = models.FusionModel(models.VoxelHeadConfig(), models.GraphHeadConfig(),
+                               models.table_coherent_fusion_config(), seed=0)
+    dm = model.device_model()
+    params = orc.init_params(vcfg, gcfg, fcfg, 0)
+    want = np.array([orc.score_pose(params, (vcfg, gcfg, fcfg), xyz[off[p]:off[p + 1]],
+                                    elem[off[p]:off[p + 1]].astype(np.int64),
+                                    role[off[p]:off[p + 1]].astype(np.int64))["score"] for p in range(len(sizes))])
+    for precision, tol in (("mixed", 1e-3), ("bf16", 3e-3)):
+        out = dm.score_poses(b, precision)
+        assert not out["err"].cpu().numpy().any()
+        got = out["scores"].cpu().numpy().astype(np.float64)
+        assert _rel(got, want) < tol, (precision, got, want)
