@@ -319,6 +319,10 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   const float c_hi2 = prefilter ? ((float)a.tc + delta) * ((float)a.tc + delta) : INFINITY;
   const float n_lo2 = prefilter ? ((float)a.tn - delta) * ((float)a.tn - delta) : -1.0f;
   const float n_hi2 = prefilter ? ((float)a.tn + delta) * ((float)a.tn + delta) : INFINITY;
+  // covalent band as centre / half-width (a slightly wider band; without the
+  // prefilter every candidate is in it)
+  const float c_mid2 = prefilter ? 0.5f * (c_lo2 + c_hi2) : 0.0f;
+  const float c_half2 = prefilter ? 0.5f * (c_hi2 - c_lo2) * 1.0001f + 1e-6f : INFINITY;
   // 1: edge, 0: not, decided in fp32; inside the band the exact float64 predicate
   auto decide = [&](float d2f, float lo2, float hi2, double xi, double yi, double zi, int j, double t) -> bool {
     if (d2f > hi2) return false;
@@ -487,16 +491,21 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
           // settled exactly afterwards
           bool anyband = false;
           if (len <= 32) {
+            // hits shifted in from the top (bit k <- candidate qe-1-k..), one
+            // reversal after the loop; the band test as one distance to the
+            // band's middle (a superset of the band: the re-walk is exact)
             uint32_t r32 = 0u;
+            float bmin = INFINITY;
             for (int q = qb; q < qe; ++q) {
               const int j = cell_list[q];
               const float4 fj = pf[j];
               const float ddx = fi.x - fj.x, ddy = fi.y - fj.y, ddz = fi.z - fj.z;
               const float d2f = ddx * ddx + ddy * ddy + ddz * ddz;
-              r32 |= (uint32_t)(d2f <= c_lo2) << (q - qb);
-              anyband |= d2f > c_lo2 && d2f <= c_hi2;
+              r32 = (r32 >> 1) | (d2f <= c_lo2 ? 0x80000000u : 0u);
+              bmin = fminf(bmin, fabsf(d2f - c_mid2));
             }
-            rm = r32;
+            rm = len ? r32 >> (32 - len) : 0u;
+            anyband = bmin <= c_half2;
           } else {
             for (int q = qb; q < qe; ++q) {
               const int j = cell_list[q];
