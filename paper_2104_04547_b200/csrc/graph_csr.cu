@@ -52,6 +52,23 @@ __host__ __device__ inline size_t graph_csr_smem_bytes(int n) {
          (size_t)n * kCovWords * 4 + (size_t)(n + 31) / 32 * 4 + 16;
 }
 
+// 32x32 bit-matrix transpose across a warp: on return, bit j of lane l is
+// bit l of lane j's input (one row index bit swapped with one column index
+// bit per butterfly stage)
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  constexpr uint32_t kLow[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int s = 16 >> k;
+    const bool upper = lane & s;
+    const uint32_t keep = upper ? ~kLow[k] : kLow[k];
+    const uint32_t out = x & ~keep;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, upper ? out << s : out >> s, s);
+    x = (x & keep) | y;
+  }
+  return x;
+}
+
 // Exclusive scan of u16 counts c[0..n) into out[i] = base + prefix (int64,
 // global); returns the total.  Starts with a barrier.
 __device__ int block_scan_u16_to_global(const uint16_t* c, int n, int64_t* out, int64_t base, int* warp_tot) {
@@ -364,7 +381,9 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       const bool lv = lj < nL;
       const int j = lv ? Llist[lj] : 0;
       const float4 fj = pf[j];
-      uint32_t m0 = 0u, m1 = 0u;
+      // lane l keeps the chunk's ballot of S atom l (b0) / 32 + l (b1); one
+      // warp transpose per word turns them into the L rows' masks
+      uint32_t b0 = 0u, b1 = 0u;
       for (int si = 0; si < nS; ++si) {
         const int i = Slist[si];
         const float4 fi = pf[i];
@@ -374,11 +393,14 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
         if (d2f > n_hi2) hit = false;
         else if (d2f <= n_lo2) hit = lv;
         else hit = lv && exact_pair_slow(pv, i, j, rmax2, a.tn);
-        const uint32_t b = hit ? 1u : 0u;
-        const int c = __popc(__ballot_sync(0xffffffffu, hit));
-        if (si < 32) { m0 |= b << si; sacc0 += lane == si ? c : 0; }
-        else { m1 |= b << (si - 32); sacc1 += lane == si - 32 ? c : 0; }
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (si < 32) b0 = lane == si ? bal : b0;
+        else b1 = lane == si - 32 ? bal : b1;
       }
+      sacc0 += __popc(b0);
+      sacc1 += __popc(b1);
+      const uint32_t m0 = warp_transpose32(b0, lane);
+      const uint32_t m1 = W > 1 ? warp_transpose32(b1, lane) : 0u;
       if (lv) {
         mask[lj * W] = m0;
         if (W > 1) mask[lj * W + 1] = m1;
@@ -577,22 +599,27 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   col_t* coln = a.col_ncov + cbase;
   double* distn = DIST ? a.dist_ncov + cbase : nullptr;
   if (use_mask) {
-    for (int si = warp; si < nS; si += kCsrWarps) {          // S rows: L ids ascending
-      const int i = Slist[si];
-      double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
-      int w = startn(i);
+    for (int w = warp; w < W; w += kCsrWarps) {   // S rows 32w + lane: L ids ascending
+      const int si = 32 * w + lane;
+      const bool sv = si < nS;
+      const int i = sv ? Slist[si] : 0;
+      double xi, yi, zi; int32_t ei_, ri_;
+      if (DIST && sv) pv.atom(i, xi, yi, zi, ei_, ri_);
+      int o = sv ? startn(i) : 0;
       for (int l0 = 0; l0 < nL; l0 += 32) {
+        // this chunk's mask words, transposed: lane l gets S atom 32w + l's
+        // hits among L atoms l0 .. l0 + 31
         const int lj = l0 + lane;
-        const bool hit = lj < nL && ((mask[lj * W + (si >> 5)] >> (si & 31)) & 1u);
-        const unsigned m = __ballot_sync(0xffffffffu, hit);
-        if (hit) {
-          const int o = w + __popc(m & ((1u << lane) - 1u));
-          const int j = Llist[lj];
+        uint32_t bits = warp_transpose32(lj < nL ? mask[lj * W + w] : 0u, lane);
+        while (bits) {
+          const int b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int j = Llist[l0 + b];
           FS_DCHECK(o < a.cap, "graph ncov S fill", o, a.cap);
           coln[o] = j;
           if (DIST) { double d; exact_edge(pv, xi, yi, zi, j, rmax2, a.tn, &d); distn[o] = d; }
+          ++o;
         }
-        w += __popc(m);
       }
     }
     for (int lj = threadIdx.x; lj < nL; lj += blockDim.x) {  // L rows: S ids ascending
