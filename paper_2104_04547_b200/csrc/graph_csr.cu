@@ -340,6 +340,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   // prefilter every candidate is in it)
   const float c_mid2 = prefilter ? 0.5f * (c_lo2 + c_hi2) : 0.0f;
   const float c_half2 = prefilter ? 0.5f * (c_hi2 - c_lo2) * 1.0001f + 1e-6f : INFINITY;
+  const float n_mid2 = prefilter ? 0.5f * (n_lo2 + n_hi2) : 0.0f;
+  const float n_half2 = prefilter ? 0.5f * (n_hi2 - n_lo2) * 1.0001f + 1e-6f : INFINITY;
   // 1: edge, 0: not, decided in fp32; inside the band the exact float64 predicate
   auto decide = [&](float d2f, float lo2, float hi2, double xi, double yi, double zi, int j, double t) -> bool {
     if (d2f > hi2) return false;
@@ -380,27 +382,48 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       const int lj = l0 + lane;
       const bool lv = lj < nL;
       const int j = lv ? Llist[lj] : 0;
-      const float4 fj = pf[j];
-      // lane l keeps the chunk's ballot of S atom l (b0) / 32 + l (b1); one
-      // warp transpose per word turns them into the L rows' masks
+      // idle lanes sit at infinity: never a hit, never in the band
+      const float4 fj = lv ? pf[j] : make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+      // lane l keeps the chunk's ballot of S atom l (b0) / 32 + l (b1) of the
+      // fp32-certain hits; one warp transpose per word turns them into the L
+      // rows' masks.  The band test is one distance to the band's middle (a
+      // superset); a lane that saw the band settles its row exactly below.
       uint32_t b0 = 0u, b1 = 0u;
-      for (int si = 0; si < nS; ++si) {
-        const int i = Slist[si];
-        const float4 fi = pf[i];
-        const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
-        const float d2f = dx * dx + dy * dy + dz * dz;
-        bool hit;
-        if (d2f > n_hi2) hit = false;
-        else if (d2f <= n_lo2) hit = lv;
-        else hit = lv && exact_pair_slow(pv, i, j, rmax2, a.tn);
-        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-        if (si < 32) b0 = lane == si ? bal : b0;
-        else b1 = lane == si - 32 ? bal : b1;
+      float bmin = INFINITY;
+      auto sweep = [&](int s0, int s1, uint32_t& bw) {
+#pragma unroll 4
+        for (int si = s0; si < s1; ++si) {
+          const float4 fi = pf[Slist[si]];
+          const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+          const float d2f = dx * dx + dy * dy + dz * dz;
+          bmin = fminf(bmin, fabsf(d2f - n_mid2));
+          const uint32_t bal = __ballot_sync(0xffffffffu, d2f <= n_lo2);
+          bw = lane == si - s0 ? bal : bw;
+        }
+      };
+      sweep(0, min(nS, 32), b0);
+      if (nS > 32) sweep(32, nS, b1);
+      uint32_t m0 = warp_transpose32(b0, lane);
+      uint32_t m1 = W > 1 ? warp_transpose32(b1, lane) : 0u;
+      const bool band = bmin <= n_half2;
+      if (__any_sync(0xffffffffu, band)) {   // rare: exact float64 predicate inside the band
+        if (band) {
+          for (int si = 0; si < nS; ++si) {
+            const int i = Slist[si];
+            const float4 fi = pf[i];
+            const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+            const float d2f = dx * dx + dy * dy + dz * dz;
+            if (lv && d2f > n_lo2 && d2f <= n_hi2 && exact_pair_slow(pv, i, j, rmax2, a.tn)) {
+              if (si < 32) m0 |= 1u << si;
+              else m1 |= 1u << (si - 32);
+            }
+          }
+        }
+        b0 = warp_transpose32(m0, lane);
+        if (W > 1) b1 = warp_transpose32(m1, lane);
       }
       sacc0 += __popc(b0);
       sacc1 += __popc(b1);
-      const uint32_t m0 = warp_transpose32(b0, lane);
-      const uint32_t m1 = W > 1 ? warp_transpose32(b1, lane) : 0u;
       if (lv) {
         mask[lj * W] = m0;
         if (W > 1) mask[lj * W + 1] = m1;
