@@ -889,6 +889,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
   const float c_hi2 = prefilter ? ((float)a.tc + delta) * ((float)a.tc + delta) : INFINITY;
   const float n_lo2 = prefilter ? ((float)a.tn - delta) * ((float)a.tn - delta) : -1.0f;
   const float n_hi2 = prefilter ? ((float)a.tn + delta) * ((float)a.tn + delta) : INFINITY;
+  const float n_mid2 = prefilter ? 0.5f * (n_lo2 + n_hi2) : 0.0f;
+  const float n_half2 = prefilter ? 0.5f * (n_hi2 - n_lo2) * 1.0001f + 1e-6f : INFINITY;
 
   // ---- non-covalent (ligand x pocket) bitmasks: lanes over pocket atoms,
   // loop over the ligand atoms (broadcast reads); each lane builds its pocket
@@ -898,27 +900,54 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
   __syncthreads();
   {
     int acc[kFactWords] = {0, 0, 0, 0};   // lane l: hits of ligand atoms 32w + l
+    const int nW = (nL + 31) / 32;
     for (int j0 = warp * 32; j0 < np; j0 += kCsrWarps * 32) {
       const int j = j0 + lane;
       const bool jv = j < np;
-      const float4 fj = pf[jv ? j : 0];
-      uint32_t m[kFactWords] = {0u, 0u, 0u, 0u};
+      // idle lanes sit at infinity: never a hit, never in the band
+      const float4 fj = jv ? pf[j] : make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+      // lane l keeps the ballot of ligand atom 32w + l (fp32-certain hits);
+      // warp transposes turn them into the pocket rows' masks; lanes that saw
+      // the band (one distance to its middle, a superset) settle exactly
+      uint32_t b[kFactWords] = {0u, 0u, 0u, 0u};
+      float bmin = INFINITY;
 #pragma unroll
       for (int w = 0; w < kFactWords; ++w) {
         const int s1 = min(nL, 32 * (w + 1));
+#pragma unroll 4
         for (int s = 32 * w; s < s1; ++s) {
           const float4 fi = lf[s];
           const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
           const float d2f = dx * dx + dy * dy + dz * dz;
-          bool hit;
-          if (d2f > n_hi2) hit = false;
-          else if (d2f <= n_lo2) hit = jv;
-          else hit = jv && exact_pair_slow(pv, np + s, j, rmax2, a.tn);
-          m[w] |= (hit ? 1u : 0u) << (s & 31);
-          const int c = __popc(__ballot_sync(0xffffffffu, hit));
-          acc[w] += lane == (s & 31) ? c : 0;
+          bmin = fminf(bmin, fabsf(d2f - n_mid2));
+          const uint32_t bal = __ballot_sync(0xffffffffu, d2f <= n_lo2);
+          b[w] = lane == s - 32 * w ? bal : b[w];
         }
       }
+      uint32_t m[kFactWords] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int w = 0; w < kFactWords; ++w)
+        if (w < nW) m[w] = warp_transpose32(b[w], lane);
+      const bool band = bmin <= n_half2;
+      if (__any_sync(0xffffffffu, band)) {   // rare: exact float64 predicate inside the band
+        if (band) {
+          for (int s = 0; s < nL; ++s) {
+            const float4 fi = lf[s];
+            const float dx = fi.x - fj.x, dy = fi.y - fj.y, dz = fi.z - fj.z;
+            const float d2f = dx * dx + dy * dy + dz * dz;
+            if (jv && d2f > n_lo2 && d2f <= n_hi2 && exact_pair_slow(pv, np + s, j, rmax2, a.tn)) {
+#pragma unroll
+              for (int w = 0; w < kFactWords; ++w)
+                if (s >> 5 == w) m[w] |= 1u << (s & 31);
+            }
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < kFactWords; ++w)
+          if (w < nW) b[w] = warp_transpose32(m[w], lane);
+      }
+#pragma unroll
+      for (int w = 0; w < kFactWords; ++w) acc[w] += __popc(b[w]);
       if (jv) {
 #pragma unroll
         for (int w = 0; w < kFactWords; ++w) mask[j * kFactWords + w] = m[w];
@@ -1010,17 +1039,22 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
       }
       o += __popc(m);
     }
-    o = offn[s];
+  }
+  // ligand rows' pocket neighbours: warp w takes ligand atoms 32w + lane; each
+  // 32-atom pocket chunk's mask words, transposed, are the lanes' hit bits
+  for (int w = warp; w < (nL + 31) / 32; w += kCsrWarps) {
+    const int s = 32 * w + lane;
+    int o = s < nL ? offn[s] : 0;
     for (int j0 = 0; j0 < np; j0 += 32) {
-      const int j = j0 + lane;
-      const bool hit = j < np && ((mask[j * kFactWords + (s >> 5)] >> (s & 31)) & 1u);
-      const unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (hit) {
-        FS_DCHECK(o + __popc(m & below) < a.cap, "coln lig", o + __popc(m & below), a.cap);
+      const int jl = j0 + lane;
+      uint32_t bits = warp_transpose32(jl < np ? mask[jl * kFactWords + w] : 0u, lane);
+      while (bits) {
+        const int j = j0 + __ffs(bits) - 1;
+        bits &= bits - 1;
+        FS_DCHECK(o < a.cap, "coln lig", o, a.cap);
         FS_DCHECK(nLp + rank[j] < nc, "coln val", nLp + rank[j], nc);
-        coln[o + __popc(m & below)] = nLp + rank[j];
+        coln[o++] = nLp + rank[j];
       }
-      o += __popc(m);
     }
   }
   // pocket rows: their ligand neighbours, ascending

@@ -1,7 +1,8 @@
 """Serial featurize-stage time (voxelizer + fused radius graph) per 16,384
 config-4 poses for an FS_LIB build, and a bitwise check of the scores
 against the default build's (the scoring-path CSR order is part of the
-result)."""
+result).  AB_CACHED=1: the pocket-factored path (fs_score_poses_cached),
+whole-call time."""
 import json
 import os
 import sys
@@ -27,6 +28,24 @@ def main():
     lib = bench.screen_library(0, 1640, seed=1).slice(0, 16384)
     pocket = synth.make_pocket(1000, seed=0)
     dlib = DeviceLibrary(lib, [pocket], torch.device("cuda", 0))
+    if os.environ.get("AB_CACHED") == "1":
+        cache = dm.prepare_pockets(dlib.pocket_xyz, dlib.pocket_elem, dlib.pocket_role, dlib.pocket_off)
+        call = lambda: dm.score_poses_cached(dlib.batch(0, 16384), cache, 32768, rescore=False)  # noqa: E731
+        out = call()
+        t = []
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            out = call()
+            e1.record()
+            torch.cuda.synchronize()
+            t.append(e0.elapsed_time(e1))
+        s = out["scores"].float().cpu().numpy()
+        ref = os.path.join(ROOT, "gpurun_out", "graph_ab_cached_scores.npy")
+        same = bool(np.array_equal(np.load(ref), s)) if os.path.exists(ref) else np.save(ref, s)
+        print(json.dumps({"var": sys.argv[1], "cached_ms_16384": min(t), "all": t, "scores_bitwise_equal_first": same}))
+        return
     evs = [torch.cuda.Event(enable_timing=True) for _ in N.STAGES]
     for e in evs:
         e.record()
