@@ -704,9 +704,14 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       // replay the count pass's hits: candidate index c of a stencil column
       // run maps to cell_list[qb + c - c0]; the row's own atom (a candidate
       // that always hits) is not emitted
+      // (a row that is not re-tested has < kCovBits candidates and <= 64 per
+      // column: each column's hits are one 64-bit window of the kept bits)
+      static_assert(kCovWords == 3, "covalent hit window assumes 96 kept bits");
       const int ri = (int)pf[i].w;
       const int kp = keys[i];
       const int cz = kp & 15, cy = (kp >> 4) & 15, cx = (kp >> 8) & 15;
+      const uint64_t blo = (uint64_t)bits[0] | ((uint64_t)bits[1] << 32);
+      const uint64_t bhi = bits[2];
       int c0 = 0;
       for (int dx = -1; dx <= 1; ++dx) {
         const int ax = cx + dx;
@@ -717,19 +722,17 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
           const int z0 = max(cz - 1, 0), z1 = min(cz + 1, nca - 1);
           const int k0 = ri * NC + (ax * nca + ay) * nca + z0, k1 = ri * NC + (ax * nca + ay) * nca + z1;
           const int qb = k0 == 0 ? 0 : cell_start[k0 - 1], qe = cell_start[k1];
-          const int cend = c0 + (qe - qb);
-          int c = c0;
-          while (c < cend) {
-            const uint32_t w = bits[c >> 5] >> (c & 31);
-            if (w == 0u) { c += 32 - (c & 31); continue; }
-            c += __ffs(w) - 1;
-            if (c >= cend) break;
-            const int j = cell_list[qb + (c - c0)];
+          const int len = qe - qb;
+          uint64_t cb = c0 >= 64 ? bhi >> (c0 - 64) : c0 == 0 ? blo : (blo >> c0) | (bhi << (64 - c0));
+          if (len < 64) cb &= (1ull << len) - 1ull;
+          while (cb) {
+            const int b = __ffsll((long long)cb) - 1;
+            cb &= cb - 1ull;
+            const int j = cell_list[qb + b];
             FS_DCHECK(o < a.cap, "graph cov fill", o, a.cap);
             if (j != i) colc[o++] = (col_t)j;
-            ++c;
           }
-          c0 = cend;
+          c0 += len;
         }
       }
       continue;
