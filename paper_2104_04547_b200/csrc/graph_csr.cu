@@ -452,31 +452,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     }
   }
 
-  // ---- covalent degrees: 27-cell stencil, one thread per row.  visit(j, c)
-  // sees every candidate j != i with its running candidate index c. ----
-  auto cov_cand = [&](int i, auto&& visit) {
-    const int ri = (int)pf[i].w;
-    const int kp = keys[i];
-    const int cz = kp & 15, cy = (kp >> 4) & 15, cx = (kp >> 8) & 15;
-    int c = 0;
-    for (int dx = -1; dx <= 1; ++dx) {
-      const int ax = cx + dx;
-      if (ax < 0 || ax >= nca) continue;
-      for (int dy = -1; dy <= 1; ++dy) {
-        const int ay = cy + dy;
-        if (ay < 0 || ay >= nca) continue;
-        const int z0 = max(cz - 1, 0), z1 = min(cz + 1, nca - 1);
-        const int k0 = ri * NC + (ax * nca + ay) * nca + z0, k1 = ri * NC + (ax * nca + ay) * nca + z1;
-        const int qb = k0 == 0 ? 0 : cell_start[k0 - 1], qe = cell_start[k1];
-        for (int q = qb; q < qe; ++q) {
-          const int j = cell_list[q];
-          if (j == i) continue;
-          visit(j, c++);
-        }
-      }
-    }
-    return c;
-  };
+  // ---- covalent degrees: 27-cell stencil, one thread per row ----
   auto cov_scan = [&](int i, auto&& emit) {
     double xi, yi, zi; int32_t ei_, ri_; pv.atom(i, xi, yi, zi, ei_, ri_);
     const float4 fi = pf[i];
