@@ -1,3 +1,4 @@
+# Single-B200 evidence run for profiles/r02 (gpurun): GPU tests, smoke, bench lines, launch list, step ncu capture.
 python -m pytest tests -m gpu -q > gpurun_out/final_pytest_gpu.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke.log 2>&1
 python bench.py > gpurun_out/final_bench_bf16.json 2> gpurun_out/final_bench_bf16.err
