@@ -371,9 +371,9 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   for (int i = threadIdx.x; i < (n + 31) / 32; i += blockDim.x) ovf[i] = 0u;
   if (use_mask) {
     // lanes over L atoms (32 per warp chunk), loop over the S atoms (broadcast
-    // shared reads): each lane builds its L row's hit mask in registers, no
-    // atomics on the mask; S-row counts accumulate per warp chunk.  Same fp32
-    // operands and order (S - L) as the fill, so the same decisions.
+    // shared reads): the chunk's per-S-atom ballots become the L rows' hit
+    // masks (no atomics on the mask); S-row counts accumulate per lane.  The
+    // masks are the only record of the decisions: both fills read them.
     int* s_ncnt = reinterpret_cast<int*>(red);   // [<= 64], red is free here
     if (threadIdx.x < 32 * kMaskWords) s_ncnt[threadIdx.x] = 0;
     __syncthreads();
@@ -873,8 +873,8 @@ __global__ void __launch_bounds__(kCsrThreads) graph_fact_kernel(GraphFactArgs a
 
   // ---- non-covalent (ligand x pocket) bitmasks: lanes over pocket atoms,
   // loop over the ligand atoms (broadcast reads); each lane builds its pocket
-  // row's mask in registers (no mask atomics), ligand-row counts accumulate
-  // per lane.  Same fp32 operands and order (ligand - pocket) as before. ----
+  // row's mask through ballots + warp transposes (no mask atomics),
+  // ligand-row counts accumulate per lane; both fills read the masks. ----
   for (int i = threadIdx.x; i < kFactMaxLig; i += blockDim.x) s_ncnt[i] = 0;
   __syncthreads();
   {
