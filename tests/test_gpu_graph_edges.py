@@ -218,6 +218,25 @@ def test_factored_scoring_graph_bitwise(pocket_atoms, lig):
     _compare(got, ne, nd, noff, "ncov")
 
 
+@pytest.mark.parametrize("shift", [0.0, 2048.0])
+def test_factored_scoring_graph_threshold_ulp_and_far_cases(shift):
+    """The factored graph's exact float64 settle: ligand atoms at t, t - 1 ulp
+    and t + 1 ulp from pocket / ligand atoms (the fp32 band), and the same
+    poses moved to |coords| >= 1024 A (prefilter off), bitwise."""
+    pk, lib = _ulp_poses(200, seed=11)
+    pk.xyz = pk.xyz + shift
+    lib.xyz = lib.xyz + shift
+    got = _gpu_entries(_pocket_batch(pk, lib), 32768, factored=True, max_pocket=len(pk.xyz))
+    assert not got["err"].any()
+    pos, roles, off = _full_arrays(pk, lib)
+    ce, cd, coff, ne, nd, noff = _oracle(pos, roles, off)
+    lig_only = (ce[:, 0] >= len(pk.xyz))
+    cp = np.repeat(np.arange(lib.n_poses), np.diff(coff))
+    coff2 = np.concatenate([[0], np.cumsum(np.bincount(cp[lig_only], minlength=lib.n_poses))])
+    _compare(got, ce[lig_only], cd[lig_only], coff2, "cov")
+    _compare(got, ne, nd, noff, "ncov")
+
+
 def test_factored_graph_flags_oversize_ligands():
     pk, lib = _screen_arrays(3, seed=3, pocket_atoms=300, ligand_atoms=(129, 140))
     got = _gpu_entries(_pocket_batch(pk, lib), 32768, factored=True, max_pocket=300)
