@@ -164,9 +164,9 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[33];
   __shared__ double s_min[3];
-  __shared__ int s_flags, s_role_cnt[2];
+  __shared__ int s_flags, s_n0;
   __shared__ int warp_tot[32];
-  __shared__ int warp_cnt[2][kCsrWarps];
+  __shared__ int warp_cnt[kCsrWarps];
 
   const int p = blockIdx.x;
   const PoseView pv = pose_view(a.b, p);
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       a.row_cov[base + i] = cbase; a.row_ncov[base + i] = cbase;
     }
   };
-  if (threadIdx.x == 0) { s_flags = 0; s_role_cnt[0] = 0; s_role_cnt[1] = 0; }
+  if (threadIdx.x == 0) s_flags = 0;
   if (n > a.smem_atoms) { fail(FS_ERR_TOO_LARGE); return; }
   const int SA = (a.smem_atoms + 3) & ~3;   // 16-byte aligned sub-arrays
   float4* pf = reinterpret_cast<float4*>(smem_raw);
@@ -223,21 +223,28 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     hi[0] = fmax(hi[0], x); hi[1] = fmax(hi[1], y); hi[2] = fmax(hi[2], z);
   }
   if (flags) atomicOr(&s_flags, flags);
+  // the six bounds in one block reduction (fmin / fmax are order-free),
+  // through the cell table (zeroed only after it)
   double ext_max = 0.0, absmax = 0.0;
-  for (int ax = 0; ax < 3; ++ax) {
-    double l = lo[ax], h = hi[ax];
-    for (int o = 16; o > 0; o >>= 1) {
-      l = fmin(l, __shfl_xor_sync(0xffffffffu, l, o));
-      h = fmax(h, __shfl_xor_sync(0xffffffffu, h, o));
+  {
+    double* rb = reinterpret_cast<double*>(cell_start);   // [6][kCsrWarps]
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      for (int o = 16; o > 0; o >>= 1) {
+        lo[ax] = fmin(lo[ax], __shfl_xor_sync(0xffffffffu, lo[ax], o));
+        hi[ax] = fmax(hi[ax], __shfl_xor_sync(0xffffffffu, hi[ax], o));
+      }
+      if (lane == 0) { rb[ax * kCsrWarps + warp] = lo[ax]; rb[(3 + ax) * kCsrWarps + warp] = hi[ax]; }
     }
     __syncthreads();
-    if (lane == 0) { red[warp] = l; red[16 + warp] = h; }
-    __syncthreads();
-    l = red[0]; h = red[16];
-    for (int w = 1; w < kCsrWarps; ++w) { l = fmin(l, red[w]); h = fmax(h, red[16 + w]); }
-    if (threadIdx.x == 0) s_min[ax] = l;
-    ext_max = fmax(ext_max, h - l);
-    absmax = fmax(absmax, fmax(fabs(l), fabs(h)));
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      double l = rb[ax * kCsrWarps], h = rb[(3 + ax) * kCsrWarps];
+      for (int w = 1; w < kCsrWarps; ++w) { l = fmin(l, rb[ax * kCsrWarps + w]); h = fmax(h, rb[(3 + ax) * kCsrWarps + w]); }
+      if (threadIdx.x == 0) s_min[ax] = l;
+      ext_max = fmax(ext_max, h - l);
+      absmax = fmax(absmax, fmax(fabs(l), fabs(h)));
+    }
   }
   __syncthreads();
   if (s_flags) { fail(s_flags); return; }
@@ -278,31 +285,28 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
     keys[i] = (uint16_t)(r << 12 | cx << 8 | cy << 4 | cz);
     atomicAdd(&cell_start[r * NC + (cx * nca + cy) * nca + cz], 1);
   }
+  // role lists: each thread takes a contiguous id range; one block scan of
+  // the role-0 counts places every id (roles are 0 / 1, validated above)
   {
-    int run[2] = {0, 0};
-    for (int t0 = 0; t0 < n; t0 += blockDim.x) {
-      const int i = t0 + threadIdx.x;
-      const int r = (i < n) ? (int)pf[i].w : -1;
-      const unsigned m0 = __ballot_sync(0xffffffffu, r == 0), m1 = __ballot_sync(0xffffffffu, r == 1);
-      if (lane == 0) { warp_cnt[0][warp] = __popc(m0); warp_cnt[1][warp] = __popc(m1); }
-      __syncthreads();
-      if (r >= 0) {
-        int pos = run[r] + __popc((r == 0 ? m0 : m1) & ((1u << lane) - 1u));
-        for (int w = 0; w < warp; ++w) pos += warp_cnt[r][w];
-        cell_list[i] = (uint16_t)pos;    // rank inside the role (cell_list is filled later)
-      }
-      for (int w = 0; w < kCsrWarps; ++w) { run[0] += warp_cnt[0][w]; run[1] += warp_cnt[1][w]; }
-      __syncthreads();
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int i0 = min(n, (int)threadIdx.x * per), i1 = min(n, i0 + per);
+    int c = 0;
+    for (int i = i0; i < i1; ++i) c += pf[i].w == 0.f;
+    int inc = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
     }
-    if (threadIdx.x == 0) { s_role_cnt[0] = run[0]; s_role_cnt[1] = run[1]; }
-  }
-  __syncthreads();
-  const int n0 = s_role_cnt[0];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int r = (int)pf[i].w, rk = cell_list[i];
-    role_list[(r == 0 ? 0 : n0) + rk] = (uint16_t)i;
+    if (lane == 31) warp_cnt[warp] = inc;
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < kCsrWarps; ++w) { const int v = warp_cnt[w]; before += w < warp ? v : 0; tot += v; }
+    if (threadIdx.x == 0) s_n0 = tot;
+    int p0 = before + inc - c, p1 = tot + i0 - p0;   // this range's first role-0 / role-1 slots
+    for (int i = i0; i < i1; ++i) role_list[pf[i].w == 0.f ? p0++ : p1++] = (uint16_t)i;
   }
   block_exclusive_scan(cell_start, 2 * NC, warp_tot);
+  const int n0 = s_n0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int kp = keys[i];
     const int slot = atomicAdd(&cell_start[(kp >> 12) * NC + (((kp >> 8) & 15) * nca + ((kp >> 4) & 15)) * nca +
