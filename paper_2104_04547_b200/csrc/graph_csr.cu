@@ -726,18 +726,19 @@ __global__ void __launch_bounds__(kCsrThreads) graph_csr_kernel(GraphCsrArgs a) 
       }
       ++o;
     });
-    if (!DIST) continue;
-    for (int x = rb + 1; x < o; ++x) {
-      const int v = colc[x];
-      const double dv = DIST ? distc[x] : 0.0;
-      int y = x - 1;
-      while (y >= rb && colc[y] > v) {
-        colc[y + 1] = colc[y];
-        if (DIST) distc[y + 1] = distc[y];
-        --y;
+    if constexpr (DIST) {   // featurizer path: ascending neighbour id
+      for (int x = rb + 1; x < o; ++x) {
+        const int v = colc[x];
+        const double dv = distc[x];
+        int y = x - 1;
+        while (y >= rb && colc[y] > v) {
+          colc[y + 1] = colc[y];
+          distc[y + 1] = distc[y];
+          --y;
+        }
+        colc[y + 1] = v;
+        distc[y + 1] = dv;
       }
-      colc[y + 1] = v;
-      if (DIST) distc[y + 1] = dv;
     }
   }
   if (!DIST) {
