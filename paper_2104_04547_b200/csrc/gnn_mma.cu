@@ -570,21 +570,21 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           hv[4 * k] = v.x; hv[4 * k + 1] = v.y; hv[4 * k + 2] = v.z; hv[4 * k + 3] = v.w;
         }
         store_nat16(Gc + i * 24, Gn + i * 24, hv);
-        continue;
-      }
+      } else {
 #pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        const float4 v = src[k];
-        reinterpret_cast<float4*>(Hc + i * 24)[k] = v;
-        if constexpr (G16) {
-          const __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
-          uint2 u;
-          u.x = *reinterpret_cast<const uint32_t*>(&lo);
-          u.y = *reinterpret_cast<const uint32_t*>(&hi);
-          reinterpret_cast<uint2*>(Gc + i * 24)[k] = u;
-          reinterpret_cast<uint2*>(Gn + i * 24)[k] = u;
-        } else {
-          reinterpret_cast<float4*>(Hn + i * 24)[k] = v;
+        for (int k = 0; k < 6; ++k) {
+          const float4 v = src[k];
+          reinterpret_cast<float4*>(Hc + i * 24)[k] = v;
+          if constexpr (G16) {
+            const __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
+            uint2 u;
+            u.x = *reinterpret_cast<const uint32_t*>(&lo);
+            u.y = *reinterpret_cast<const uint32_t*>(&hi);
+            reinterpret_cast<uint2*>(Gc + i * 24)[k] = u;
+            reinterpret_cast<uint2*>(Gn + i * 24)[k] = u;
+          } else {
+            reinterpret_cast<float4*>(Hn + i * 24)[k] = v;
+          }
         }
       }
       continue;
@@ -929,12 +929,15 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) gnn_mma_kernel(GnnMmaArgs a
           m.nch = __reduce_max_sync(0xffffffffu, m.dk);
         };
         auto ld4 = [&](const Meta& m, int q) -> uint2 {   // ids q..q+3 of the lane's row
-          if constexpr (PADDED) return q < m.ek ? __ldg(reinterpret_cast<const uint2*>(m.ck + q)) : make_uint2(padw, padw);
-          uint32_t j[4];
+          if constexpr (PADDED) {
+            return q < m.ek ? __ldg(reinterpret_cast<const uint2*>(m.ck + q)) : make_uint2(padw, padw);
+          } else {
+            uint32_t j[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            j[u] = q + u < m.ek ? static_cast<uint32_t>(__ldg(m.ck + q + u)) : static_cast<uint32_t>(npad);
-          return make_uint2(j[0] | (j[1] << 16), j[2] | (j[3] << 16));
+            for (int u = 0; u < 4; ++u)
+              j[u] = q + u < m.ek ? static_cast<uint32_t>(__ldg(m.ck + q + u)) : static_cast<uint32_t>(npad);
+            return make_uint2(j[0] | (j[1] << 16), j[2] | (j[3] << 16));
+          }
         };
         Meta cur;
         meta(warp, cur);
